@@ -1,0 +1,68 @@
+// Internal declarations shared by the libicv translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/icv.h"
+
+namespace icv {
+
+// ---- error plumbing --------------------------------------------------------
+void set_error(const std::string& msg);
+int fail(int status, const std::string& msg);
+int cuda_check(cudaError_t e, const char* what);
+void note_launch(int n = 1);
+
+// ---- geometry --------------------------------------------------------------
+struct Geom {
+  int R, S, SY, SX, DY, DX, PT, PL, PB, PR, C, K;
+  int64_t N, H, W;   // bound input extent
+  int64_t OH, OW;    // output extent
+  int RS() const { return R * S; }
+};
+// Validates desc/in and fills g (ICV_ERR_ARG / ICV_ERR_GEOMETRY on failure).
+int make_geom(const icv_conv_desc* d, const icv_shape4* in, Geom* g);
+
+// ---- kernel families ---------------------------------------------------------
+enum Family { kFamF32Exact = 0, kFamTcBf16 = 1, kFamTcU8 = 2, kFamCoreBf16 = 3, kFamCoreU8 = 4 };
+int family_for(int32_t dtype, int C);
+// Output-channel tile width of the tensor-core kernels for this problem.
+int tc_block_n(int family, int K);
+// Packed-filter layout (byte offsets inside the icv_pack_filter buffer).
+struct PackedLayout {
+  int family;
+  int block_n;        // tensor-core families
+  int n_pad;          // packed rows (output channels, zero padded)
+  int cblocks;        // 128-byte channel blocks per tap (tensor-core families)
+  int64_t row_bytes;  // bytes per packed output channel row
+  int64_t w_off, w_bytes, bias_off, bias_bytes, total;
+};
+int packed_layout(const icv_conv_desc* d, int32_t dtype, PackedLayout* L);
+
+// ---- kernels (launchers) ---------------------------------------------------
+int launch_ib_build(const Geom& g, int64_t batch, int32_t mr, int64_t first_tile, int32_t ib_dtype, void* ib,
+                    cudaStream_t st);
+int launch_pack(const Geom& g, const PackedLayout& L, int32_t w_dtype, const void* w, const void* bias,
+                const icv_quant* q, void* packed, cudaStream_t st);
+
+struct ConvArgs {
+  Geom g;
+  int64_t P;  // output pixels = batch * OH * OW
+  int32_t mr;
+  const void* x;
+  const void* zero_row;
+  const void* ib;
+  int32_t ib_is_i32;
+  const uint8_t* packed;
+  PackedLayout L;
+  void* y;
+  // uint8 requantization
+  int32_t zx, zw, zo, qmin, qmax, m0, shift;
+};
+int launch_conv_f32_exact(const ConvArgs& a, cudaStream_t st);
+int launch_conv_core(const ConvArgs& a, cudaStream_t st);       // bf16 / u8, any C (CUDA cores)
+int launch_conv_tc(const ConvArgs& a, cudaStream_t st);         // bf16 / u8 tcgen05
+
+}  // namespace icv

@@ -1,0 +1,363 @@
+// K2/K3/K6: the indirect-GEMM mainloop on sm_100a tensor cores.
+//
+// Replaces indirect_conv's hot loop (reference indirect.py:287-294) for
+// bf16 (tcgen05 kind::f16, fp32 accumulate) and uint8 (kind::i8, s32
+// accumulate) when pixel rows are 16-byte aligned.  GEMM view:
+// M = output pixels, N = output channels, K = R*S taps x C channels.
+//
+// Persistent, warp-specialised CTA (one per SM, 288 threads):
+//   warps 0-3  A producers.  Thread r owns row r of the 128-pixel M tile.
+//              Per tap e it reads that pixel's row reference from the
+//              indirection buffer (the paper's "load fresh row pointers per
+//              kernel element", Listing 3), resolves ZERO_REF to the bound
+//              zero row, and gathers the row's 128-byte channel block with
+//              eight 16-byte cp.async into the stage's A tile in the
+//              canonical 128B-swizzle K-major layout.  Completion is
+//              signalled on the stage's mbarrier (cp.async.mbarrier.arrive
+//              .noinc).  Thread 0 also issues the TMA load of the matching
+//              128-byte column block of the packed filter (B operand).
+//   warp 8     MMA issuer (one elected lane): 4 x tcgen05.mma (K = 32 bytes
+//              each) per stage into a TMEM accumulator; tcgen05.commit frees
+//              the smem stage and, after the last k-step, publishes the
+//              accumulator.  For uint8 a second N=16 MMA against an all-ones
+//              B tile accumulates the per-pixel input row sum needed by the
+//              zero-point correction.
+//   warps 4-7  epilogue: tcgen05.ld the accumulator (warp w reads TMEM lanes
+//              32*(w%4)..), add the folded bias / zero-point constants, cast
+//              to bf16 or requantize to uint8, store NHWC rows.  Two TMEM
+//              accumulator stages let the epilogue of tile i overlap the
+//              mainloop of tile i+1.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "icv_internal.h"
+#include "requant.cuh"
+#include "sm100_ptx.cuh"
+
+namespace icv {
+namespace {
+
+constexpr int kThreads = 288;
+constexpr int kBM = 128;
+constexpr int kABytes = kBM * 128;  // one 128-byte K block per row
+
+template <bool kI8, int BN>
+struct Cfg {
+  static constexpr int kBBytes = BN * 128;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStagesRaw = (192 * 1024) / kStageBytes;
+  static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
+  static constexpr int kOnesBytes = kI8 ? 16 * 128 : 0;
+  static constexpr int kAccStride = kI8 ? 2 * BN : BN;  // TMEM columns per accumulator stage
+  static constexpr int kTmemNeed = 2 * kAccStride;
+  static constexpr uint32_t kTmemCols = kTmemNeed <= 32 ? 32 : kTmemNeed <= 64 ? 64 : kTmemNeed <= 128 ? 128
+                                        : kTmemNeed <= 256 ? 256 : 512;
+  static constexpr int kBarBytes = 256;
+  static constexpr int kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + kOnesBytes + kBarBytes;
+  static_assert(kTmemNeed <= 512, "TMEM overflow");
+  static_assert(kSmemBytes <= 232448, "shared memory overflow");
+};
+
+struct TcArgs {
+  const uint8_t* x;
+  const uint8_t* zero_row;
+  const void* ib;
+  int32_t ib_is_i32;
+  int64_t mr, P;
+  int32_t RS, c_bytes, cblocks, elem_bytes, K, n_tiles;
+  int64_t total_tiles;
+  const void* bias;  // f32 (bf16) or int32 (u8) per padded output channel
+  void* y;
+  int32_t zw, zo, qmin, qmax, m0, shift;
+};
+
+__device__ __forceinline__ int64_t load_ref(const TcArgs& a, int64_t ent) {
+  if (a.ib_is_i32) return (int64_t)__ldg(static_cast<const int32_t*>(a.ib) + ent);
+  return __ldg(static_cast<const int64_t*>(a.ib) + ent);
+}
+
+template <bool kI8, int BN>
+__global__ void __launch_bounds__(kThreads, 1) igemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_b,
+                                                               const TcArgs a) {
+  using C = Cfg<kI8, BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + C::kStages * kABytes;
+  uint8_t* sOnes = sB + C::kStages * C::kBBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sOnes + C::kOnesBytes);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* tfull = empty + C::kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&full[s], 128 + 1);  // 128 producer cp.async arrivals + 1 expect_tx arrival
+      mbar_init(&empty[s], 1);       // tcgen05.commit
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);       // tcgen05.commit after the last k-step
+      mbar_init(&tempty[s], 128);    // every epilogue thread
+    }
+    fence_mbar_init();
+    tma_prefetch_desc(&tmap_b);
+  }
+  if constexpr (kI8) {
+    // all-ones B tile (16 rows x 128 bytes) for the per-pixel row-sum MMA
+    if (threadIdx.x >= 128 && threadIdx.x < 256) {
+      reinterpret_cast<uint4*>(sOnes)[threadIdx.x - 128] = make_uint4(0x01010101u, 0x01010101u, 0x01010101u,
+                                                                      0x01010101u);
+      fence_proxy_async_smem();
+    }
+  }
+  if (warp == 8) tmem_alloc<C::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int num_kb = a.RS * a.cblocks;
+  const uint32_t sA_u32 = smem_u32(sA);
+  const uint32_t sB_u32 = smem_u32(sB);
+
+  if (warp < 4) {
+    // ------------------------------------------------------------ producers
+    const int r = threadIdx.x;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
+      const int64_t mt = tile / a.n_tiles;
+      const int nt = (int)(tile - mt * a.n_tiles);
+      int64_t p = mt * kBM + r;
+      p = p < a.P ? p : a.P - 1;                       // clamped lane (indirect.py:111)
+      const int64_t ent0 = (p / a.mr) * a.RS * a.mr + p % a.mr;
+      int64_t off_next = load_ref(a, ent0);
+      for (int e = 0; e < a.RS; ++e) {
+        const int64_t off = off_next;
+        if (e + 1 < a.RS) off_next = load_ref(a, ent0 + (int64_t)(e + 1) * a.mr);   // prefetch next tap
+        const uint8_t* src = off < 0 ? a.zero_row : a.x + off * a.elem_bytes;     // ZERO_REF -> zero row
+        for (int cb = 0; cb < a.cblocks; ++cb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (r == 0) {
+            mbar_arrive_expect_tx(&full[stage], C::kBBytes);
+            tma_load_2d(sB_u32 + stage * C::kBBytes, &tmap_b, &full[stage], (e * a.cblocks + cb) * 128, nt * BN);
+          }
+          const uint32_t dst = sA_u32 + stage * kABytes + r * 128;
+          const int b0 = cb * 128;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int b = b0 + j * 16;
+            int valid = a.c_bytes - b;
+            valid = valid < 0 ? 0 : (valid > 16 ? 16 : valid);
+            cp_async_16(dst + ((j ^ (r & 7)) << 4), src + (valid ? b : 0), (uint32_t)valid);
+          }
+          cp_async_mbar_arrive_noinc(&full[stage]);
+          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 8) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc<kI8>(kBM, BN);
+      constexpr uint32_t idesc_ones = make_idesc<kI8>(kBM, 16);
+      const uint64_t ones_desc = sw128_kmajor_desc(smem_u32(sOnes));
+      int stage = 0;
+      uint32_t phase = 0;
+      int as = 0;
+      uint32_t aphase = 0;
+      for (int64_t tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
+        mbar_wait(&tempty[as], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + as * C::kAccStride;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tensor-core reads
+          const uint64_t adesc = sw128_kmajor_desc(sA_u32 + stage * kABytes);
+          const uint64_t bdesc = sw128_kmajor_desc(sB_u32 + stage * C::kBBytes);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {  // 4 x 32-byte K steps per 128-byte block
+            const uint32_t acc = (kb | k) != 0;
+            tc_mma<kI8>(d, adesc + 2 * k, bdesc + 2 * k, idesc, acc);
+            if constexpr (kI8) tc_mma<true>(d + BN, adesc + 2 * k, ones_desc + 2 * k, idesc_ones, acc);
+          }
+          tc_commit(&empty[stage]);
+          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(&tfull[as]);
+        if (++as == 2) { as = 0; aphase ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int slot = warp & 3;
+    const int row = slot * 32 + lane;
+    int as = 0;
+    uint32_t aphase = 0;
+    for (int64_t tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
+      const int64_t mt = tile / a.n_tiles;
+      const int nt = (int)(tile - mt * a.n_tiles);
+      mbar_wait(&tfull[as], aphase);
+      tc_fence_after();
+      const int64_t p = mt * kBM + row;
+      const uint32_t taddr = tmem_base + ((uint32_t)(slot * 32) << 16) + as * C::kAccStride;
+      int32_t rowsum = 0;
+      if constexpr (kI8) {
+        uint32_t rs;
+        tmem_ld_32x32b_x1(taddr + BN, rs);
+        tmem_ld_wait();
+        rowsum = (int32_t)rs;
+      }
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(taddr + c, v);
+        tmem_ld_wait();
+        const int n = nt * BN + c;
+        if (p < a.P && n < a.K) {
+          if constexpr (!kI8) {
+            const float* bias = static_cast<const float*>(a.bias) + n;
+            __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.y) + p * a.K + n;
+            if ((a.K & 7) == 0 && n + 32 <= a.K) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                uint32_t w4[4];
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                  const int i = q * 8 + h * 2;
+                  __nv_bfloat162 two = __floats2bfloat162_rn(__uint_as_float(v[i]) + bias[i],
+                                                             __uint_as_float(v[i + 1]) + bias[i + 1]);
+                  w4[h] = *reinterpret_cast<uint32_t*>(&two);
+                }
+                reinterpret_cast<uint4*>(out)[q] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                if (n + i < a.K) out[i] = __float2bfloat16_rn(__uint_as_float(v[i]) + bias[i]);
+            }
+          } else {
+            const int32_t* cst = static_cast<const int32_t*>(a.bias) + n;
+            uint8_t* out = static_cast<uint8_t*>(a.y) + p * a.K + n;
+            const long long corr = -(long long)a.zw * rowsum;
+            uint32_t packed[8];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const int32_t acc = (int32_t)((long long)(int32_t)v[i] + cst[i] + corr);
+              const uint32_t q8 = requant_u8(acc, a.m0, a.shift, a.zo, a.qmin, a.qmax);
+              if ((i & 3) == 0) packed[i >> 2] = q8;
+              else packed[i >> 2] |= q8 << (8 * (i & 3));
+            }
+            if ((a.K & 15) == 0 && n + 32 <= a.K) {
+              reinterpret_cast<uint4*>(out)[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+              reinterpret_cast<uint4*>(out)[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                if (n + i < a.K) out[i] = (uint8_t)(packed[i >> 2] >> (8 * (i & 3)));
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[as]);
+      if (++as == 2) { as = 0; aphase ^= 1; }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 8) {
+    tc_fence_after();
+    tmem_dealloc<C::kTmemCols>(tmem_base);
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+template <bool kI8, int BN>
+int launch_tc(const ConvArgs& c, cudaStream_t st) {
+  using Cf = Cfg<kI8, BN>;
+  auto kernel = igemm_tc_kernel<kI8, BN>;
+  static std::once_flag attr_once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(attr_once, [&] {
+    attr_err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::kSmemBytes);
+  });
+  if (attr_err != cudaSuccess) return cuda_check(attr_err, "cudaFuncSetAttribute(smem)");
+
+  auto encode = get_encode();
+  if (!encode) return fail(ICV_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  CUtensorMap tmap;
+  const cuuint64_t dims[2] = {(cuuint64_t)c.L.row_bytes, (cuuint64_t)c.L.n_pad};
+  const cuuint64_t strides[1] = {(cuuint64_t)c.L.row_bytes};
+  const cuuint32_t box[2] = {128, (cuuint32_t)BN};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult cr = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(c.packed + c.L.w_off), dims,
+                       strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return fail(ICV_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
+
+  TcArgs a;
+  a.x = static_cast<const uint8_t*>(c.x);
+  a.zero_row = static_cast<const uint8_t*>(c.zero_row);
+  a.ib = c.ib;
+  a.ib_is_i32 = c.ib_is_i32;
+  a.mr = c.mr;
+  a.P = c.P;
+  a.RS = c.g.RS();
+  a.elem_bytes = kI8 ? 1 : 2;
+  a.c_bytes = c.g.C * a.elem_bytes;
+  a.cblocks = c.L.cblocks;
+  a.K = c.g.K;
+  a.n_tiles = c.L.n_pad / BN;
+  const int64_t m_tiles = (c.P + kBM - 1) / kBM;
+  a.total_tiles = m_tiles * a.n_tiles;
+  a.bias = c.packed + c.L.bias_off;
+  a.y = c.y;
+  a.zw = c.zw; a.zo = c.zo; a.qmin = c.qmin; a.qmax = c.qmax; a.m0 = c.m0; a.shift = c.shift;
+
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)(a.total_tiles < sms ? a.total_tiles : sms);
+  kernel<<<grid, kThreads, Cf::kSmemBytes, st>>>(tmap, a);
+  note_launch();
+  return cuda_check(cudaGetLastError(), "igemm_tc launch");
+}
+
+}  // namespace
+
+int launch_conv_tc(const ConvArgs& c, cudaStream_t st) {
+  const int bn = c.L.block_n;
+  if (c.L.family == kFamTcBf16) {
+    if (bn == 64) return launch_tc<false, 64>(c, st);
+    if (bn == 128) return launch_tc<false, 128>(c, st);
+    if (bn == 256) return launch_tc<false, 256>(c, st);
+  } else if (c.L.family == kFamTcU8) {
+    if (bn == 64) return launch_tc<true, 64>(c, st);
+    if (bn == 128) return launch_tc<true, 128>(c, st);
+  }
+  return fail(ICV_ERR_UNSUPPORTED, "no tensor-core kernel for this tile width");
+}
+
+}  // namespace icv

@@ -1,0 +1,360 @@
+"""Parity of the CUDA path (through libicv.so's C ABI) with the oracle and
+with the reference-generated golden fixtures.  Runs on a B200 only.
+
+  * indirection buffer: bit-exact (int64 canonical form and int32)
+  * float32 convolution: bit-exact (reference arithmetic contract)
+  * bfloat16 convolution: rel 1e-2 vs the f32 oracle on bf16-rounded operands
+  * uint8 convolution: bit-exact vs the int64 oracle
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1907_02129_b200 as icv
+from conftest import P, make_params
+from helpers import assert_bf16_close, fill_uniform, sha
+from oracle import conv as oconv
+from oracle import ib as oib
+from oracle import quant as oq
+from paper_1907_02129_b200 import _lib as L
+from paper_1907_02129_b200.workloads import CFG1, CFG2, CFG3A, CFG3B, CFG4
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def to_params(d) -> icv.ConvParams:
+    return icv.ConvParams(**d)
+
+
+def dev_ib(params, shape, mr, batch=None, index_dtype=torch.int64, seed=0, dtype=torch.float32):
+    x = icv.tensor_fill_random(shape, seed, device=DEV, dtype=dtype)
+    zero = icv.make_zero_row(params.in_channels, dtype=dtype, device=DEV)
+    out_shape = icv.conv_output_shape(params, shape)
+    ib = icv.init_indirection_buffer(x, zero, params, out_shape, icv.TileConfig(mr=mr), batch=batch,
+                                     index_dtype=index_dtype)
+    return x, zero, out_shape, ib
+
+
+# --------------------------------------------------------------------- IB (K1)
+def test_ib_known_answers(golden):
+    for case in golden["ib_kat"]:
+        p = to_params(case["params"])
+        shape = icv.Shape4(*case["in_shape"])
+        _, _, _, ib = dev_ib(p, shape, case["mr"])
+        got = ib.offsets_host()
+        assert list(got.shape) == case["offsets_shape"], case["name"]
+        assert got.reshape(-1).tolist() == case["offsets"], case["name"]
+
+
+def test_ib_sweep_digests_int64_and_int32(golden):
+    for row in golden["ib_sweep"]:
+        p = to_params(row["params"])
+        shape = icv.Shape4(*row["in_shape"])
+        for mr, (oshape, digest) in row["mr"].items():
+            _, _, _, ib = dev_ib(p, shape, int(mr))
+            assert sha(ib.offsets_host().astype("<i8")) == digest, (row["i"], mr)
+            if mr == "4":
+                _, _, _, ib32 = dev_ib(p, shape, 4, index_dtype=torch.int32)
+                assert ib32.offsets.dtype == torch.int32
+                assert sha(ib32.offsets_host().astype("<i8")) == digest, (row["i"], "int32")
+        if "batch1_mr4" in row:
+            x, zero, out_shape, ib1 = dev_ib(p, shape, 4, batch=1)
+            assert sha(ib1.offsets_host().astype("<i8")) == row["batch1_mr4"][1]
+            grown = icv.update_for_batch_growth(ib1, 2)
+            assert sha(grown.offsets_host().astype("<i8")) == row["grown_mr4"]
+
+
+def test_ib_matches_oracle_at_full_config_sizes():
+    """Every BASELINE config, canonical int64 form, bit-exact (cfg3a's IB is
+    19.7 M entries at mr=128)."""
+    for w in (CFG1, CFG2, CFG3A, CFG3B, CFG4):
+        for mr in (4, 128):
+            x = icv.NhwcTensor.empty(w.in_shape, dtype=torch.uint8 if w.dtype == "u8" else torch.bfloat16,
+                                     device=DEV)
+            zero = icv.make_zero_row(w.in_shape.c, dtype=x.dtype, device=DEV)
+            out_shape = icv.conv_output_shape(w.params, w.in_shape)
+            ib = icv.init_indirection_buffer(x, zero, w.params, out_shape, icv.TileConfig(mr=mr))
+            oh, ow = w.out_hw
+            want = oib.compute_offsets(w.in_shape.astuple(), w.params, oh, ow, w.in_shape.n, mr)
+            assert np.array_equal(ib.offsets_host(), want), (w.name, mr)
+
+
+def test_ib_growth_preserves_prefix_on_device():
+    params = make_params(r=3, s=3, pt=1, pl=1, c=3, k=4)
+    phys = icv.tensor_fill_random(icv.Shape4(2, 3, 3, 3), seed=50, device=DEV)
+    zero = icv.make_zero_row(3, device=DEV)
+    out1 = icv.conv_output_shape(params, phys.shape)
+    ib1 = icv.init_indirection_buffer(phys, zero, params, out1, icv.TileConfig(), batch=1)
+    grown = icv.update_for_batch_growth(ib1, 2)
+    fresh = icv.init_indirection_buffer(phys, zero, params, out1, icv.TileConfig(), batch=2)
+    assert torch.equal(grown.offsets, fresh.offsets)
+    keep = ib1.pixel_count // 4
+    assert torch.equal(grown.offsets[:keep], ib1.offsets[:keep])
+    assert icv.update_for_batch_growth(grown, 2) is grown
+
+
+# ------------------------------------------------------------ float32 (K5)
+def run_f32(params, shape, seed_x, seed_w, bias, mr=4, nr=8):
+    tile = icv.TileConfig(mr=mr, nr=nr)
+    x = icv.NhwcTensor(shape, torch.from_numpy(fill_uniform(shape.numel, seed_x)).to(DEV))
+    filt = icv.filter_fill_random(params, seed_w, device=DEV)
+    zero = icv.make_zero_row(params.in_channels, device=DEV)
+    out_shape = icv.conv_output_shape(params, shape)
+    ib = icv.init_indirection_buffer(x, zero, params, out_shape, tile)
+    pf = icv.pack_filter(filt, None if bias is None else torch.from_numpy(bias), params, tile)
+    return icv.indirect_conv(x, pf, ib, params, tile).numpy()
+
+
+def test_f32_sweep_bit_exact(golden):
+    for row in golden["conv_sweep"]:
+        p = to_params(row["params"])
+        shape = icv.Shape4(*row["in_shape"])
+        i = row["i"]
+        bias = np.random.default_rng(i + 2).uniform(-1.0, 1.0, p.out_channels).astype(np.float32)
+        out = run_f32(p, shape, i, i + 1, bias)
+        assert sha(out.astype("<f4")) == row["out_sha"], (i, row["params"], row["in_shape"])
+
+
+@pytest.mark.parametrize("mr", [None, 1, 128])
+def test_f32_kat_bit_exact(golden, mr):
+    for row in golden["conv_kat"]:
+        p = to_params(row["params"])
+        shape = icv.Shape4(*row["in_shape"])
+        s = row["seed"]
+        bias = np.random.default_rng(s + 2).uniform(-1, 1, p.out_channels).astype(np.float32)
+        out = run_f32(p, shape, s, s + 1, bias, mr=row["mr"] if mr is None else mr, nr=row["nr"])
+        assert sha(out.astype("<f4")) == row["out_sha"], row["name"]
+
+
+def test_cfg1_bit_exact(golden):
+    w = CFG1
+    tile = icv.TileConfig()
+    x = icv.NhwcTensor(w.in_shape, torch.from_numpy(w.input_host()).to(DEV))
+    filt = icv.FilterTensor(64, 3, 3, 64, torch.from_numpy(w.filter_host()).to(DEV))
+    pf = icv.pack_filter(filt, torch.from_numpy(w.bias_host()), w.params, tile)
+    zero = icv.make_zero_row(64, device=DEV)
+    ib = icv.init_indirection_buffer(x, zero, w.params, icv.conv_output_shape(w.params, w.in_shape), tile)
+    assert sha(ib.offsets_host().astype("<i8")) == golden["cfg1"]["ib_mr4_sha"]
+    out = icv.indirect_conv(x, pf, ib, w.params, tile).numpy()
+    assert sha(out.astype("<f4")) == golden["cfg1"]["out_sha"]
+
+
+# ------------------------------------------------------------ bfloat16 (K2)
+def bf16_problem(w, n_img=None, mr=128, index_dtype=torch.int64):
+    n_img = w.in_shape.n if n_img is None else n_img
+    shape = icv.Shape4(n_img, w.in_shape.h, w.in_shape.w, w.in_shape.c)
+    xh = w.input_host(0, n_img)
+    wh = w.filter_host()
+    x = icv.NhwcTensor(shape, torch.from_numpy(xh).to(DEV).to(torch.bfloat16))
+    p = w.params
+    filt = icv.FilterTensor(p.out_channels, p.kernel_h, p.kernel_w, p.in_channels,
+                            torch.from_numpy(wh).to(DEV).to(torch.bfloat16))
+    tile = icv.TileConfig(mr=mr)
+    pf = icv.pack_filter(filt, None, p, tile)
+    zero = icv.make_zero_row(p.in_channels, dtype=torch.bfloat16, device=DEV)
+    ib = icv.init_indirection_buffer(x, zero, p, icv.conv_output_shape(p, shape), tile, index_dtype=index_dtype)
+    y = icv.indirect_conv(x, pf, ib, p, tile)
+    return shape, oconv.bf16_round(xh), oconv.bf16_round(wh), ib, y
+
+
+@pytest.mark.parametrize("w", [CFG2, CFG3A, CFG3B], ids=lambda w: w.name)
+def test_bf16_slice_vs_reference_golden(golden, w):
+    """N=1 slices whose f32-reference outputs are pinned in the fixtures."""
+    case = next(c for c in golden["bf16_slices"] if c["name"] == w.name)
+    shape, xr, wr, ib, y = bf16_problem(w, n_img=case["images"])
+    assert sha(xr.astype("<f4")) == case["x_bf16_sha"]
+    oh, ow = w.out_hw
+    ref = oconv.indirect_conv_f32(xr, np.zeros(shape.c, np.float32), ib.offsets_host(), w.params, wr, None,
+                                  shape.n, oh, ow)
+    assert sha(ref.astype("<f4")) == case["out_sha"]          # oracle == reference on these operands
+    assert_bf16_close(y.numpy().reshape(ref.shape), ref)
+
+
+@pytest.mark.parametrize("w", [CFG2, CFG3A, CFG3B], ids=lambda w: w.name)
+def test_bf16_full_config_sampled_pixels(w):
+    """Full BASELINE batch; the oracle is evaluated on 4096 seeded random
+    output pixels (rows are independent) plus the first and last pixel."""
+    shape, xr, wr, ib, y = bf16_problem(w)
+    oh, ow = w.out_hw
+    pixels = shape.n * oh * ow
+    idx = np.unique(np.concatenate([[0, pixels - 1], np.random.default_rng(7).integers(0, pixels, 4096)]))
+    ref = oconv.indirect_conv_f32(xr, np.zeros(shape.c, np.float32), ib.offsets_host(), w.params, wr, None,
+                                  shape.n, oh, ow, pixel_index=idx)
+    got = y.numpy().reshape(pixels, -1)[idx]
+    assert_bf16_close(got, ref)
+
+
+@pytest.mark.parametrize("geom", [
+    dict(r=3, s=3, pt=1, pl=1, c=64, k=64, n=2, h=9, w=11, mr=4),       # K=64 tile, tails
+    dict(r=3, s=3, pt=1, pl=1, c=72, k=200, n=1, h=13, w=7, mr=3),      # C % 64 != 0, K % BN != 0
+    dict(r=1, s=1, c=256, k=512, n=3, h=7, w=7, mr=128),                # pointwise, 2 N tiles
+    dict(r=3, s=2, sy=2, sx=1, dy=2, dx=1, pt=2, pl=1, pb=0, pr=2, c=16, k=40, n=2, h=10, w=9, mr=1),
+    dict(r=5, s=5, pt=2, pl=2, c=8, k=24, n=1, h=6, w=6, mr=4),         # C=8: single 16-byte chunk
+    dict(r=7, s=7, sy=2, sx=2, pt=3, pl=3, c=3, k=64, n=2, h=20, w=18, mr=4),   # channel-poor (CUDA cores)
+])
+@pytest.mark.parametrize("index_dtype", [torch.int64, torch.int32])
+def test_bf16_edge_geometries(geom, index_dtype):
+    g = dict(geom)
+    n, h, wd, mr = g.pop("n"), g.pop("h"), g.pop("w"), g.pop("mr")
+    p = make_params(**g)
+    shape = icv.Shape4(n, h, wd, p.in_channels)
+    rng = np.random.default_rng(3)
+    xh = rng.standard_normal(shape.numel, dtype=np.float32)
+    wh = rng.standard_normal(p.out_channels * p.kernel_elems * p.in_channels, dtype=np.float32)
+    bias = rng.standard_normal(p.out_channels, dtype=np.float32)
+    tile = icv.TileConfig(mr=mr)
+    x = icv.NhwcTensor(shape, torch.from_numpy(xh).to(DEV).to(torch.bfloat16))
+    filt = icv.FilterTensor(p.out_channels, p.kernel_h, p.kernel_w, p.in_channels, torch.from_numpy(wh).to(DEV))
+    pf = icv.pack_filter(filt, torch.from_numpy(bias), p, tile, compute_dtype=torch.bfloat16)
+    zero = icv.make_zero_row(p.in_channels, dtype=torch.bfloat16, device=DEV)
+    out_shape = icv.conv_output_shape(p, shape)
+    ib = icv.init_indirection_buffer(x, zero, p, out_shape, tile, index_dtype=index_dtype)
+    y = icv.indirect_conv(x, pf, ib, p, tile).numpy().reshape(-1, p.out_channels)
+    ref = oconv.indirect_conv_f32(oconv.bf16_round(xh), np.zeros(shape.c, np.float32), ib.offsets_host(), p,
+                                  oconv.bf16_round(wh), bias, n, out_shape.h, out_shape.w)
+    assert_bf16_close(y, ref)
+
+
+# --------------------------------------------------------------- uint8 (K3)
+def u8_problem(w, n_img=None, mr=4):
+    n_img = w.in_shape.n if n_img is None else n_img
+    shape = icv.Shape4(n_img, w.in_shape.h, w.in_shape.w, w.in_shape.c)
+    q = w.quant
+    qp = icv.QuantParams(q.input_zero_point, q.input_scale, q.kernel_zero_point, q.kernel_scale,
+                         q.output_zero_point, q.output_scale, q.output_min, q.output_max)
+    xh = w.input_host(0, n_img)
+    wh = w.filter_host()
+    bias = w.bias_host()
+    p = w.params
+    x = icv.NhwcTensor(shape, torch.from_numpy(xh).to(DEV))
+    filt = icv.FilterTensor(p.out_channels, p.kernel_h, p.kernel_w, p.in_channels, torch.from_numpy(wh).to(DEV))
+    tile = icv.TileConfig(mr=mr)
+    pf = icv.pack_filter(filt, torch.from_numpy(bias), p, tile, quant=qp)
+    zero = icv.make_zero_row(p.in_channels, dtype=torch.uint8, device=DEV, fill=q.input_zero_point)
+    ib = icv.init_indirection_buffer(x, zero, p, icv.conv_output_shape(p, shape), tile)
+    y = icv.indirect_conv(x, pf, ib, p, tile)
+    return shape, xh, wh, bias, zero.cpu().numpy(), ib, y
+
+
+def test_u8_cfg4_full_batch_bit_exact_sampled():
+    w = CFG4
+    q = w.quant
+    shape, xh, wh, bias, zero, ib, y = u8_problem(w)
+    oh, ow = w.out_hw
+    pixels = shape.n * oh * ow
+    idx = np.unique(np.concatenate([[0, pixels - 1], np.random.default_rng(8).integers(0, pixels, 3000)]))
+    ref = oq.indirect_conv_u8(xh, zero, ib.offsets_host(), w.params, wh, bias, shape.n, oh, ow,
+                              q.input_zero_point, q.input_scale, q.kernel_zero_point, q.kernel_scale,
+                              q.output_zero_point, q.output_scale, pixel_index=idx)
+    got = y.numpy().reshape(pixels, -1)[idx]
+    assert np.array_equal(got, ref), int((got != ref).sum())
+
+
+def test_u8_cfg4_slice_bit_exact_all_pixels():
+    w = CFG4
+    q = w.quant
+    shape, xh, wh, bias, zero, ib, y = u8_problem(w, n_img=2, mr=128)
+    oh, ow = w.out_hw
+    ref = oq.indirect_conv_u8(xh, zero, ib.offsets_host(), w.params, wh, bias, shape.n, oh, ow,
+                              q.input_zero_point, q.input_scale, q.kernel_zero_point, q.kernel_scale,
+                              q.output_zero_point, q.output_scale)
+    assert np.array_equal(y.numpy().reshape(ref.shape), ref)
+
+
+@pytest.mark.parametrize("geom", [
+    dict(r=3, s=3, pt=1, pl=1, c=16, k=24, n=2, h=7, w=9, mr=4, zx=3, zw=250),
+    dict(r=3, s=3, sy=2, sx=2, pt=1, pl=1, c=48, k=130, n=1, h=11, w=10, mr=1, zx=128, zw=127),
+    dict(r=1, s=1, c=128, k=64, n=2, h=5, w=5, mr=128, zx=0, zw=0),
+    dict(r=3, s=3, pt=1, pl=1, c=5, k=9, n=1, h=6, w=5, mr=4, zx=100, zw=7),     # C % 16 != 0 (CUDA cores)
+])
+def test_u8_edge_geometries(geom):
+    g = dict(geom)
+    n, h, wd, mr, zx, zw = (g.pop(k) for k in ("n", "h", "w", "mr", "zx", "zw"))
+    p = make_params(**g)
+    shape = icv.Shape4(n, h, wd, p.in_channels)
+    rng = np.random.default_rng(9)
+    xh = rng.integers(0, 256, shape.numel, dtype=np.uint8)
+    wh = rng.integers(0, 256, p.out_channels * p.kernel_elems * p.in_channels, dtype=np.uint8)
+    bias = rng.integers(-5000, 5000, p.out_channels, dtype=np.int32)
+    qp = icv.QuantParams(zx, 0.02, zw, 0.005, 128, 0.1)
+    tile = icv.TileConfig(mr=mr)
+    x = icv.NhwcTensor(shape, torch.from_numpy(xh).to(DEV))
+    filt = icv.FilterTensor(p.out_channels, p.kernel_h, p.kernel_w, p.in_channels, torch.from_numpy(wh).to(DEV))
+    pf = icv.pack_filter(filt, torch.from_numpy(bias), p, tile, quant=qp)
+    zero = icv.make_zero_row(p.in_channels, dtype=torch.uint8, device=DEV, fill=zx)
+    out_shape = icv.conv_output_shape(p, shape)
+    ib = icv.init_indirection_buffer(x, zero, p, out_shape, tile)
+    y = icv.indirect_conv(x, pf, ib, p, tile).numpy().reshape(-1, p.out_channels)
+    ref = oq.indirect_conv_u8(xh, zero.cpu().numpy(), ib.offsets_host(), p, wh, bias, n, out_shape.h,
+                              out_shape.w, zx, 0.02, zw, 0.005, 128, 0.1)
+    assert np.array_equal(y, ref), int((y != ref).sum())
+
+
+def test_requant_params_native_equals_oracle():
+    for sx, sw, so in [(0.02, 0.005, 0.1), (0.5, 0.25, 0.3), (1e-3, 2e-3, 7e-4), (0.9, 0.9, 0.95)]:
+        qp = icv.QuantParams(0, sx, 0, sw, 0, so)
+        assert qp.requant() == oq.requant_params(sx, sw, so)
+
+
+# ------------------------------------------------------- API semantics on GPU
+def test_api_semantics_mirror_reference_tests():
+    """test_indirect.py:184-216 and :293-305 on the device path."""
+    params = make_params(r=3, s=3, pt=1, pl=1, c=3, k=4)
+    tile = icv.TileConfig()
+    x = icv.tensor_fill_random(icv.Shape4(2, 5, 5, 3), 15, device=DEV)
+    zero = icv.make_zero_row(3, device=DEV)
+    out_shape = icv.conv_output_shape(params, x.shape)
+    ib = icv.init_indirection_buffer(x, zero, params, out_shape, tile)
+    pf = icv.pack_filter(icv.filter_fill_random(params, 16, device=DEV), None, params, tile)
+    a = icv.indirect_conv(x, pf, ib, params, tile).numpy()
+    b = icv.indirect_conv(x, pf, ib, params, tile).numpy()
+    assert a.tobytes() == b.tobytes()                                 # repeat invocations identical
+    assert zero.cpu().tolist() == [0.0, 0.0, 0.0]                     # zero row stays pure
+    small = icv.indirect_conv(x, pf, ib, params, tile, batch=1)       # logical truncation
+    assert small.shape.n == 1
+    assert small.numpy().tobytes() == a[: 5 * 5 * 4].tobytes()
+    other = icv.tensor_fill_random(x.shape, 999, device=DEV)
+    with pytest.raises(icv.StaleBufferError):
+        icv.indirect_conv(other, pf, ib, params, tile)
+    with pytest.raises(icv.StaleBufferError):
+        icv.indirect_conv(x, pf, ib, params, icv.TileConfig(mr=2, nr=8))
+    shifted = make_params(r=3, s=3, pt=1, pl=1, sy=2, sx=2, c=3, k=4)
+    pf2 = icv.pack_filter(icv.filter_fill_random(shifted, 1, device=DEV), None, shifted, tile)
+    with pytest.raises(icv.StaleBufferError):
+        icv.indirect_conv(x, pf2, ib, shifted, tile)
+    with pytest.raises(ValueError):
+        icv.indirect_conv(x, pf, ib, params, tile, batch=3)
+    # rebind to a copy gives the same numbers; same object -> identical buffer
+    copy = icv.tensor_fill_random(x.shape, 15, device=DEV)
+    ib2 = icv.rebind_input(ib, copy, icv.make_zero_row(3, device=DEV))
+    assert torch.equal(ib2.offsets, ib.offsets)
+    assert icv.indirect_conv(copy, pf, ib2, params, tile).numpy().tobytes() == a.tobytes()
+    with pytest.raises(ValueError):
+        icv.rebind_input(ib, icv.tensor_fill_random(icv.Shape4(2, 6, 5, 3), 1, device=DEV), zero)
+
+
+def test_grown_buffer_convolves_like_fresh():
+    """test_indirect.py:279-291 (bit-exact vs the direct oracle)."""
+    params = make_params(r=3, s=3, pt=1, pl=1, c=3, k=5)
+    tile = icv.TileConfig()
+    phys = icv.tensor_fill_random(icv.Shape4(2, 4, 4, 3), 53, device=DEV)
+    zero = icv.make_zero_row(3, device=DEV)
+    out_shape = icv.conv_output_shape(params, phys.shape)
+    pf = icv.pack_filter(icv.filter_fill_random(params, 54, device=DEV), None, params, tile)
+    ib1 = icv.init_indirection_buffer(phys, zero, params, out_shape, tile, batch=1)
+    out = icv.indirect_conv(phys, pf, icv.update_for_batch_growth(ib1, 2), params, tile).numpy()
+    ref = oconv.direct_conv_f32(fill_uniform(phys.shape.numel, 53).reshape(2, 4, 4, 3),
+                                fill_uniform(5 * 9 * 3, 54), None, params)
+    assert out.tobytes() == ref.reshape(-1).tobytes()
+
+
+def test_kernel_selection_is_native_tensor_core_for_baseline_configs():
+    assert L.kernel_name(CFG2.params, CFG2.in_shape, torch.bfloat16).startswith("icv_igemm_tc<bf16")
+    assert L.kernel_name(CFG3B.params, CFG3B.in_shape, torch.bfloat16).startswith("icv_igemm_tc<bf16")
+    assert L.kernel_name(CFG4.params, CFG4.in_shape, torch.uint8).startswith("icv_igemm_tc<u8")
+    assert L.kernel_name(CFG1.params, CFG1.in_shape, torch.float32) == "icv_conv_f32_exact"
+    before = L.launch_count()
+    bf16_problem(CFG2, n_img=1)
+    assert L.launch_count() > before
