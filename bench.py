@@ -110,6 +110,12 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------- CPU reference arm
+def _init_worker():
+    os.environ["OMP_NUM_THREADS"] = "1"
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    os.environ["MKL_NUM_THREADS"] = "1"
+
+
 def _cpu_worker(args):
     """One image of the workload through the oracle port (restates
     convbench.indirect: _compute_offsets + indirect_conv).  Returns seconds
@@ -154,7 +160,7 @@ def cpu_reference(name: str, steps: int, warmup: int, cores: int | None = None) 
     flops_img = w.flops // n_img
     ctx = mp.get_context("spawn")
     times = []
-    with ctx.Pool(per_step, initializer=os.environ.__setitem__, initargs=("OMP_NUM_THREADS", "1")) as pool:
+    with ctx.Pool(per_step, initializer=_init_worker) as pool:
         for it in range(warmup + steps):
             imgs = [(name, (it * per_step + j) % n_img) for j in range(per_step)]
             t0 = time.perf_counter()
