@@ -55,8 +55,14 @@ struct Cfg {
   static constexpr int kTmemNeed = 2 * kAccStride;
   static constexpr uint32_t kTmemCols = kTmemNeed <= 32 ? 32 : kTmemNeed <= 64 ? 64 : kTmemNeed <= 128 ? 128
                                         : kTmemNeed <= 256 ? 256 : 512;
+  // epilogue staging: per epilogue warp, 32 rows x 32 output columns, rows
+  // padded to a 16-byte multiple that keeps the row-per-lane writes
+  // bank-conflict free
+  static constexpr int kOutRowBytes = kI8 ? 32 : 64;
+  static constexpr int kStageRowBytes = kI8 ? 48 : 80;
+  static constexpr int kEpiBytes = 4 * 32 * kStageRowBytes;
   static constexpr int kBarBytes = 256;
-  static constexpr int kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + kOnesBytes + kBarBytes;
+  static constexpr int kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + kOnesBytes + kEpiBytes + kBarBytes;
   static_assert(kTmemNeed <= 512, "TMEM overflow");
   static_assert(kSmemBytes <= 232448, "shared memory overflow");
 };
@@ -65,7 +71,6 @@ struct TcArgs {
   const uint8_t* x;
   const uint8_t* zero_row;
   const void* ib;
-  int32_t ib_is_i32;
   int64_t mr, P;
   int32_t RS, c_bytes, cblocks, elem_bytes, K, n_tiles;
   int64_t total_tiles;
@@ -74,12 +79,21 @@ struct TcArgs {
   int32_t zw, zo, qmin, qmax, m0, shift;
 };
 
-__device__ __forceinline__ int64_t load_ref(const TcArgs& a, int64_t ent) {
-  if (a.ib_is_i32) return (int64_t)__ldg(static_cast<const int32_t*>(a.ib) + ent);
-  return __ldg(static_cast<const int64_t*>(a.ib) + ent);
+// First buffer entry of output pixel p (clamped to the last real pixel,
+// indirect.py:111): ((p / mr) * RS) * mr + p % mr; tap e adds e * mr.
+__device__ __forceinline__ int64_t first_entry(const TcArgs& a, int64_t tile_m, int row) {
+  int64_t p = tile_m * kBM + row;
+  p = p < a.P ? p : a.P - 1;
+  const int64_t t = p / a.mr;
+  return t * a.RS * a.mr + (p - t * a.mr);
 }
 
-template <bool kI8, int BN>
+template <typename IbT>
+__device__ __forceinline__ int64_t load_ref(const TcArgs& a, int64_t ent) {
+  return (int64_t)__ldg(static_cast<const IbT*>(a.ib) + ent);
+}
+
+template <bool kI8, int BN, typename IbT>
 __global__ void __launch_bounds__(kThreads, 1) igemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_b,
                                                                const TcArgs a) {
   using C = Cfg<kI8, BN>;
@@ -88,7 +102,8 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_tc_kernel(const __grid_cons
   uint8_t* sA = smem;
   uint8_t* sB = sA + C::kStages * kABytes;
   uint8_t* sOnes = sB + C::kStages * C::kBBytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sOnes + C::kOnesBytes);
+  uint8_t* sEpi = sOnes + C::kOnesBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + C::kEpiBytes);
   uint64_t* empty = full + C::kStages;
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + 2;
@@ -128,34 +143,51 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_tc_kernel(const __grid_cons
 
   if (warp < 4) {
     // ------------------------------------------------------------ producers
-    const int r = threadIdx.x;
+    // Warp w gathers rows [32w, 32w+32) of the A tile.  Each lane loads the
+    // row reference of ONE row per tap (lane l -> row 32w+l, one coalesced
+    // read of the buffer); the references are then shuffled so that 8
+    // consecutive lanes copy the 8 16-byte chunks of one row: every cp.async
+    // instruction moves 4 whole 128-byte rows (full L2 lines), and every
+    // row lands as 128 contiguous (swizzled) shared-memory bytes.
+    const int chunk = lane & 7;
+    const int sub = lane >> 3;
     int stage = 0;
     uint32_t phase = 0;
-    for (int64_t tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
-      const int64_t mt = tile / a.n_tiles;
-      const int nt = (int)(tile - mt * a.n_tiles);
-      int64_t p = mt * kBM + r;
-      p = p < a.P ? p : a.P - 1;                       // clamped lane (indirect.py:111)
-      const int64_t ent0 = (p / a.mr) * a.RS * a.mr + p % a.mr;
-      int64_t off_next = load_ref(a, ent0);
+    int64_t tile = blockIdx.x;
+    int64_t ent0 = tile < a.total_tiles ? first_entry(a, tile / a.n_tiles, warp * 32 + lane) : 0;
+    int64_t off_next = tile < a.total_tiles ? load_ref<IbT>(a, ent0) : 0;
+    for (; tile < a.total_tiles; tile += gridDim.x) {
+      const int nt = (int)(tile % a.n_tiles);
+      const int64_t next_tile = tile + gridDim.x;
       for (int e = 0; e < a.RS; ++e) {
-        const int64_t off = off_next;
-        if (e + 1 < a.RS) off_next = load_ref(a, ent0 + (int64_t)(e + 1) * a.mr);   // prefetch next tap
-        const uint8_t* src = off < 0 ? a.zero_row : a.x + off * a.elem_bytes;     // ZERO_REF -> zero row
+        const int64_t off_own = off_next;
+        // prefetch the next tap's reference (or the next tile's first tap)
+        if (e + 1 < a.RS) {
+          off_next = load_ref<IbT>(a, ent0 + (int64_t)(e + 1) * a.mr);
+        } else if (next_tile < a.total_tiles) {
+          ent0 = first_entry(a, next_tile / a.n_tiles, warp * 32 + lane);
+          off_next = load_ref<IbT>(a, ent0);
+        }
+        const uint8_t* src[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int64_t off = __shfl_sync(0xffffffffu, off_own, 4 * i + sub);
+          src[i] = off < 0 ? a.zero_row : a.x + off * a.elem_bytes;      // ZERO_REF -> bound zero row
+        }
         for (int cb = 0; cb < a.cblocks; ++cb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          if (r == 0) {
+          if (threadIdx.x == 0) {
             mbar_arrive_expect_tx(&full[stage], C::kBBytes);
             tma_load_2d(sB_u32 + stage * C::kBBytes, &tmap_b, &full[stage], (e * a.cblocks + cb) * 128, nt * BN);
           }
-          const uint32_t dst = sA_u32 + stage * kABytes + r * 128;
-          const int b0 = cb * 128;
+          const int b = cb * 128 + chunk * 16;
+          int valid = a.c_bytes - b;
+          valid = valid < 0 ? 0 : (valid > 16 ? 16 : valid);
+          const uint32_t dst0 = sA_u32 + stage * kABytes;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int b = b0 + j * 16;
-            int valid = a.c_bytes - b;
-            valid = valid < 0 ? 0 : (valid > 16 ? 16 : valid);
-            cp_async_16(dst + ((j ^ (r & 7)) << 4), src + (valid ? b : 0), (uint32_t)valid);
+          for (int i = 0; i < 8; ++i) {
+            const int row = warp * 32 + 4 * i + sub;
+            cp_async_16(dst0 + row * 128 + ((chunk ^ (row & 7)) << 4), src[i] + (valid ? b : 0), (uint32_t)valid);
           }
           cp_async_mbar_arrive_noinc(&full[stage]);
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
@@ -198,8 +230,12 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_tc_kernel(const __grid_cons
     __syncwarp();
   } else {
     // ------------------------------------------------------------ epilogue
+    // Warp w reads TMEM lanes 32*(w%4).. (its 32 rows), 32 columns at a
+    // time; finished values go through a per-warp staging buffer so the
+    // global stores are row-contiguous (8 lanes per 64-byte row segment).
     const int slot = warp & 3;
-    const int row = slot * 32 + lane;
+    uint8_t* stg = sEpi + slot * 32 * C::kStageRowBytes;
+    const bool vec_ok = kI8 ? (a.K & 15) == 0 : (a.K & 7) == 0;
     int as = 0;
     uint32_t aphase = 0;
     for (int64_t tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
@@ -207,7 +243,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_tc_kernel(const __grid_cons
       const int nt = (int)(tile - mt * a.n_tiles);
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
-      const int64_t p = mt * kBM + row;
+      const int64_t row0 = mt * kBM + slot * 32;  // first pixel of this warp's rows
       const uint32_t taddr = tmem_base + ((uint32_t)(slot * 32) << 16) + as * C::kAccStride;
       int32_t rowsum = 0;
       if constexpr (kI8) {
@@ -218,54 +254,69 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_tc_kernel(const __grid_cons
       }
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
+        const int n = nt * BN + c;
+        if (n >= a.K) break;
         uint32_t v[32];
         tmem_ld_32x32b_x32(taddr + c, v);
         tmem_ld_wait();
-        const int n = nt * BN + c;
-        if (p < a.P && n < a.K) {
-          if constexpr (!kI8) {
-            const float* bias = static_cast<const float*>(a.bias) + n;
-            __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.y) + p * a.K + n;
-            if ((a.K & 7) == 0 && n + 32 <= a.K) {
+        uint32_t w[kI8 ? 8 : 16];
+        if constexpr (!kI8) {
+          const float4* bias4 = reinterpret_cast<const float4*>(static_cast<const float*>(a.bias) + n);
 #pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                uint32_t w4[4];
+          for (int q = 0; q < 8; ++q) {
+            const float4 b = __ldg(bias4 + q);
+            __nv_bfloat162 lo = __floats2bfloat162_rn(__uint_as_float(v[4 * q + 0]) + b.x,
+                                                      __uint_as_float(v[4 * q + 1]) + b.y);
+            __nv_bfloat162 hi = __floats2bfloat162_rn(__uint_as_float(v[4 * q + 2]) + b.z,
+                                                      __uint_as_float(v[4 * q + 3]) + b.w);
+            w[2 * q] = *reinterpret_cast<uint32_t*>(&lo);
+            w[2 * q + 1] = *reinterpret_cast<uint32_t*>(&hi);
+          }
+        } else {
+          const int4* cst4 = reinterpret_cast<const int4*>(static_cast<const int32_t*>(a.bias) + n);
+          const long long corr = -(long long)a.zw * rowsum;
 #pragma unroll
-                for (int h = 0; h < 4; ++h) {
-                  const int i = q * 8 + h * 2;
-                  __nv_bfloat162 two = __floats2bfloat162_rn(__uint_as_float(v[i]) + bias[i],
-                                                             __uint_as_float(v[i + 1]) + bias[i + 1]);
-                  w4[h] = *reinterpret_cast<uint32_t*>(&two);
-                }
-                reinterpret_cast<uint4*>(out)[q] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
-              }
-            } else {
+          for (int q = 0; q < 8; ++q) {
+            const int4 b = __ldg(cst4 + q);
+            const int bb[4] = {b.x, b.y, b.z, b.w};
+            uint32_t word = 0;
 #pragma unroll
-              for (int i = 0; i < 32; ++i)
-                if (n + i < a.K) out[i] = __float2bfloat16_rn(__uint_as_float(v[i]) + bias[i]);
+            for (int h = 0; h < 4; ++h) {
+              const int32_t acc = (int32_t)((long long)(int32_t)v[4 * q + h] + bb[h] + corr);
+              word |= (uint32_t)requant_u8(acc, a.m0, a.shift, a.zo, a.qmin, a.qmax) << (8 * h);
             }
-          } else {
-            const int32_t* cst = static_cast<const int32_t*>(a.bias) + n;
-            uint8_t* out = static_cast<uint8_t*>(a.y) + p * a.K + n;
-            const long long corr = -(long long)a.zw * rowsum;
-            uint32_t packed[8];
+            w[q] = word;
+          }
+        }
+        // stage: lane = row
+        uint4* my = reinterpret_cast<uint4*>(stg + lane * C::kStageRowBytes);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const int32_t acc = (int32_t)((long long)(int32_t)v[i] + cst[i] + corr);
-              const uint32_t q8 = requant_u8(acc, a.m0, a.shift, a.zo, a.qmin, a.qmax);
-              if ((i & 3) == 0) packed[i >> 2] = q8;
-              else packed[i >> 2] |= q8 << (8 * (i & 3));
-            }
-            if ((a.K & 15) == 0 && n + 32 <= a.K) {
-              reinterpret_cast<uint4*>(out)[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-              reinterpret_cast<uint4*>(out)[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+        for (int q = 0; q < C::kOutRowBytes / 16; ++q) my[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+        __syncwarp();
+        // write out: lanes cover (row, 16-byte chunk) pairs
+        constexpr int kChunks = C::kOutRowBytes / 16;      // 4 (bf16) or 2 (u8) chunks per row
+        constexpr int kRowsPerPass = 32 / kChunks;
+        const int eb = kI8 ? 1 : 2;
+#pragma unroll
+        for (int pass = 0; pass < 32 / kRowsPerPass; ++pass) {
+          const int rr = pass * kRowsPerPass + lane / kChunks;
+          const int q = lane % kChunks;
+          const int64_t p = row0 + rr;
+          if (p < a.P) {
+            const uint4 val = *reinterpret_cast<const uint4*>(stg + rr * C::kStageRowBytes + q * 16);
+            const int col = n + q * (16 / eb);
+            uint8_t* dst = static_cast<uint8_t*>(a.y) + (p * a.K + col) * eb;
+            if (vec_ok && col + 16 / eb <= a.K) {
+              *reinterpret_cast<uint4*>(dst) = val;
             } else {
-#pragma unroll
-              for (int i = 0; i < 32; ++i)
-                if (n + i < a.K) out[i] = (uint8_t)(packed[i >> 2] >> (8 * (i & 3)));
+              const uint8_t* bytes = reinterpret_cast<const uint8_t*>(&val);
+              for (int j = 0; j < 16 / eb; ++j)
+                if (col + j < a.K)
+                  for (int t = 0; t < eb; ++t) dst[j * eb + t] = bytes[j * eb + t];
             }
           }
         }
+        __syncwarp();
       }
       tc_fence_before();
       mbar_arrive(&tempty[as]);
@@ -294,10 +345,10 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-template <bool kI8, int BN>
+template <bool kI8, int BN, typename IbT>
 int launch_tc(const ConvArgs& c, cudaStream_t st) {
   using Cf = Cfg<kI8, BN>;
-  auto kernel = igemm_tc_kernel<kI8, BN>;
+  auto kernel = igemm_tc_kernel<kI8, BN, IbT>;
   static std::once_flag attr_once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(attr_once, [&] {
@@ -321,7 +372,6 @@ int launch_tc(const ConvArgs& c, cudaStream_t st) {
   a.x = static_cast<const uint8_t*>(c.x);
   a.zero_row = static_cast<const uint8_t*>(c.zero_row);
   a.ib = c.ib;
-  a.ib_is_i32 = c.ib_is_i32;
   a.mr = c.mr;
   a.P = c.P;
   a.RS = c.g.RS();
@@ -345,19 +395,25 @@ int launch_tc(const ConvArgs& c, cudaStream_t st) {
   return cuda_check(cudaGetLastError(), "igemm_tc launch");
 }
 
+template <typename IbT>
+int dispatch_bn(const ConvArgs& c, int bn, cudaStream_t st) {
+  if (c.L.family == kFamTcBf16) {
+    if (bn == 64) return launch_tc<false, 64, IbT>(c, st);
+    if (bn == 128) return launch_tc<false, 128, IbT>(c, st);
+    if (bn == 256) return launch_tc<false, 256, IbT>(c, st);
+  } else if (c.L.family == kFamTcU8) {
+    if (bn == 64) return launch_tc<true, 64, IbT>(c, st);
+    if (bn == 128) return launch_tc<true, 128, IbT>(c, st);
+  }
+  return fail(ICV_ERR_UNSUPPORTED, "no tensor-core kernel for this tile width");
+}
+
 }  // namespace
 
 int launch_conv_tc(const ConvArgs& c, cudaStream_t st) {
   const int bn = c.L.block_n;
-  if (c.L.family == kFamTcBf16) {
-    if (bn == 64) return launch_tc<false, 64>(c, st);
-    if (bn == 128) return launch_tc<false, 128>(c, st);
-    if (bn == 256) return launch_tc<false, 256>(c, st);
-  } else if (c.L.family == kFamTcU8) {
-    if (bn == 64) return launch_tc<true, 64>(c, st);
-    if (bn == 128) return launch_tc<true, 128>(c, st);
-  }
-  return fail(ICV_ERR_UNSUPPORTED, "no tensor-core kernel for this tile width");
+  if (c.ib_is_i32) return dispatch_bn<int32_t>(c, bn, st);
+  return dispatch_bn<int64_t>(c, bn, st);
 }
 
 }  // namespace icv
