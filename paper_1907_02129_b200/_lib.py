@@ -17,7 +17,7 @@ import torch
 
 from .errors import InvalidGeometryError, NativeLibraryError, StaleBufferError, UnsupportedError  # noqa: F401
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libicv.so")
+LIB_PATH = os.environ.get("ICV_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libicv.so")
 
 ICV_OK, ICV_ERR_ARG, ICV_ERR_GEOMETRY, ICV_ERR_STALE, ICV_ERR_UNSUPPORTED, ICV_ERR_CUDA = 0, -1, -2, -3, -4, -5
 ICV_F32, ICV_BF16, ICV_U8, ICV_I32, ICV_I64 = 0, 1, 2, 3, 4

@@ -40,16 +40,32 @@
 namespace icv {
 namespace {
 
-constexpr int kThreads = 288;
+#ifndef ICV_EPI_WARPS
+#define ICV_EPI_WARPS 8
+#endif
+constexpr int kEpiWarps = ICV_EPI_WARPS;          // 4 or 8 (two column halves)
+constexpr int kMmaWarp = 4 + kEpiWarps;
+constexpr int kThreads = 32 * (kMmaWarp + 1);     // 4 producer warps + epilogue warps + 1 MMA warp
+constexpr int kMaxBias = 2048;                    // output channels whose epilogue constants live in smem
 constexpr int kBM = 128;
 constexpr int kABytes = kBM * 128;  // one 128-byte K block per row
 
 template <bool kI8, int BN>
 struct Cfg {
   static constexpr int kBBytes = BN * 128;
-  static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStagesRaw = (192 * 1024) / kStageBytes;
-  static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
+  // One smem "slot" holds one 128-byte K block of A (128 rows) and of B
+  // (BN rows).  A pipeline stage groups kKB slots behind one full/empty
+  // mbarrier pair, so the MMA warp pays one barrier wait per kKB*4 MMAs:
+  // a wait + issue round costs ~330 cycles, more than four N=128 MMAs take
+  // (256 cycles), so narrow tiles batch two K blocks per stage.
+  static constexpr int kKB = BN >= 256 ? 1 : 2;
+  static constexpr int kSlotBytes = kABytes + kBBytes;
+#ifndef ICV_SLOT_KB
+#define ICV_SLOT_KB 192
+#endif
+  static constexpr int kSlotsRaw = (ICV_SLOT_KB * 1024) / kSlotBytes;
+  static constexpr int kSlots = (kSlotsRaw > 8 ? 8 : kSlotsRaw) / kKB * kKB;
+  static constexpr int kStages = kSlots / kKB;
   static constexpr int kOnesBytes = kI8 ? 16 * 128 : 0;
   static constexpr int kAccStride = kI8 ? 2 * BN : BN;  // TMEM columns per accumulator stage
   static constexpr int kTmemNeed = 2 * kAccStride;
@@ -60,12 +76,44 @@ struct Cfg {
   // bank-conflict free
   static constexpr int kOutRowBytes = kI8 ? 32 : 64;
   static constexpr int kStageRowBytes = kI8 ? 48 : 80;
-  static constexpr int kEpiBytes = 4 * 32 * kStageRowBytes;
+  static constexpr int kEpiBytes = kEpiWarps * 32 * kStageRowBytes;
+  static constexpr int kBiasBytes = 4 * kMaxBias;
   static constexpr int kBarBytes = 256;
-  static constexpr int kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + kOnesBytes + kEpiBytes + kBarBytes;
+  static constexpr int kSmemBytes =
+      1024 /*align slack*/ + kSlots * kSlotBytes + kOnesBytes + kEpiBytes + kBiasBytes + kBarBytes;
   static_assert(kTmemNeed <= 512, "TMEM overflow");
   static_assert(kSmemBytes <= 232448, "shared memory overflow");
 };
+
+#ifdef ICV_STATS
+// Debug-build timeline counters (per CTA): 0 producer empty-wait, 1 producer
+// loop, 2 MMA full-wait, 3 MMA tmem-empty-wait, 4 MMA loop, 5 epilogue
+// tmem-full-wait, 6 epilogue loop, 7 k-blocks.  Not compiled in release.
+__device__ unsigned long long g_icv_stats[1024][8];
+#define STAT_BEGIN(v) long long v = clock64()
+#define STAT_ADD(slot, v) atomicAdd(&g_icv_stats[blockIdx.x][slot], (unsigned long long)(clock64() - (v)))
+#define STAT_INC(slot) atomicAdd(&g_icv_stats[blockIdx.x][slot], 1ull)
+#else
+#define STAT_BEGIN(v)
+#define STAT_ADD(slot, v)
+#define STAT_INC(slot)
+#endif
+
+#ifdef ICV_TRACE
+// Debug-build timeline: per CTA, globaltimer (ns) at kernel entry [0], after
+// setup [1], MMA thread's last commit of tile i [2+i], epilogue thread 128's
+// tmem-full wakeup of tile i [10+i] and release [18+i], producer 0 start of
+// tile i [26+i] (i < 8).
+__device__ unsigned long long g_icv_trace[1024][34];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TRACE(slot) g_icv_trace[blockIdx.x][slot] = gtime()
+#else
+#define TRACE(slot)
+#endif
 
 struct TcArgs {
   const uint8_t* x;
@@ -77,6 +125,7 @@ struct TcArgs {
   const void* bias;  // f32 (bf16) or int32 (u8) per padded output channel
   void* y;
   int32_t zw, zo, qmin, qmax, m0, shift;
+  int32_t n_pad;
 };
 
 // First buffer entry of output pixel p (clamped to the last real pixel,
@@ -100,10 +149,11 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_tc_kernel(const __grid_cons
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = sA + C::kStages * kABytes;
-  uint8_t* sOnes = sB + C::kStages * C::kBBytes;
+  uint8_t* sB = sA + C::kSlots * kABytes;
+  uint8_t* sOnes = sB + C::kSlots * C::kBBytes;
   uint8_t* sEpi = sOnes + C::kOnesBytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + C::kEpiBytes);
+  uint32_t* sBias = reinterpret_cast<uint32_t*>(sEpi + C::kEpiBytes);   // f32 or int32 per output channel
+  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + C::kEpiBytes + C::kBiasBytes);
   uint64_t* empty = full + C::kStages;
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + 2;
@@ -111,6 +161,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_tc_kernel(const __grid_cons
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) TRACE(0);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) {
@@ -119,7 +170,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_tc_kernel(const __grid_cons
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);       // tcgen05.commit after the last k-step
-      mbar_init(&tempty[s], 128);    // every epilogue thread
+      mbar_init(&tempty[s], 32 * kEpiWarps);   // every epilogue thread
     }
     fence_mbar_init();
     tma_prefetch_desc(&tmap_b);
@@ -132,11 +183,16 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_tc_kernel(const __grid_cons
       fence_proxy_async_smem();
     }
   }
-  if (warp == 8) tmem_alloc<C::kTmemCols>(tmem_slot);
+  // epilogue constants (bias / folded zero-point terms) for every padded
+  // output channel, staged once per CTA
+  for (int i = threadIdx.x; i < a.n_pad && i < kMaxBias; i += blockDim.x)
+    sBias[i] = __ldg(static_cast<const uint32_t*>(a.bias) + i);
+  if (warp == kMmaWarp) tmem_alloc<C::kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) TRACE(1);
   const int num_kb = a.RS * a.cblocks;
   const uint32_t sA_u32 = smem_u32(sA);
   const uint32_t sB_u32 = smem_u32(sB);
@@ -153,12 +209,15 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_tc_kernel(const __grid_cons
     const int sub = lane >> 3;
     int stage = 0;
     uint32_t phase = 0;
+    STAT_BEGIN(tloop);
     int64_t tile = blockIdx.x;
     int64_t ent0 = tile < a.total_tiles ? first_entry(a, tile / a.n_tiles, warp * 32 + lane) : 0;
     int64_t off_next = tile < a.total_tiles ? load_ref<IbT>(a, ent0) : 0;
-    for (; tile < a.total_tiles; tile += gridDim.x) {
+    for (int ti = 0; tile < a.total_tiles; tile += gridDim.x, ++ti) {
+      if (threadIdx.x == 0 && ti < 8) TRACE(26 + ti);
       const int nt = (int)(tile % a.n_tiles);
       const int64_t next_tile = tile + gridDim.x;
+      int kb = 0;
       for (int e = 0; e < a.RS; ++e) {
         const int64_t off_own = off_next;
         // prefetch the next tap's reference (or the next tile's first tap)
@@ -174,74 +233,114 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_tc_kernel(const __grid_cons
           const int64_t off = __shfl_sync(0xffffffffu, off_own, 4 * i + sub);
           src[i] = off < 0 ? a.zero_row : a.x + off * a.elem_bytes;      // ZERO_REF -> bound zero row
         }
-        for (int cb = 0; cb < a.cblocks; ++cb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          if (threadIdx.x == 0) {
-            mbar_arrive_expect_tx(&full[stage], C::kBBytes);
-            tma_load_2d(sB_u32 + stage * C::kBBytes, &tmap_b, &full[stage], (e * a.cblocks + cb) * 128, nt * BN);
+        for (int cb = 0; cb < a.cblocks; ++cb, ++kb) {
+          const int j = kb % C::kKB;                       // slot within the stage
+          if (j == 0) {
+            STAT_BEGIN(tw);
+            mbar_wait(&empty[stage], phase ^ 1);
+            if (threadIdx.x == 0) {
+              STAT_ADD(0, tw);
+              const int nsub = min(C::kKB, num_kb - kb);
+              mbar_arrive_expect_tx(&full[stage], nsub * C::kBBytes);
+            }
           }
+          const int slot = stage * C::kKB + j;
+          if (threadIdx.x == 0)
+            tma_load_2d(sB_u32 + slot * C::kBBytes, &tmap_b, &full[stage], kb * 128, nt * BN);
           const int b = cb * 128 + chunk * 16;
           int valid = a.c_bytes - b;
           valid = valid < 0 ? 0 : (valid > 16 ? 16 : valid);
-          const uint32_t dst0 = sA_u32 + stage * kABytes;
+          const uint32_t dst0 = sA_u32 + slot * kABytes;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int row = warp * 32 + 4 * i + sub;
             cp_async_16(dst0 + row * 128 + ((chunk ^ (row & 7)) << 4), src[i] + (valid ? b : 0), (uint32_t)valid);
           }
-          cp_async_mbar_arrive_noinc(&full[stage]);
-          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+          if (j == C::kKB - 1 || kb == num_kb - 1) {
+            cp_async_mbar_arrive_noinc(&full[stage]);
+            if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+          }
         }
       }
     }
-  } else if (warp == 8) {
+    if (threadIdx.x == 0) STAT_ADD(1, tloop);
+  } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = make_idesc<kI8>(kBM, BN);
-      constexpr uint32_t idesc_ones = make_idesc<kI8>(kBM, 16);
-      const uint64_t ones_desc = sw128_kmajor_desc(smem_u32(sOnes));
-      int stage = 0;
-      uint32_t phase = 0;
-      int as = 0;
-      uint32_t aphase = 0;
-      for (int64_t tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
-        mbar_wait(&tempty[as], aphase ^ 1);
+    // The whole warp runs the loop (so stage/descriptor values are
+    // warp-uniform and live in uniform registers); one elected lane issues
+    // the tcgen05.mma / tcgen05.commit instructions.
+    constexpr uint32_t idesc = make_idesc<kI8>(kBM, BN);
+    constexpr uint32_t idesc_ones = make_idesc<kI8>(kBM, 16);
+    const uint64_t ones_desc = sw128_kmajor_desc(smem_u32(sOnes));
+    const int stages_per_tile = (num_kb + C::kKB - 1) / C::kKB;
+    int stage = 0;
+    uint32_t phase = 0;
+    int as = 0;
+    uint32_t aphase = 0;
+    STAT_BEGIN(mloop);
+    for (int64_t tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
+      STAT_BEGIN(mw);
+      mbar_wait(&tempty[as], aphase ^ 1);
+      if (lane == 0) STAT_ADD(3, mw);
+      tc_fence_after();
+      const uint32_t d = tmem_base + as * C::kAccStride;
+      for (int si = 0; si < stages_per_tile; ++si) {
+        const int nsub = min(C::kKB, num_kb - si * C::kKB);
+        STAT_BEGIN(fw);
+        mbar_wait(&full[stage], phase);
+        if (lane == 0) { STAT_ADD(2, fw); STAT_INC(7); }
         tc_fence_after();
-        const uint32_t d = tmem_base + as * C::kAccStride;
-        for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tensor-core reads
-          const uint64_t adesc = sw128_kmajor_desc(sA_u32 + stage * kABytes);
-          const uint64_t bdesc = sw128_kmajor_desc(sB_u32 + stage * C::kBBytes);
+        if (elect_one()) {
+          for (int j = 0; j < nsub; ++j) {
+            const int slot = stage * C::kKB + j;
+            const uint64_t adesc = sw128_kmajor_desc(sA_u32 + slot * kABytes);
+            const uint64_t bdesc = sw128_kmajor_desc(sB_u32 + slot * C::kBBytes);
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {  // 4 x 32-byte K steps per 128-byte block
-            const uint32_t acc = (kb | k) != 0;
-            tc_mma<kI8>(d, adesc + 2 * k, bdesc + 2 * k, idesc, acc);
-            if constexpr (kI8) tc_mma<true>(d + BN, adesc + 2 * k, ones_desc + 2 * k, idesc_ones, acc);
+            for (int k = 0; k < 4; ++k) {  // 4 x 32-byte K steps per 128-byte block
+              const uint32_t acc = (si | j | k) != 0;
+              tc_mma<kI8>(d, adesc + 2 * k, bdesc + 2 * k, idesc, acc);
+              if constexpr (kI8) tc_mma<true>(d + BN, adesc + 2 * k, ones_desc + 2 * k, idesc_ones, acc);
+            }
           }
           tc_commit(&empty[stage]);
-          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+          if (si == stages_per_tile - 1) tc_commit(&tfull[as]);
         }
-        tc_commit(&tfull[as]);
-        if (++as == 2) { as = 0; aphase ^= 1; }
+        __syncwarp();
+        if (++stage == C::kStages) { stage = 0; phase ^= 1; }
       }
+      if (lane == 0) {
+        const int ti = (int)((tile - blockIdx.x) / gridDim.x);
+        if (ti < 8) TRACE(2 + ti);
+      }
+      if (++as == 2) { as = 0; aphase ^= 1; }
     }
-    __syncwarp();
+    if (lane == 0) STAT_ADD(4, mloop);
   } else {
     // ------------------------------------------------------------ epilogue
-    // Warp w reads TMEM lanes 32*(w%4).. (its 32 rows), 32 columns at a
-    // time; finished values go through a per-warp staging buffer so the
-    // global stores are row-contiguous (8 lanes per 64-byte row segment).
-    const int slot = warp & 3;
-    uint8_t* stg = sEpi + slot * 32 * C::kStageRowBytes;
+    // Epilogue warp e reads TMEM lanes 32*(e%4).. (its 32 rows; the lane
+    // quarter a warp may access is fixed by warp_id % 4) and, with 8
+    // epilogue warps, one half of the tile's columns.  32 columns per
+    // tcgen05.ld; the next chunk's load is in flight while the current one
+    // is converted.  Finished values go through a per-warp staging buffer
+    // so global stores are row-contiguous (16-byte chunks, whole rows).
+    const int ew = warp - 4;
+    const int slot = ew & 3;
+    constexpr int kColGroups = kEpiWarps / 4;
+    constexpr int kColsPerWarp = BN / kColGroups;
+    const int col0 = (ew / 4) * kColsPerWarp;
+    uint8_t* stg = sEpi + ew * 32 * C::kStageRowBytes;
     const bool vec_ok = kI8 ? (a.K & 15) == 0 : (a.K & 7) == 0;
     int as = 0;
     uint32_t aphase = 0;
+    STAT_BEGIN(eloop);
     for (int64_t tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
       const int64_t mt = tile / a.n_tiles;
       const int nt = (int)(tile - mt * a.n_tiles);
+      STAT_BEGIN(ewt);
       mbar_wait(&tfull[as], aphase);
+      if (threadIdx.x == 128) STAT_ADD(5, ewt);
+      const int ti_ = (int)((tile - blockIdx.x) / gridDim.x);
+      if (threadIdx.x == 128 && ti_ < 8) TRACE(10 + ti_);
       tc_fence_after();
       const int64_t row0 = mt * kBM + slot * 32;  // first pixel of this warp's rows
       const uint32_t taddr = tmem_base + ((uint32_t)(slot * 32) << 16) + as * C::kAccStride;
@@ -252,19 +351,25 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_tc_kernel(const __grid_cons
         tmem_ld_wait();
         rowsum = (int32_t)rs;
       }
+      const int nchunks = min(kColsPerWarp, a.K - nt * BN - col0) > 0
+                              ? (min(kColsPerWarp, a.K - nt * BN - col0) + 31) / 32 : 0;
+      uint32_t v[32];
+      if (nchunks > 0) {
+        tmem_ld_32x32b_x32(taddr + col0, v);
+        tmem_ld_wait_regs(v);
+      }
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int ci = 0; ci < nchunks; ++ci) {
+        const int c = col0 + ci * 32;
         const int n = nt * BN + c;
-        if (n >= a.K) break;
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(taddr + c, v);
-        tmem_ld_wait();
+        uint32_t vn[32];
+        if (ci + 1 < nchunks) tmem_ld_32x32b_x32(taddr + c + 32, vn);
         uint32_t w[kI8 ? 8 : 16];
         if constexpr (!kI8) {
-          const float4* bias4 = reinterpret_cast<const float4*>(static_cast<const float*>(a.bias) + n);
+          const float4* bias4 = reinterpret_cast<const float4*>(sBias + n);
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
-            const float4 b = __ldg(bias4 + q);
+            const float4 b = bias4[q];
             __nv_bfloat162 lo = __floats2bfloat162_rn(__uint_as_float(v[4 * q + 0]) + b.x,
                                                       __uint_as_float(v[4 * q + 1]) + b.y);
             __nv_bfloat162 hi = __floats2bfloat162_rn(__uint_as_float(v[4 * q + 2]) + b.z,
@@ -273,11 +378,11 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_tc_kernel(const __grid_cons
             w[2 * q + 1] = *reinterpret_cast<uint32_t*>(&hi);
           }
         } else {
-          const int4* cst4 = reinterpret_cast<const int4*>(static_cast<const int32_t*>(a.bias) + n);
+          const int4* cst4 = reinterpret_cast<const int4*>(sBias + n);
           const long long corr = -(long long)a.zw * rowsum;
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
-            const int4 b = __ldg(cst4 + q);
+            const int4 b = cst4[q];
             const int bb[4] = {b.x, b.y, b.z, b.w};
             uint32_t word = 0;
 #pragma unroll
@@ -296,7 +401,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_tc_kernel(const __grid_cons
         // write out: lanes cover (row, 16-byte chunk) pairs
         constexpr int kChunks = C::kOutRowBytes / 16;      // 4 (bf16) or 2 (u8) chunks per row
         constexpr int kRowsPerPass = 32 / kChunks;
-        const int eb = kI8 ? 1 : 2;
+        constexpr int eb = kI8 ? 1 : 2;
 #pragma unroll
         for (int pass = 0; pass < 32 / kRowsPerPass; ++pass) {
           const int rr = pass * kRowsPerPass + lane / kChunks;
@@ -317,16 +422,23 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_tc_kernel(const __grid_cons
           }
         }
         __syncwarp();
+        if (ci + 1 < nchunks) {
+          tmem_ld_wait_regs(vn);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = vn[i];
+        }
       }
       tc_fence_before();
       mbar_arrive(&tempty[as]);
+      if (threadIdx.x == 128 && ti_ < 8) TRACE(18 + ti_);
       if (++as == 2) { as = 0; aphase ^= 1; }
     }
+    if (threadIdx.x == 128) STAT_ADD(6, eloop);
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 8) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
     tmem_dealloc<C::kTmemCols>(tmem_base);
   }
@@ -385,6 +497,8 @@ int launch_tc(const ConvArgs& c, cudaStream_t st) {
   a.bias = c.packed + c.L.bias_off;
   a.y = c.y;
   a.zw = c.zw; a.zo = c.zo; a.qmin = c.qmin; a.qmax = c.qmax; a.m0 = c.m0; a.shift = c.shift;
+  a.n_pad = c.L.n_pad;
+  if (c.L.n_pad > kMaxBias) return fail(ICV_ERR_UNSUPPORTED, "more than 2048 output channels");
 
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -409,6 +523,28 @@ int dispatch_bn(const ConvArgs& c, int bn, cudaStream_t st) {
 }
 
 }  // namespace
+
+#ifdef ICV_TRACE
+extern "C" ICV_API int icv_debug_trace(unsigned long long* host, int reset) {
+  if (host && cudaMemcpyFromSymbol(host, g_icv_trace, sizeof(g_icv_trace)) != cudaSuccess) return ICV_ERR_CUDA;
+  if (reset) {
+    static unsigned long long zeros[1024][34];
+    if (cudaMemcpyToSymbol(g_icv_trace, zeros, sizeof(zeros)) != cudaSuccess) return ICV_ERR_CUDA;
+  }
+  return ICV_OK;
+}
+#endif
+
+#ifdef ICV_STATS
+extern "C" ICV_API int icv_debug_stats(unsigned long long* host, int reset) {
+  if (host && cudaMemcpyFromSymbol(host, g_icv_stats, sizeof(g_icv_stats)) != cudaSuccess) return ICV_ERR_CUDA;
+  if (reset) {
+    static unsigned long long zeros[1024][8];
+    if (cudaMemcpyToSymbol(g_icv_stats, zeros, sizeof(zeros)) != cudaSuccess) return ICV_ERR_CUDA;
+  }
+  return ICV_OK;
+}
+#endif
 
 int launch_conv_tc(const ConvArgs& c, cudaStream_t st) {
   const int bn = c.L.block_n;

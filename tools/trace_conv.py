@@ -1,0 +1,57 @@
+"""Per-CTA timeline of the tcgen05 kernel (debug build with ICV_TRACE):
+    ICV_LIB=.../libicv_trace.so python tools/trace_conv.py cfg2"""
+import ctypes
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_1907_02129_b200 as icv  # noqa: E402
+from paper_1907_02129_b200 import _lib as L  # noqa: E402
+
+
+def main():
+    from paper_1907_02129_b200.workloads import CONFIGS
+
+    name = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
+    dev = torch.device("cuda", 0)
+    w, x, xh, pf, ib, y, tile = bench.setup_problem(name, 0, CONFIGS[name].in_shape.n, dev)
+    fn = L.lib().icv_debug_trace
+    fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for _ in range(3):
+        icv.indirect_conv(x, pf, ib, w.params, tile, out=y)
+    fn(None, 1)
+    flush.fill_(1)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    icv.indirect_conv(x, pf, ib, w.params, tile, out=y)
+    e.record()
+    torch.cuda.synchronize()
+    buf = np.zeros((1024, 34), np.uint64)
+    fn(buf.ctypes.data, 0)
+    tr = buf[:148].astype(np.int64)
+    t0 = tr[:, 0][tr[:, 0] > 0].min()
+    rel = np.where(tr > 0, tr - t0, -1)
+    print(f"{name}: event {s.elapsed_time(e) * 1e3:.1f} us; kernel entry spread {(rel[:, 0].max()) / 1e3:.2f} us; "
+          f"setup {np.median(rel[:, 1] - rel[:, 0]) / 1e3:.2f} us")
+    last_end = rel[:, 18:26].max()
+    print(f"last epilogue release at {last_end / 1e3:.2f} us after first CTA entry")
+    for cta in (0, 1, 73, 147):
+        r = rel[cta]
+        tiles = [i for i in range(8) if r[2 + i] >= 0]
+        row = " | ".join(f"t{i}: prod {r[26 + i] / 1e3:.2f} mma_end {r[2 + i] / 1e3:.2f} "
+                         f"epi {r[10 + i] / 1e3:.2f}-{r[18 + i] / 1e3:.2f}" for i in tiles)
+        print(f"cta {cta:3d} entry {r[0] / 1e3:.2f} setup {r[1] / 1e3:.2f} :: {row}")
+    d = rel[:, 3] - rel[:, 2]
+    print(f"median tile-1 mainloop (mma_end1 - mma_end0) {np.median(d[d > 0]) / 1e3:.2f} us; "
+          f"median epilogue {np.median((rel[:, 18] - rel[:, 10])[rel[:, 10] >= 0]) / 1e3:.2f} us")
+
+
+if __name__ == "__main__":
+    main()
