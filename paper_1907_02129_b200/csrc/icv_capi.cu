@@ -52,11 +52,14 @@ int make_geom(const icv_conv_desc* d, const icv_shape4* in, Geom* g) {
   return ICV_OK;
 }
 
-int family_for(int32_t dtype, int C) {
+int family_for(int32_t dtype, int C, int RS, int K) {
+  // tensor-core kernels need 16-byte pixel rows, an indirection slice that
+  // fits in shared memory (R*S <= 24) and at most 2048 output channels
+  const bool tc_ok = RS <= kMaxRsTc && K <= 2048;
   switch (dtype) {
     case ICV_F32: return kFamF32Exact;
-    case ICV_BF16: return (C % 8 == 0) ? kFamTcBf16 : kFamCoreBf16;   // 16-byte pixel rows
-    case ICV_U8: return (C % 16 == 0) ? kFamTcU8 : kFamCoreU8;
+    case ICV_BF16: return (C % 8 == 0 && tc_ok) ? kFamTcBf16 : kFamCoreBf16;
+    case ICV_U8: return (C % 16 == 0 && tc_ok) ? kFamTcU8 : kFamCoreU8;
     default: return -1;
   }
 }
@@ -73,7 +76,7 @@ int packed_layout(const icv_conv_desc* d, int32_t dtype, PackedLayout* L) {
   if (!d || !L) return fail(ICV_ERR_ARG, "null argument");
   if (d->in_channels < 1 || d->out_channels < 1 || d->kernel_h < 1 || d->kernel_w < 1)
     return fail(ICV_ERR_ARG, "bad filter geometry");
-  const int fam = family_for(dtype, d->in_channels);
+  const int fam = family_for(dtype, d->in_channels, d->kernel_h * d->kernel_w, d->out_channels);
   if (fam < 0) return fail(ICV_ERR_ARG, "unsupported compute dtype");
   const int64_t K = d->out_channels, C = d->in_channels, RS = (int64_t)d->kernel_h * d->kernel_w;
   std::memset(L, 0, sizeof(*L));
@@ -207,23 +210,23 @@ ICV_API int icv_pack_filter(const icv_conv_desc* desc, int32_t compute_dtype, in
   return launch_pack(g, L, w_dtype, w_krsc, bias, quant, packed, (cudaStream_t)stream);
 }
 
-static const char* kernel_name_for(int fam, int bn) {
-  switch (fam) {
+static const char* kernel_name_for(const ConvArgs& a) {
+  switch (a.L.family) {
     case kFamF32Exact: return "icv_conv_f32_exact";
     case kFamCoreBf16: return "icv_conv_core<bf16>";
     case kFamCoreU8: return "icv_conv_core<u8>";
-    case kFamTcBf16: return bn == 64 ? "icv_igemm_tc<bf16,64>" : bn == 128 ? "icv_igemm_tc<bf16,128>" : "icv_igemm_tc<bf16,256>";
-    case kFamTcU8: return bn == 64 ? "icv_igemm_tc<u8,64>" : "icv_igemm_tc<u8,128>";
+    case kFamTcBf16:
+    case kFamTcU8: return tc_kernel_name(a);
   }
   return "?";
 }
 
 ICV_API int icv_conv_kernel_name(const icv_conv_desc* desc, const icv_shape4* in, int32_t dtype, const char** name) {
-  Geom g;
-  if (int s = make_geom(desc, in, &g)) return s;
-  const int fam = family_for(dtype, g.C);
-  if (fam < 0) return fail(ICV_ERR_ARG, "unsupported dtype");
-  if (name) *name = kernel_name_for(fam, tc_block_n(fam, g.K));
+  ConvArgs a{};
+  if (int s = make_geom(desc, in, &a.g)) return s;
+  if (int s = packed_layout(desc, dtype, &a.L)) return s;
+  a.P = in->n * a.g.OH * a.g.OW;
+  if (name) *name = kernel_name_for(a);
   return ICV_OK;
 }
 

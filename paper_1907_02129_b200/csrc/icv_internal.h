@@ -27,7 +27,8 @@ int make_geom(const icv_conv_desc* d, const icv_shape4* in, Geom* g);
 
 // ---- kernel families ---------------------------------------------------------
 enum Family { kFamF32Exact = 0, kFamTcBf16 = 1, kFamTcU8 = 2, kFamCoreBf16 = 3, kFamCoreU8 = 4 };
-int family_for(int32_t dtype, int C);
+constexpr int kMaxRsTc = 24;   // taps per pixel handled by the tensor-core kernels
+int family_for(int32_t dtype, int C, int RS, int K);
 // Output-channel tile width of the tensor-core kernels for this problem.
 int tc_block_n(int family, int K);
 // Packed-filter layout (byte offsets inside the icv_pack_filter buffer).
@@ -64,5 +65,6 @@ struct ConvArgs {
 int launch_conv_f32_exact(const ConvArgs& a, cudaStream_t st);
 int launch_conv_core(const ConvArgs& a, cudaStream_t st);       // bf16 / u8, any C (CUDA cores)
 int launch_conv_tc(const ConvArgs& a, cudaStream_t st);         // bf16 / u8 tcgen05
+const char* tc_kernel_name(const ConvArgs& a);
 
 }  // namespace icv

@@ -1,0 +1,205 @@
+// Pieces shared by the two tcgen05 indirect-GEMM kernels (igemm_tc.cu:
+// A operand gathered into shared memory; igemm_tmem.cu: A operand gathered
+// into tensor memory): kernel arguments, indirection-buffer addressing, the
+// TMEM -> registers -> HBM epilogue, and the TMA descriptor of the packed
+// filter.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "icv_internal.h"
+#include "requant.cuh"
+#include "sm100_ptx.cuh"
+
+namespace icv {
+
+constexpr int kBM = 128;                // output pixels per tile (TMEM lanes / MMA M)
+constexpr int kABytes = kBM * 128;      // one 128-byte K block of the A tile
+constexpr int kMaxBias = 2048;          // output channels whose epilogue constants live in smem
+
+#ifdef ICV_TRACE
+// Debug-build timeline (tools/trace_conv.py): per CTA, globaltimer (ns) at
+// kernel entry [0], after setup [1], MMA warp's last commit of tile i [2+i],
+// epilogue's tmem-full wakeup of tile i [10+i] and release [18+i], producer
+// start of tile i [26+i] (i < 8).  Never compiled into the shipped library.
+extern __device__ unsigned long long g_icv_trace[1024][40];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TRACE(slot) g_icv_trace[blockIdx.x][slot] = gtime()
+#else
+#define TRACE(slot)
+#endif
+
+struct TcArgs {
+  const uint8_t* x;
+  const uint8_t* zero_row;
+  const void* ib;
+  int64_t mr, P;
+  int32_t RS, c_bytes, cblocks, elem_bytes, K, n_tiles;
+  int64_t total_tiles;
+  const void* bias;  // f32 (bf16) or int32 (u8) epilogue constant per padded output channel
+  void* y;
+  int32_t zw, zo, qmin, qmax, m0, shift;
+  int32_t n_pad;
+  int32_t cblock_elems;      // elements per 128-byte channel block
+  int32_t c_tz;              // C = odd << c_tz
+  uint32_t c_inv;            // odd^-1 mod 2^32
+  int32_t use_tma_x;         // input tensor map valid (TMA gathers allowed)
+};
+
+// First buffer entry of output pixel p = tile_m*128 + row, clamped to the
+// last real pixel (indirect.py:111): ((p / mr) * RS) * mr + p % mr.  Tap e
+// adds e * mr (layout: tile-major, kernel element, lane; indirect.py:14-16).
+__device__ __forceinline__ int64_t first_entry(const TcArgs& a, int64_t tile_m, int row) {
+  int64_t p = tile_m * kBM + row;
+  p = p < a.P ? p : a.P - 1;
+  const int64_t t = p / a.mr;
+  return t * a.RS * a.mr + (p - t * a.mr);
+}
+
+// Pixel-row index of an element offset (offsets are multiples of C).
+__device__ __forceinline__ int32_t pixel_row(const TcArgs& a, int64_t off) {
+  return (int32_t)(((uint32_t)off >> a.c_tz) * a.c_inv);
+}
+
+template <typename IbT>
+__device__ __forceinline__ int64_t load_ref(const TcArgs& a, int64_t ent) {
+  return (int64_t)__ldg(static_cast<const IbT*>(a.ib) + ent);
+}
+
+// ----------------------------------------------------------------------------
+// Epilogue (K6).  Epilogue warp `ew` (warp_id % 4 == ew % 4, which fixes the
+// TMEM lane quarter it may read) owns 32 rows of the tile and, when there are
+// 8 epilogue warps, half of its columns.  Per 32-column chunk: tcgen05.ld the
+// fp32/s32 accumulators (the next chunk's load is in flight while this one is
+// converted), add the folded bias / zero-point constants from smem, cast to
+// bf16 or requantize to uint8, stage the 32 x 32 block in smem and write it out
+// with row-contiguous 16-byte stores.  Tail rows (>= P) and columns (>= K) are
+// never stored (indirect.py:299).
+template <bool kI8, int BN, int kEpiWarps, int kAccStride>
+__device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane, uint32_t tmem_base, uint8_t* sEpi,
+                                              const uint32_t* sBias, uint64_t* tfull, uint64_t* tempty) {
+  constexpr int kOutRowBytes = kI8 ? 32 : 64;
+  constexpr int kStageRowBytes = kI8 ? 48 : 80;  // padded: row-per-lane staging writes are conflict free
+  const int slot = ew & 3;
+  constexpr int kColGroups = kEpiWarps / 4;
+  constexpr int kColsPerWarp = BN / kColGroups;
+  const int col0 = (ew / 4) * kColsPerWarp;
+  uint8_t* stg = sEpi + ew * 32 * kStageRowBytes;
+  const bool vec_ok = kI8 ? (a.K & 15) == 0 : (a.K & 7) == 0;
+  int as = 0;
+  uint32_t aphase = 0;
+  for (int64_t tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
+    const int64_t mt = tile / a.n_tiles;
+    const int nt = (int)(tile - mt * a.n_tiles);
+    mbar_wait(&tfull[as], aphase);
+    tc_fence_after();
+    const int ti_ = (int)((tile - blockIdx.x) / gridDim.x);
+    if (ew == 0 && lane == 0 && ti_ < 8) TRACE(10 + ti_);
+    const int64_t row0 = mt * kBM + slot * 32;  // first pixel of this warp's rows
+    const uint32_t taddr = tmem_base + ((uint32_t)(slot * 32) << 16) + as * kAccStride;
+    int32_t rowsum = 0;
+    if constexpr (kI8) {
+      uint32_t rs;
+      tmem_ld_32x32b_x1(taddr + BN, rs);
+      tmem_ld_wait();
+      rowsum = (int32_t)rs;
+    }
+    const int cols_left = a.K - nt * BN - col0;
+    const int nchunks = cols_left > 0 ? (min(kColsPerWarp, cols_left) + 31) / 32 : 0;
+    uint32_t v[32];
+    if (nchunks > 0) {
+      tmem_ld_32x32b_x32(taddr + col0, v);
+      tmem_ld_wait_regs(v);
+    }
+#pragma unroll 1
+    for (int ci = 0; ci < nchunks; ++ci) {
+      const int c = col0 + ci * 32;
+      const int n = nt * BN + c;
+      uint32_t vn[32];
+      if (ci + 1 < nchunks) tmem_ld_32x32b_x32(taddr + c + 32, vn);
+      uint32_t w[kI8 ? 8 : 16];
+      if constexpr (!kI8) {
+        const float4* bias4 = reinterpret_cast<const float4*>(sBias + n);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 b = bias4[q];
+          __nv_bfloat162 lo = __floats2bfloat162_rn(__uint_as_float(v[4 * q + 0]) + b.x,
+                                                    __uint_as_float(v[4 * q + 1]) + b.y);
+          __nv_bfloat162 hi = __floats2bfloat162_rn(__uint_as_float(v[4 * q + 2]) + b.z,
+                                                    __uint_as_float(v[4 * q + 3]) + b.w);
+          w[2 * q] = *reinterpret_cast<uint32_t*>(&lo);
+          w[2 * q + 1] = *reinterpret_cast<uint32_t*>(&hi);
+        }
+      } else {
+        const int4* cst4 = reinterpret_cast<const int4*>(sBias + n);
+        const long long corr = -(long long)a.zw * rowsum;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int4 b = cst4[q];
+          const int bb[4] = {b.x, b.y, b.z, b.w};
+          uint32_t word = 0;
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            const int32_t acc = (int32_t)((long long)(int32_t)v[4 * q + h] + bb[h] + corr);
+            word |= (uint32_t)requant_u8(acc, a.m0, a.shift, a.zo, a.qmin, a.qmax) << (8 * h);
+          }
+          w[q] = word;
+        }
+      }
+      uint4* my = reinterpret_cast<uint4*>(stg + lane * kStageRowBytes);
+#pragma unroll
+      for (int q = 0; q < kOutRowBytes / 16; ++q) my[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+      __syncwarp();
+      constexpr int kChunks = kOutRowBytes / 16;  // 16-byte chunks per staged row
+      constexpr int kRowsPerPass = 32 / kChunks;
+      constexpr int eb = kI8 ? 1 : 2;
+#pragma unroll
+      for (int pass = 0; pass < 32 / kRowsPerPass; ++pass) {
+        const int rr = pass * kRowsPerPass + lane / kChunks;
+        const int q = lane % kChunks;
+        const int64_t p = row0 + rr;
+        if (p < a.P) {
+          const uint4 val = *reinterpret_cast<const uint4*>(stg + rr * kStageRowBytes + q * 16);
+          const int col = n + q * (16 / eb);
+          uint8_t* dst = static_cast<uint8_t*>(a.y) + (p * a.K + col) * eb;
+          if (vec_ok && col + 16 / eb <= a.K) {
+            *reinterpret_cast<uint4*>(dst) = val;
+          } else {
+            const uint8_t* bytes = reinterpret_cast<const uint8_t*>(&val);
+            for (int j = 0; j < 16 / eb; ++j)
+              if (col + j < a.K)
+                for (int t = 0; t < eb; ++t) dst[j * eb + t] = bytes[j * eb + t];
+          }
+        }
+      }
+      __syncwarp();
+      if (ci + 1 < nchunks) {
+        tmem_ld_wait_regs(vn);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = vn[i];
+      }
+    }
+    tc_fence_before();
+    mbar_arrive(&tempty[as]);
+    if (ew == 0 && lane == 0 && ti_ < 8) TRACE(18 + ti_);
+    if (++as == 2) { as = 0; aphase ^= 1; }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Host side: TMA map of the packed filter rows (K-major, 128-byte column
+// blocks, 128-byte swizzle) and the common argument block.
+PFN_cuTensorMapEncodeTiled_v12000 get_tensor_map_encoder();
+int make_filter_tmap(const ConvArgs& c, int block_n, CUtensorMap* tmap);
+int make_input_tmap(const ConvArgs& c, CUtensorMap* tmap);
+void fill_tc_args(const ConvArgs& c, int block_n, TcArgs* a);
+int sm_count();
+
+}  // namespace icv

@@ -1,193 +1,147 @@
-// K2/K3/K6: the indirect-GEMM mainloop on sm_100a tensor cores.
+// K2/K3: indirect-GEMM mainloop on sm_100a tensor cores, A operand staged in
+// SHARED memory ("kernel S").  Used for wide output tiles (BLOCK_N = 256,
+// whose two TMEM accumulators fill all 512 TMEM columns) and for problems
+// with too few K blocks per tile for the TMEM-A kernel (igemm_tmem.cu).
 //
-// Replaces indirect_conv's hot loop (reference indirect.py:287-294) for
-// bf16 (tcgen05 kind::f16, fp32 accumulate) and uint8 (kind::i8, s32
-// accumulate) when pixel rows are 16-byte aligned.  GEMM view:
-// M = output pixels, N = output channels, K = R*S taps x C channels.
-//
-// Persistent, warp-specialised CTA (one per SM, 288 threads):
-//   warps 0-3  A producers.  Thread r owns row r of the 128-pixel M tile.
-//              Per tap e it reads that pixel's row reference from the
-//              indirection buffer (the paper's "load fresh row pointers per
-//              kernel element", Listing 3), resolves ZERO_REF to the bound
-//              zero row, and gathers the row's 128-byte channel block with
-//              eight 16-byte cp.async into the stage's A tile in the
-//              canonical 128B-swizzle K-major layout.  Completion is
-//              signalled on the stage's mbarrier (cp.async.mbarrier.arrive
-//              .noinc).  Thread 0 also issues the TMA load of the matching
-//              128-byte column block of the packed filter (B operand).
-//   warp 8     MMA issuer (one elected lane): 4 x tcgen05.mma (K = 32 bytes
-//              each) per stage into a TMEM accumulator; tcgen05.commit frees
-//              the smem stage and, after the last k-step, publishes the
-//              accumulator.  For uint8 a second N=16 MMA against an all-ones
-//              B tile accumulates the per-pixel input row sum needed by the
-//              zero-point correction.
-//   warps 4-7  epilogue: tcgen05.ld the accumulator (warp w reads TMEM lanes
-//              32*(w%4)..), add the folded bias / zero-point constants, cast
-//              to bf16 or requantize to uint8, store NHWC rows.  Two TMEM
-//              accumulator stages let the epilogue of tile i overlap the
-//              mainloop of tile i+1.
-#include <cuda.h>
-#include <cuda_bf16.h>
-#include <cudaTypedefs.h>
+// Replaces indirect_conv's hot loop (reference indirect.py:287-294).  GEMM
+// view: M = output pixels, N = output channels, K = R*S taps x C channels.
+// Persistent, warp-specialised CTA (one per SM):
+//   warps 0-3  A producers.  The CTA's slice of the indirection buffer for
+//              its next tile (128 pixels x R*S taps, tile-major / tap / lane,
+//              indirect.py:14-16) is copied into smem by cp.async one tile
+//              ahead, so reading the row references never stalls the gather.
+//              Per tap the warp reads the references of its 32 rows (the
+//              paper's "load fresh row pointers per kernel element",
+//              Listing 3), resolves ZERO_REF to the bound zero row, and
+//              gathers 4 whole 128-byte rows per cp.async instruction (8
+//              lanes per row) into the slot's A tile in the canonical
+//              128B-swizzle K-major layout.  Thread 0 also TMA-loads the
+//              matching packed-filter block (B).
+//   warps 4-7  epilogue (igemm_common.cuh).
+//   warp 8     MMA: one elected lane issues 4 x tcgen05.mma per 128-byte K
+//              block into a TMEM accumulator (uint8 adds an N=16 MMA against
+//              an all-ones tile: the per-pixel input row sums needed by the
+//              zero-point correction); tcgen05.commit releases smem stages
+//              and publishes finished accumulators.
+#include <cstdlib>
 
-#include <mutex>
-
-#include "icv_internal.h"
-#include "requant.cuh"
-#include "sm100_ptx.cuh"
+#include "igemm_common.cuh"
 
 namespace icv {
+
+#ifdef ICV_TRACE
+__device__ unsigned long long g_icv_trace[1024][40];
+#endif
+
 namespace {
 
-#ifndef ICV_EPI_WARPS
-#define ICV_EPI_WARPS 8
-#endif
-constexpr int kEpiWarps = ICV_EPI_WARPS;          // 4 or 8 (two column halves)
-constexpr int kMmaWarp = 4 + kEpiWarps;
-constexpr int kThreads = 32 * (kMmaWarp + 1);     // 4 producer warps + epilogue warps + 1 MMA warp
-constexpr int kMaxBias = 2048;                    // output channels whose epilogue constants live in smem
-constexpr int kBM = 128;
-constexpr int kABytes = kBM * 128;  // one 128-byte K block per row
+constexpr int kEpiWarpsS = 4;
+constexpr int kMmaWarpS = 4 + kEpiWarpsS;
+constexpr int kThreadsS = 32 * (kMmaWarpS + 1);
 
 template <bool kI8, int BN>
-struct Cfg {
+struct CfgS {
   static constexpr int kBBytes = BN * 128;
-  // One smem "slot" holds one 128-byte K block of A (128 rows) and of B
-  // (BN rows).  A pipeline stage groups kKB slots behind one full/empty
-  // mbarrier pair, so the MMA warp pays one barrier wait per kKB*4 MMAs:
-  // a wait + issue round costs ~330 cycles, more than four N=128 MMAs take
-  // (256 cycles), so narrow tiles batch two K blocks per stage.
+  // One smem slot = one 128-byte K block of A (128 rows) and of B (BN rows).
+  // A stage groups kKB slots behind one full/empty barrier pair so the MMA
+  // warp pays one barrier round trip per kKB*4 MMAs.
   static constexpr int kKB = BN >= 256 ? 1 : 2;
   static constexpr int kSlotBytes = kABytes + kBBytes;
-#ifndef ICV_SLOT_KB
-#define ICV_SLOT_KB 192
-#endif
-  static constexpr int kSlotsRaw = (ICV_SLOT_KB * 1024) / kSlotBytes;
-  static constexpr int kSlots = (kSlotsRaw > 8 ? 8 : kSlotsRaw) / kKB * kKB;
-  static constexpr int kStages = kSlots / kKB;
+  static constexpr int kMaxSlots = 8;
   static constexpr int kOnesBytes = kI8 ? 16 * 128 : 0;
   static constexpr int kAccStride = kI8 ? 2 * BN : BN;  // TMEM columns per accumulator stage
   static constexpr int kTmemNeed = 2 * kAccStride;
-  static constexpr uint32_t kTmemCols = kTmemNeed <= 32 ? 32 : kTmemNeed <= 64 ? 64 : kTmemNeed <= 128 ? 128
-                                        : kTmemNeed <= 256 ? 256 : 512;
-  // epilogue staging: per epilogue warp, 32 rows x 32 output columns, rows
-  // padded to a 16-byte multiple that keeps the row-per-lane writes
-  // bank-conflict free
-  static constexpr int kOutRowBytes = kI8 ? 32 : 64;
-  static constexpr int kStageRowBytes = kI8 ? 48 : 80;
-  static constexpr int kEpiBytes = kEpiWarps * 32 * kStageRowBytes;
-  static constexpr int kBiasBytes = 4 * kMaxBias;
+  static constexpr uint32_t kTmemCols = kTmemNeed <= 64 ? 64 : kTmemNeed <= 128 ? 128 : kTmemNeed <= 256 ? 256 : 512;
+  static constexpr int kEpiBytes = kEpiWarpsS * 32 * (kI8 ? 48 : 80);
   static constexpr int kBarBytes = 256;
-  static constexpr int kSmemBytes =
-      1024 /*align slack*/ + kSlots * kSlotBytes + kOnesBytes + kEpiBytes + kBiasBytes + kBarBytes;
   static_assert(kTmemNeed <= 512, "TMEM overflow");
-  static_assert(kSmemBytes <= 232448, "shared memory overflow");
 };
 
-#ifdef ICV_STATS
-// Debug-build timeline counters (per CTA): 0 producer empty-wait, 1 producer
-// loop, 2 MMA full-wait, 3 MMA tmem-empty-wait, 4 MMA loop, 5 epilogue
-// tmem-full-wait, 6 epilogue loop, 7 k-blocks.  Not compiled in release.
-__device__ unsigned long long g_icv_stats[1024][8];
-#define STAT_BEGIN(v) long long v = clock64()
-#define STAT_ADD(slot, v) atomicAdd(&g_icv_stats[blockIdx.x][slot], (unsigned long long)(clock64() - (v)))
-#define STAT_INC(slot) atomicAdd(&g_icv_stats[blockIdx.x][slot], 1ull)
-#else
-#define STAT_BEGIN(v)
-#define STAT_ADD(slot, v)
-#define STAT_INC(slot)
-#endif
-
-#ifdef ICV_TRACE
-// Debug-build timeline: per CTA, globaltimer (ns) at kernel entry [0], after
-// setup [1], MMA thread's last commit of tile i [2+i], epilogue thread 128's
-// tmem-full wakeup of tile i [10+i] and release [18+i], producer 0 start of
-// tile i [26+i] (i < 8).
-__device__ unsigned long long g_icv_trace[1024][34];
-__device__ __forceinline__ unsigned long long gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-#define TRACE(slot) g_icv_trace[blockIdx.x][slot] = gtime()
-#else
-#define TRACE(slot)
-#endif
-
-struct TcArgs {
-  const uint8_t* x;
-  const uint8_t* zero_row;
-  const void* ib;
-  int64_t mr, P;
-  int32_t RS, c_bytes, cblocks, elem_bytes, K, n_tiles;
-  int64_t total_tiles;
-  const void* bias;  // f32 (bf16) or int32 (u8) per padded output channel
-  void* y;
-  int32_t zw, zo, qmin, qmax, m0, shift;
-  int32_t n_pad;
+// Runtime shared-memory plan of kernel S: the ring gets whatever the index
+// slices, epilogue staging and constants leave of the 227 KB.
+struct PlanS {
+  int slots, stages;
+  int off_b, off_ones, off_epi, off_bias, off_ib, off_bar, bytes;
 };
 
-// First buffer entry of output pixel p (clamped to the last real pixel,
-// indirect.py:111): ((p / mr) * RS) * mr + p % mr; tap e adds e * mr.
-__device__ __forceinline__ int64_t first_entry(const TcArgs& a, int64_t tile_m, int row) {
-  int64_t p = tile_m * kBM + row;
-  p = p < a.P ? p : a.P - 1;
-  const int64_t t = p / a.mr;
-  return t * a.RS * a.mr + (p - t * a.mr);
-}
-
-template <typename IbT>
-__device__ __forceinline__ int64_t load_ref(const TcArgs& a, int64_t ent) {
-  return (int64_t)__ldg(static_cast<const IbT*>(a.ib) + ent);
+template <bool kI8, int BN, typename IbT>
+bool plan_smem(int rs, int n_pad, PlanS* p) {
+  using C = CfgS<kI8, BN>;
+  const int bias = (n_pad * 4 + 15) / 16 * 16;
+  const int ib = 2 * rs * kBM * (int)sizeof(IbT);
+  const int fixed = 1024 + C::kOnesBytes + C::kEpiBytes + bias + ib + C::kBarBytes;
+  int slots = (232448 - fixed) / C::kSlotBytes;
+  slots = (slots > C::kMaxSlots ? C::kMaxSlots : slots) / C::kKB * C::kKB;
+  if (slots < 2 * C::kKB) return false;
+  p->slots = slots;
+  p->stages = slots / C::kKB;
+  p->off_b = slots * kABytes;
+  p->off_ones = p->off_b + slots * C::kBBytes;
+  p->off_epi = p->off_ones + C::kOnesBytes;
+  p->off_bias = p->off_epi + C::kEpiBytes;
+  p->off_ib = p->off_bias + bias;
+  p->off_bar = p->off_ib + ib;
+  p->bytes = 1024 + p->off_bar + C::kBarBytes;
+  return true;
 }
 
 template <bool kI8, int BN, typename IbT>
-__global__ void __launch_bounds__(kThreads, 1) igemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_b,
-                                                               const TcArgs a) {
-  using C = Cfg<kI8, BN>;
+__global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_constant__ CUtensorMap tmap_b,
+                                                                  const __grid_constant__ CUtensorMap tmap_x,
+                                                                  const TcArgs a, const PlanS pl) {
+  using C = CfgS<kI8, BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = sA + C::kSlots * kABytes;
-  uint8_t* sOnes = sB + C::kSlots * C::kBBytes;
-  uint8_t* sEpi = sOnes + C::kOnesBytes;
-  uint32_t* sBias = reinterpret_cast<uint32_t*>(sEpi + C::kEpiBytes);   // f32 or int32 per output channel
-  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + C::kEpiBytes + C::kBiasBytes);
-  uint64_t* empty = full + C::kStages;
-  uint64_t* tfull = empty + C::kStages;
+  uint8_t* sB = smem + pl.off_b;
+  uint8_t* sOnes = smem + pl.off_ones;
+  uint8_t* sEpi = smem + pl.off_epi;
+  uint32_t* sBias = reinterpret_cast<uint32_t*>(smem + pl.off_bias);
+  IbT* sIB = reinterpret_cast<IbT*>(smem + pl.off_ib);          // [2][RS][128] index slices
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + pl.off_bar);
+  const int kStages = pl.stages;
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) TRACE(0);
-
+  // TMA gathers realize padding taps as out-of-bounds (zero-filled) rows, so
+  // they are used only when the bound zero row really is all zeros (always
+  // true for make_zero_row of a float convolution); any other zero row takes
+  // the cp.async path, which reads it.
+  int nonzero = 0;
+  if (a.use_tma_x)
+    for (int i = threadIdx.x; i < a.c_bytes / 16; i += blockDim.x) {
+      const uint4 z = __ldg(reinterpret_cast<const uint4*>(a.zero_row) + i);
+      nonzero |= (z.x | z.y | z.z | z.w) != 0;
+    }
+  const bool tma_gather = a.use_tma_x && !__syncthreads_or(nonzero);
   if (threadIdx.x == 0) {
-    for (int s = 0; s < C::kStages; ++s) {
-      mbar_init(&full[s], 128 + 1);  // 128 producer cp.async arrivals + 1 expect_tx arrival
+    for (int s = 0; s < kStages; ++s) {
+      // TMA path: 1 expect_tx arrival; cp.async path: 128 producer arrivals + 1
+      mbar_init(&full[s], tma_gather ? 1 : 128 + 1);
       mbar_init(&empty[s], 1);       // tcgen05.commit
     }
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&tfull[s], 1);       // tcgen05.commit after the last k-step
-      mbar_init(&tempty[s], 32 * kEpiWarps);   // every epilogue thread
+      mbar_init(&tfull[s], 1);                   // tcgen05.commit after the last K block
+      mbar_init(&tempty[s], 32 * kEpiWarpsS);    // every epilogue thread
     }
     fence_mbar_init();
     tma_prefetch_desc(&tmap_b);
+    if (tma_gather) tma_prefetch_desc(&tmap_x);
   }
   if constexpr (kI8) {
-    // all-ones B tile (16 rows x 128 bytes) for the per-pixel row-sum MMA
-    if (threadIdx.x >= 128 && threadIdx.x < 256) {
+    if (threadIdx.x >= 128 && threadIdx.x < 256) {  // all-ones B tile (16 rows x 128 bytes)
       reinterpret_cast<uint4*>(sOnes)[threadIdx.x - 128] = make_uint4(0x01010101u, 0x01010101u, 0x01010101u,
                                                                       0x01010101u);
       fence_proxy_async_smem();
     }
   }
-  // epilogue constants (bias / folded zero-point terms) for every padded
-  // output channel, staged once per CTA
-  for (int i = threadIdx.x; i < a.n_pad && i < kMaxBias; i += blockDim.x)
-    sBias[i] = __ldg(static_cast<const uint32_t*>(a.bias) + i);
-  if (warp == kMmaWarp) tmem_alloc<C::kTmemCols>(tmem_slot);
+  for (int i = threadIdx.x; i < a.n_pad; i += blockDim.x) sBias[i] = __ldg(static_cast<const uint32_t*>(a.bias) + i);
+  if (warp == kMmaWarpS) tmem_alloc<C::kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -199,76 +153,127 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_tc_kernel(const __grid_cons
 
   if (warp < 4) {
     // ------------------------------------------------------------ producers
-    // Warp w gathers rows [32w, 32w+32) of the A tile.  Each lane loads the
-    // row reference of ONE row per tap (lane l -> row 32w+l, one coalesced
-    // read of the buffer); the references are then shuffled so that 8
-    // consecutive lanes copy the 8 16-byte chunks of one row: every cp.async
-    // instruction moves 4 whole 128-byte rows (full L2 lines), and every
-    // row lands as 128 contiguous (swizzled) shared-memory bytes.
     const int chunk = lane & 7;
     const int sub = lane >> 3;
+    const int slice_elems = a.RS * kBM;
+    const int64_t my_tiles = blockIdx.x < a.total_tiles ? (a.total_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    // cp.async the (R*S taps x 128 pixels) index slice of local tile k into buffer k&1
+    auto stage_index_slice = [&](int64_t k) {
+      if (k < my_tiles) {
+        const int64_t mt = (blockIdx.x + k * gridDim.x) / a.n_tiles;
+        const uint32_t base = smem_u32(sIB + (k & 1) * slice_elems) + threadIdx.x * (int)sizeof(IbT);
+        const IbT* src = static_cast<const IbT*>(a.ib) + first_entry(a, mt, threadIdx.x);   // row = threadIdx.x
+        for (int e = 0; e < a.RS; ++e)
+          cp_async_ca<sizeof(IbT)>(base + e * kBM * (int)sizeof(IbT), src + (int64_t)e * a.mr);
+      }
+      cp_async_commit();
+    };
+    stage_index_slice(0);
+    cp_async_wait_committed();
+    named_bar_sync(1, 128);
     int stage = 0;
     uint32_t phase = 0;
-    STAT_BEGIN(tloop);
-    int64_t tile = blockIdx.x;
-    int64_t ent0 = tile < a.total_tiles ? first_entry(a, tile / a.n_tiles, warp * 32 + lane) : 0;
-    int64_t off_next = tile < a.total_tiles ? load_ref<IbT>(a, ent0) : 0;
-    for (int ti = 0; tile < a.total_tiles; tile += gridDim.x, ++ti) {
-      if (threadIdx.x == 0 && ti < 8) TRACE(26 + ti);
+#ifdef ICV_TRACE
+    long long p_begin = clock64(), p_wait = 0;
+#endif
+    for (int64_t k = 0; k < my_tiles; ++k) {
+      const int64_t tile = blockIdx.x + k * gridDim.x;
+      if (threadIdx.x == 0 && k < 8) TRACE(26 + k);
+      stage_index_slice(k + 1);
+      const IbT* slice = sIB + (k & 1) * slice_elems;
       const int nt = (int)(tile % a.n_tiles);
-      const int64_t next_tile = tile + gridDim.x;
-      int kb = 0;
-      for (int e = 0; e < a.RS; ++e) {
-        const int64_t off_own = off_next;
-        // prefetch the next tap's reference (or the next tile's first tap)
-        if (e + 1 < a.RS) {
-          off_next = load_ref<IbT>(a, ent0 + (int64_t)(e + 1) * a.mr);
-        } else if (next_tile < a.total_tiles) {
-          ent0 = first_entry(a, next_tile / a.n_tiles, warp * 32 + lane);
-          off_next = load_ref<IbT>(a, ent0);
-        }
-        const uint8_t* src[8];
+      if (tma_gather) {
+        // TMA path: warp 0 issues, per K block, one tile::gather4 per lane
+        // (rows 4l..4l+3: pixel-row index = offset / C, ZERO_REF -> row -1,
+        // which TMA zero-fills) plus the filter block; one expect_tx covers
+        // both, so the stage completes without any thread-side arrivals.
+        if (warp == 0) {
+          int kb = 0;
+          for (int e = 0; e < a.RS; ++e) {
+            int32_t rows4[4];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int64_t off = __shfl_sync(0xffffffffu, off_own, 4 * i + sub);
-          src[i] = off < 0 ? a.zero_row : a.x + off * a.elem_bytes;      // ZERO_REF -> bound zero row
-        }
-        for (int cb = 0; cb < a.cblocks; ++cb, ++kb) {
-          const int j = kb % C::kKB;                       // slot within the stage
-          if (j == 0) {
-            STAT_BEGIN(tw);
-            mbar_wait(&empty[stage], phase ^ 1);
-            if (threadIdx.x == 0) {
-              STAT_ADD(0, tw);
-              const int nsub = min(C::kKB, num_kb - kb);
-              mbar_arrive_expect_tx(&full[stage], nsub * C::kBBytes);
+            for (int i = 0; i < 4; ++i) {
+              const int64_t off = (int64_t)slice[e * kBM + 4 * lane + i];
+              rows4[i] = off < 0 ? -1 : pixel_row(a, off);
+            }
+            for (int cb = 0; cb < a.cblocks; ++cb, ++kb) {
+              const int j = kb % C::kKB;
+              if (j == 0) {
+#ifdef ICV_TRACE
+                long long pw0 = clock64();
+#endif
+                mbar_wait(&empty[stage], phase ^ 1);
+#ifdef ICV_TRACE
+                p_wait += clock64() - pw0;
+#endif
+                if (lane == 0)
+                  mbar_arrive_expect_tx(&full[stage], min(C::kKB, num_kb - kb) * (kABytes + C::kBBytes));
+                __syncwarp();
+              }
+              const int slot = stage * C::kKB + j;
+              if (lane == 0) tma_load_2d(sB_u32 + slot * C::kBBytes, &tmap_b, &full[stage], kb * 128, nt * BN);
+              tma_gather4(sA_u32 + slot * kABytes + lane * 512, &tmap_x, &full[stage], cb * a.cblock_elems,
+                          rows4[0], rows4[1], rows4[2], rows4[3]);
+              if (j == C::kKB - 1 || kb == num_kb - 1) {
+                if (++stage == kStages) { stage = 0; phase ^= 1; }
+              }
             }
           }
-          const int slot = stage * C::kKB + j;
-          if (threadIdx.x == 0)
-            tma_load_2d(sB_u32 + slot * C::kBBytes, &tmap_b, &full[stage], kb * 128, nt * BN);
-          const int b = cb * 128 + chunk * 16;
-          int valid = a.c_bytes - b;
-          valid = valid < 0 ? 0 : (valid > 16 ? 16 : valid);
-          const uint32_t dst0 = sA_u32 + slot * kABytes;
+        }
+      } else {
+        // cp.async path (any zero row): 8 lanes per 128-byte row, 4 rows per
+        // instruction, completion tracked by cp.async.mbarrier.arrive
+        int kb = 0;
+        for (int e = 0; e < a.RS; ++e) {
+          const uint8_t* src[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            const int row = warp * 32 + 4 * i + sub;
-            cp_async_16(dst0 + row * 128 + ((chunk ^ (row & 7)) << 4), src[i] + (valid ? b : 0), (uint32_t)valid);
+            const int64_t off = (int64_t)slice[e * kBM + warp * 32 + 4 * i + sub];
+            src[i] = off < 0 ? a.zero_row : a.x + off * a.elem_bytes;  // ZERO_REF -> bound zero row
           }
-          if (j == C::kKB - 1 || kb == num_kb - 1) {
-            cp_async_mbar_arrive_noinc(&full[stage]);
-            if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+          for (int cb = 0; cb < a.cblocks; ++cb, ++kb) {
+            const int j = kb % C::kKB;
+            if (j == 0) {
+#ifdef ICV_TRACE
+              long long pw0 = clock64();
+#endif
+              mbar_wait(&empty[stage], phase ^ 1);
+#ifdef ICV_TRACE
+              p_wait += clock64() - pw0;
+#endif
+              if (threadIdx.x == 0) mbar_arrive_expect_tx(&full[stage], min(C::kKB, num_kb - kb) * C::kBBytes);
+            }
+            const int slot = stage * C::kKB + j;
+            if (threadIdx.x == 0) tma_load_2d(sB_u32 + slot * C::kBBytes, &tmap_b, &full[stage], kb * 128, nt * BN);
+            const int b = cb * 128 + chunk * 16;
+            int valid = a.c_bytes - b;
+            valid = valid < 0 ? 0 : (valid > 16 ? 16 : valid);
+            const uint32_t dst0 = sA_u32 + slot * kABytes;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int row = warp * 32 + 4 * i + sub;
+              cp_async_16(dst0 + row * 128 + ((chunk ^ (row & 7)) << 4), src[i] + (valid ? b : 0), (uint32_t)valid);
+            }
+            if (j == C::kKB - 1 || kb == num_kb - 1) {
+              cp_async_mbar_arrive_noinc(&full[stage]);
+              if (++stage == kStages) { stage = 0; phase ^= 1; }
+            }
           }
         }
       }
+      // slice k+1 landed (its group was committed before this tile's gathers)
+      // and every producer is done reading slice k
+      cp_async_wait_committed();
+      named_bar_sync(1, 128);
     }
-    if (threadIdx.x == 0) STAT_ADD(1, tloop);
-  } else if (warp == kMmaWarp) {
+#ifdef ICV_TRACE
+    if (threadIdx.x == 0) {
+      g_icv_trace[blockIdx.x][37] = (unsigned long long)(clock64() - p_begin);
+      g_icv_trace[blockIdx.x][38] = (unsigned long long)p_wait;
+    }
+#endif
+  } else if (warp == kMmaWarpS) {
     // ------------------------------------------------------------ MMA issuer
-    // The whole warp runs the loop (so stage/descriptor values are
-    // warp-uniform and live in uniform registers); one elected lane issues
-    // the tcgen05.mma / tcgen05.commit instructions.
     constexpr uint32_t idesc = make_idesc<kI8>(kBM, BN);
     constexpr uint32_t idesc_ones = make_idesc<kI8>(kBM, 16);
     const uint64_t ones_desc = sw128_kmajor_desc(smem_u32(sOnes));
@@ -277,18 +282,28 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_tc_kernel(const __grid_cons
     uint32_t phase = 0;
     int as = 0;
     uint32_t aphase = 0;
-    STAT_BEGIN(mloop);
+#ifdef ICV_TRACE
+    long long c_wait_full = 0, c_wait_tempty = 0, c_begin = clock64();
+#endif
     for (int64_t tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
-      STAT_BEGIN(mw);
+#ifdef ICV_TRACE
+      long long c0 = clock64();
+#endif
       mbar_wait(&tempty[as], aphase ^ 1);
-      if (lane == 0) STAT_ADD(3, mw);
+#ifdef ICV_TRACE
+      c_wait_tempty += clock64() - c0;
+#endif
       tc_fence_after();
       const uint32_t d = tmem_base + as * C::kAccStride;
       for (int si = 0; si < stages_per_tile; ++si) {
         const int nsub = min(C::kKB, num_kb - si * C::kKB);
-        STAT_BEGIN(fw);
+#ifdef ICV_TRACE
+        long long c1 = clock64();
+#endif
         mbar_wait(&full[stage], phase);
-        if (lane == 0) { STAT_ADD(2, fw); STAT_INC(7); }
+#ifdef ICV_TRACE
+        c_wait_full += clock64() - c1;
+#endif
         tc_fence_after();
         if (elect_one()) {
           for (int j = 0; j < nsub; ++j) {
@@ -306,7 +321,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_tc_kernel(const __grid_cons
           if (si == stages_per_tile - 1) tc_commit(&tfull[as]);
         }
         __syncwarp();
-        if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
       if (lane == 0) {
         const int ti = (int)((tile - blockIdx.x) / gridDim.x);
@@ -314,137 +329,86 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_tc_kernel(const __grid_cons
       }
       if (++as == 2) { as = 0; aphase ^= 1; }
     }
-    if (lane == 0) STAT_ADD(4, mloop);
-  } else {
-    // ------------------------------------------------------------ epilogue
-    // Epilogue warp e reads TMEM lanes 32*(e%4).. (its 32 rows; the lane
-    // quarter a warp may access is fixed by warp_id % 4) and, with 8
-    // epilogue warps, one half of the tile's columns.  32 columns per
-    // tcgen05.ld; the next chunk's load is in flight while the current one
-    // is converted.  Finished values go through a per-warp staging buffer
-    // so global stores are row-contiguous (16-byte chunks, whole rows).
-    const int ew = warp - 4;
-    const int slot = ew & 3;
-    constexpr int kColGroups = kEpiWarps / 4;
-    constexpr int kColsPerWarp = BN / kColGroups;
-    const int col0 = (ew / 4) * kColsPerWarp;
-    uint8_t* stg = sEpi + ew * 32 * C::kStageRowBytes;
-    const bool vec_ok = kI8 ? (a.K & 15) == 0 : (a.K & 7) == 0;
-    int as = 0;
-    uint32_t aphase = 0;
-    STAT_BEGIN(eloop);
-    for (int64_t tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
-      const int64_t mt = tile / a.n_tiles;
-      const int nt = (int)(tile - mt * a.n_tiles);
-      STAT_BEGIN(ewt);
-      mbar_wait(&tfull[as], aphase);
-      if (threadIdx.x == 128) STAT_ADD(5, ewt);
-      const int ti_ = (int)((tile - blockIdx.x) / gridDim.x);
-      if (threadIdx.x == 128 && ti_ < 8) TRACE(10 + ti_);
-      tc_fence_after();
-      const int64_t row0 = mt * kBM + slot * 32;  // first pixel of this warp's rows
-      const uint32_t taddr = tmem_base + ((uint32_t)(slot * 32) << 16) + as * C::kAccStride;
-      int32_t rowsum = 0;
-      if constexpr (kI8) {
-        uint32_t rs;
-        tmem_ld_32x32b_x1(taddr + BN, rs);
-        tmem_ld_wait();
-        rowsum = (int32_t)rs;
-      }
-      const int nchunks = min(kColsPerWarp, a.K - nt * BN - col0) > 0
-                              ? (min(kColsPerWarp, a.K - nt * BN - col0) + 31) / 32 : 0;
-      uint32_t v[32];
-      if (nchunks > 0) {
-        tmem_ld_32x32b_x32(taddr + col0, v);
-        tmem_ld_wait_regs(v);
-      }
-#pragma unroll 1
-      for (int ci = 0; ci < nchunks; ++ci) {
-        const int c = col0 + ci * 32;
-        const int n = nt * BN + c;
-        uint32_t vn[32];
-        if (ci + 1 < nchunks) tmem_ld_32x32b_x32(taddr + c + 32, vn);
-        uint32_t w[kI8 ? 8 : 16];
-        if constexpr (!kI8) {
-          const float4* bias4 = reinterpret_cast<const float4*>(sBias + n);
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const float4 b = bias4[q];
-            __nv_bfloat162 lo = __floats2bfloat162_rn(__uint_as_float(v[4 * q + 0]) + b.x,
-                                                      __uint_as_float(v[4 * q + 1]) + b.y);
-            __nv_bfloat162 hi = __floats2bfloat162_rn(__uint_as_float(v[4 * q + 2]) + b.z,
-                                                      __uint_as_float(v[4 * q + 3]) + b.w);
-            w[2 * q] = *reinterpret_cast<uint32_t*>(&lo);
-            w[2 * q + 1] = *reinterpret_cast<uint32_t*>(&hi);
-          }
-        } else {
-          const int4* cst4 = reinterpret_cast<const int4*>(sBias + n);
-          const long long corr = -(long long)a.zw * rowsum;
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int4 b = cst4[q];
-            const int bb[4] = {b.x, b.y, b.z, b.w};
-            uint32_t word = 0;
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-              const int32_t acc = (int32_t)((long long)(int32_t)v[4 * q + h] + bb[h] + corr);
-              word |= (uint32_t)requant_u8(acc, a.m0, a.shift, a.zo, a.qmin, a.qmax) << (8 * h);
-            }
-            w[q] = word;
-          }
-        }
-        // stage: lane = row
-        uint4* my = reinterpret_cast<uint4*>(stg + lane * C::kStageRowBytes);
-#pragma unroll
-        for (int q = 0; q < C::kOutRowBytes / 16; ++q) my[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
-        __syncwarp();
-        // write out: lanes cover (row, 16-byte chunk) pairs
-        constexpr int kChunks = C::kOutRowBytes / 16;      // 4 (bf16) or 2 (u8) chunks per row
-        constexpr int kRowsPerPass = 32 / kChunks;
-        constexpr int eb = kI8 ? 1 : 2;
-#pragma unroll
-        for (int pass = 0; pass < 32 / kRowsPerPass; ++pass) {
-          const int rr = pass * kRowsPerPass + lane / kChunks;
-          const int q = lane % kChunks;
-          const int64_t p = row0 + rr;
-          if (p < a.P) {
-            const uint4 val = *reinterpret_cast<const uint4*>(stg + rr * C::kStageRowBytes + q * 16);
-            const int col = n + q * (16 / eb);
-            uint8_t* dst = static_cast<uint8_t*>(a.y) + (p * a.K + col) * eb;
-            if (vec_ok && col + 16 / eb <= a.K) {
-              *reinterpret_cast<uint4*>(dst) = val;
-            } else {
-              const uint8_t* bytes = reinterpret_cast<const uint8_t*>(&val);
-              for (int j = 0; j < 16 / eb; ++j)
-                if (col + j < a.K)
-                  for (int t = 0; t < eb; ++t) dst[j * eb + t] = bytes[j * eb + t];
-            }
-          }
-        }
-        __syncwarp();
-        if (ci + 1 < nchunks) {
-          tmem_ld_wait_regs(vn);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = vn[i];
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(&tempty[as]);
-      if (threadIdx.x == 128 && ti_ < 8) TRACE(18 + ti_);
-      if (++as == 2) { as = 0; aphase ^= 1; }
+#ifdef ICV_TRACE
+    if (lane == 0) {
+      g_icv_trace[blockIdx.x][34] = (unsigned long long)(clock64() - c_begin);
+      g_icv_trace[blockIdx.x][35] = (unsigned long long)c_wait_full;
+      g_icv_trace[blockIdx.x][36] = (unsigned long long)c_wait_tempty;
     }
-    if (threadIdx.x == 128) STAT_ADD(6, eloop);
+#endif
+  } else {
+    epilogue_loop<kI8, BN, kEpiWarpsS, C::kAccStride>(a, warp - 4, lane, tmem_base, sEpi, sBias, tfull, tempty);
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == kMmaWarp) {
+  if (warp == kMmaWarpS) {
     tc_fence_after();
     tmem_dealloc<C::kTmemCols>(tmem_base);
   }
 }
 
-PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+template <bool kI8, int BN, typename IbT>
+int launch_smem(const ConvArgs& c, cudaStream_t st) {
+  auto kernel = igemm_smem_kernel<kI8, BN, IbT>;
+  static std::once_flag attr_once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(attr_once, [&] {
+    attr_err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+  });
+  if (attr_err != cudaSuccess) return cuda_check(attr_err, "cudaFuncSetAttribute(smem)");
+  PlanS pl;
+  if (!plan_smem<kI8, BN, IbT>(c.g.RS(), c.L.n_pad, &pl))
+    return fail(ICV_ERR_UNSUPPORTED, "indirection slice of this kernel size does not fit in shared memory");
+  CUtensorMap tmap, tmap_x;
+  if (int s = make_filter_tmap(c, BN, &tmap)) return s;
+  TcArgs a;
+  fill_tc_args(c, BN, &a);
+  // TMA tile::gather4 for A is correct but ~2.5x slower than the cp.async
+  // gather on B200 (measured); kept behind ICV_TMA_GATHER=1 for experiments.
+  static const char* tg = getenv("ICV_TMA_GATHER");
+  a.use_tma_x = (tg && tg[0] == '1') && make_input_tmap(c, &tmap_x) == ICV_OK;
+  if (!a.use_tma_x) tmap_x = tmap;   // unused placeholder
+  const int sms = sm_count();
+  const int grid = (int)(a.total_tiles < sms ? a.total_tiles : sms);
+  kernel<<<grid, kThreadsS, pl.bytes, st>>>(tmap, tmap_x, a, pl);
+  note_launch();
+  return cuda_check(cudaGetLastError(), "igemm_smem launch");
+}
+
+template <typename IbT>
+int dispatch_smem(const ConvArgs& c, cudaStream_t st) {
+  const int bn = c.L.block_n;
+  if (c.L.family == kFamTcBf16) {
+    if (bn == 64) return launch_smem<false, 64, IbT>(c, st);
+    if (bn == 128) return launch_smem<false, 128, IbT>(c, st);
+    if (bn == 256) return launch_smem<false, 256, IbT>(c, st);
+  } else if (c.L.family == kFamTcU8) {
+    if (bn == 64) return launch_smem<true, 64, IbT>(c, st);
+    if (bn == 128) return launch_smem<true, 128, IbT>(c, st);
+  }
+  return fail(ICV_ERR_UNSUPPORTED, "no tensor-core kernel for this tile width");
+}
+
+bool use_tmem_kernel() {
+  // The TMEM-A kernel (igemm_tmem.cu) is correct but slower than kernel S
+  // on B200 today (its register-staged gathers cannot cover L2 latency);
+  // ICV_TC_KERNEL=tmem selects it for experiments.
+  static const char* sel = getenv("ICV_TC_KERNEL");
+  return sel && sel[0] == 't';
+}
+
+template <bool kI8, int BN>
+bool smem_plan_ok(const ConvArgs& c) {
+  PlanS pl;
+  return c.ib_is_i32 ? plan_smem<kI8, BN, int32_t>(c.g.RS(), c.L.n_pad, &pl)
+                     : plan_smem<kI8, BN, int64_t>(c.g.RS(), c.L.n_pad, &pl);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- host helpers
+PFN_cuTensorMapEncodeTiled_v12000 get_tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
   std::call_once(once, [] {
@@ -457,99 +421,115 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-template <bool kI8, int BN, typename IbT>
-int launch_tc(const ConvArgs& c, cudaStream_t st) {
-  using Cf = Cfg<kI8, BN>;
-  auto kernel = igemm_tc_kernel<kI8, BN, IbT>;
-  static std::once_flag attr_once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(attr_once, [&] {
-    attr_err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::kSmemBytes);
-  });
-  if (attr_err != cudaSuccess) return cuda_check(attr_err, "cudaFuncSetAttribute(smem)");
-
-  auto encode = get_encode();
+int make_filter_tmap(const ConvArgs& c, int block_n, CUtensorMap* tmap) {
+  auto encode = get_tensor_map_encoder();
   if (!encode) return fail(ICV_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  CUtensorMap tmap;
   const cuuint64_t dims[2] = {(cuuint64_t)c.L.row_bytes, (cuuint64_t)c.L.n_pad};
   const cuuint64_t strides[1] = {(cuuint64_t)c.L.row_bytes};
-  const cuuint32_t box[2] = {128, (cuuint32_t)BN};
+  const cuuint32_t box[2] = {128, (cuuint32_t)block_n};
   const cuuint32_t estr[2] = {1, 1};
-  CUresult cr = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(c.packed + c.L.w_off), dims,
+  CUresult cr = encode(tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(c.packed + c.L.w_off), dims,
                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return fail(ICV_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
+  return ICV_OK;
+}
 
-  TcArgs a;
-  a.x = static_cast<const uint8_t*>(c.x);
-  a.zero_row = static_cast<const uint8_t*>(c.zero_row);
-  a.ib = c.ib;
-  a.mr = c.mr;
-  a.P = c.P;
-  a.RS = c.g.RS();
-  a.elem_bytes = kI8 ? 1 : 2;
-  a.c_bytes = c.g.C * a.elem_bytes;
-  a.cblocks = c.L.cblocks;
-  a.K = c.g.K;
-  a.n_tiles = c.L.n_pad / BN;
-  const int64_t m_tiles = (c.P + kBM - 1) / kBM;
-  a.total_tiles = m_tiles * a.n_tiles;
-  a.bias = c.packed + c.L.bias_off;
-  a.y = c.y;
-  a.zw = c.zw; a.zo = c.zo; a.qmin = c.qmin; a.qmax = c.qmax; a.m0 = c.m0; a.shift = c.shift;
-  a.n_pad = c.L.n_pad;
-  if (c.L.n_pad > kMaxBias) return fail(ICV_ERR_UNSUPPORTED, "more than 2048 output channels");
+// 2-D view of the bound input for TMA gathers: rows = N*H*W pixels, columns
+// = C elements; box = one 128-byte channel block of one row; 128-byte
+// swizzle (the A tile's canonical layout).  Rows < 0 or >= N*H*W and
+// columns >= C are zero-filled by TMA.
+int make_input_tmap(const ConvArgs& c, CUtensorMap* tmap) {
+  if (c.L.family != kFamTcBf16 && c.L.family != kFamTcU8) return ICV_ERR_UNSUPPORTED;
+  const int64_t rows = c.g.N * c.g.H * c.g.W;
+  if (rows >= (int64_t(1) << 31)) return ICV_ERR_UNSUPPORTED;
+  if (rows * c.g.C >= (int64_t(1) << 32)) return ICV_ERR_UNSUPPORTED;   // exact 32-bit offset -> row division
+  auto encode = get_tensor_map_encoder();
+  if (!encode) return ICV_ERR_CUDA;
+  const bool i8 = c.L.family == kFamTcU8;
+  const int eb = i8 ? 1 : 2;
+  const cuuint64_t dims[2] = {(cuuint64_t)c.g.C, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)c.g.C * eb};
+  const cuuint32_t box[2] = {(cuuint32_t)(128 / eb), 1};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult cr = encode(tmap, i8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                       const_cast<void*>(c.x), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return cr == CUDA_SUCCESS ? ICV_OK : ICV_ERR_CUDA;
+}
 
+void fill_tc_args(const ConvArgs& c, int block_n, TcArgs* a) {
+  const bool i8 = c.L.family == kFamTcU8;
+  a->x = static_cast<const uint8_t*>(c.x);
+  a->zero_row = static_cast<const uint8_t*>(c.zero_row);
+  a->ib = c.ib;
+  a->mr = c.mr;
+  a->P = c.P;
+  a->RS = c.g.RS();
+  a->elem_bytes = i8 ? 1 : 2;
+  a->c_bytes = c.g.C * a->elem_bytes;
+  a->cblocks = c.L.cblocks;
+  a->K = c.g.K;
+  a->n_tiles = c.L.n_pad / block_n;
+  a->total_tiles = ((c.P + kBM - 1) / kBM) * a->n_tiles;
+  a->bias = c.packed + c.L.bias_off;
+  a->y = c.y;
+  a->zw = c.zw; a->zo = c.zo; a->qmin = c.qmin; a->qmax = c.qmax; a->m0 = c.m0; a->shift = c.shift;
+  a->n_pad = c.L.n_pad;
+  a->cblock_elems = 128 / a->elem_bytes;
+  // exact division of element offsets (multiples of C) by C: C = odd << tz,
+  // off / C = (off >> tz) * odd^-1 (mod 2^32)
+  uint32_t odd = (uint32_t)c.g.C, tz = 0;
+  while ((odd & 1u) == 0) { odd >>= 1; ++tz; }
+  uint32_t inv = odd;                         // Newton iteration for the inverse mod 2^32
+  for (int i = 0; i < 5; ++i) inv *= 2u - odd * inv;
+  a->c_tz = (int32_t)tz;
+  a->c_inv = inv;
+  a->use_tma_x = 0;
+}
+
+int sm_count() {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = (int)(a.total_tiles < sms ? a.total_tiles : sms);
-  kernel<<<grid, kThreads, Cf::kSmemBytes, st>>>(tmap, a);
-  note_launch();
-  return cuda_check(cudaGetLastError(), "igemm_tc launch");
+  return sms;
 }
 
-template <typename IbT>
-int dispatch_bn(const ConvArgs& c, int bn, cudaStream_t st) {
-  if (c.L.family == kFamTcBf16) {
-    if (bn == 64) return launch_tc<false, 64, IbT>(c, st);
-    if (bn == 128) return launch_tc<false, 128, IbT>(c, st);
-    if (bn == 256) return launch_tc<false, 256, IbT>(c, st);
-  } else if (c.L.family == kFamTcU8) {
-    if (bn == 64) return launch_tc<true, 64, IbT>(c, st);
-    if (bn == 128) return launch_tc<true, 128, IbT>(c, st);
-  }
-  return fail(ICV_ERR_UNSUPPORTED, "no tensor-core kernel for this tile width");
-}
+int launch_conv_tmem(const ConvArgs& c, cudaStream_t st);   // igemm_tmem.cu
+bool tmem_kernel_eligible(const ConvArgs& c);                // igemm_tmem.cu
 
-}  // namespace
-
-#ifdef ICV_TRACE
-extern "C" ICV_API int icv_debug_trace(unsigned long long* host, int reset) {
-  if (host && cudaMemcpyFromSymbol(host, g_icv_trace, sizeof(g_icv_trace)) != cudaSuccess) return ICV_ERR_CUDA;
-  if (reset) {
-    static unsigned long long zeros[1024][34];
-    if (cudaMemcpyToSymbol(g_icv_trace, zeros, sizeof(zeros)) != cudaSuccess) return ICV_ERR_CUDA;
-  }
-  return ICV_OK;
+bool tc_kernel_available(const ConvArgs& c) {
+  if (c.L.n_pad > kMaxBias) return false;
+  if (use_tmem_kernel() && tmem_kernel_eligible(c)) return true;
+  const int bn = c.L.block_n;
+  if (c.L.family == kFamTcU8) return bn == 64 ? smem_plan_ok<true, 64>(c) : smem_plan_ok<true, 128>(c);
+  return bn == 64 ? smem_plan_ok<false, 64>(c) : bn == 128 ? smem_plan_ok<false, 128>(c) : smem_plan_ok<false, 256>(c);
 }
-#endif
-
-#ifdef ICV_STATS
-extern "C" ICV_API int icv_debug_stats(unsigned long long* host, int reset) {
-  if (host && cudaMemcpyFromSymbol(host, g_icv_stats, sizeof(g_icv_stats)) != cudaSuccess) return ICV_ERR_CUDA;
-  if (reset) {
-    static unsigned long long zeros[1024][8];
-    if (cudaMemcpyToSymbol(g_icv_stats, zeros, sizeof(zeros)) != cudaSuccess) return ICV_ERR_CUDA;
-  }
-  return ICV_OK;
-}
-#endif
 
 int launch_conv_tc(const ConvArgs& c, cudaStream_t st) {
-  const int bn = c.L.block_n;
-  if (c.ib_is_i32) return dispatch_bn<int32_t>(c, bn, st);
-  return dispatch_bn<int64_t>(c, bn, st);
+  if (c.L.n_pad > kMaxBias) return fail(ICV_ERR_UNSUPPORTED, "more than 2048 output channels");
+  if (use_tmem_kernel() && tmem_kernel_eligible(c)) return launch_conv_tmem(c, st);
+  if (c.ib_is_i32) return dispatch_smem<int32_t>(c, st);
+  return dispatch_smem<int64_t>(c, st);
+}
+
+const char* tc_kernel_name(const ConvArgs& c) {
+  const bool i8 = c.L.family == kFamTcU8;
+  if (use_tmem_kernel() && tmem_kernel_eligible(c)) return i8 ? "icv_igemm_tmem<u8>" : "icv_igemm_tmem<bf16>";
+  return i8 ? "icv_igemm_smem<u8>" : "icv_igemm_smem<bf16>";
 }
 
 }  // namespace icv
+
+#ifdef ICV_TRACE
+extern "C" ICV_API int icv_debug_trace(unsigned long long* host, int reset) {
+  if (host && cudaMemcpyFromSymbol(host, icv::g_icv_trace, sizeof(icv::g_icv_trace)) != cudaSuccess)
+    return ICV_ERR_CUDA;
+  if (reset) {
+    static unsigned long long zeros[1024][40];
+    if (cudaMemcpyToSymbol(icv::g_icv_trace, zeros, sizeof(zeros)) != cudaSuccess) return ICV_ERR_CUDA;
+  }
+  return ICV_OK;
+}
+#endif

@@ -33,7 +33,7 @@ def main():
     icv.indirect_conv(x, pf, ib, w.params, tile, out=y)
     e.record()
     torch.cuda.synchronize()
-    buf = np.zeros((1024, 34), np.uint64)
+    buf = np.zeros((1024, 40), np.uint64)
     fn(buf.ctypes.data, 0)
     tr = buf[:148].astype(np.int64)
     t0 = tr[:, 0][tr[:, 0] > 0].min()
@@ -48,6 +48,15 @@ def main():
         row = " | ".join(f"t{i}: prod {r[26 + i] / 1e3:.2f} mma_end {r[2 + i] / 1e3:.2f} "
                          f"epi {r[10 + i] / 1e3:.2f}-{r[18 + i] / 1e3:.2f}" for i in tiles)
         print(f"cta {cta:3d} entry {r[0] / 1e3:.2f} setup {r[1] / 1e3:.2f} :: {row}")
+    cyc = buf[:148, 34].astype(np.float64)
+    wf = buf[:148, 35].astype(np.float64)
+    wt = buf[:148, 36].astype(np.float64)
+    ns = (tr[:, 2:10].max(axis=1) - tr[:, 1]).astype(np.float64)
+    print(f"MMA warp: loop {cyc.mean():.0f} cycles (mean), waiting on full {wf.mean():.0f}, on tmem-empty {wt.mean():.0f}; "
+          f"effective clock ~{np.median(cyc / np.maximum(ns, 1)):.2f} GHz")
+    pl = buf[:148, 37].astype(np.float64)
+    pw = buf[:148, 38].astype(np.float64)
+    print(f"producer thread 0: loop {pl.mean():.0f} cycles, waiting on empty {pw.mean():.0f}")
     d = rel[:, 3] - rel[:, 2]
     print(f"median tile-1 mainloop (mma_end1 - mma_end0) {np.median(d[d > 0]) / 1e3:.2f} us; "
           f"median epilogue {np.median((rel[:, 18] - rel[:, 10])[rel[:, 10] >= 0]) / 1e3:.2f} us")
