@@ -53,60 +53,63 @@ def load_peaks() -> dict:
 
 # ----------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 100 ms while running."""
+    """SM clock and throttle reasons sampled every 5 ms (NVML) while running;
+    falls back to `nvidia-smi -lms 100` when NVML is unavailable."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
     def __init__(self, device_index: int):
         self.idx = device_index
-        self.samples: list[list[str]] = []
-        self.proc = None
+        self.samples: list[tuple[float, float, int, float]] = []
+        self.stop_evt = threading.Event()
         self.thread = None
+        self.marks: list[tuple[str, int]] = []
+
+    def mark(self, name: str):
+        self.marks.append((name, len(self.samples)))
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except OSError:
-            self.proc = None
-            return self
+            import pynvml
 
-        def reader():
-            for line in self.proc.stdout:
-                self.samples.append([v.strip() for v in line.split(",")])
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.idx)
 
-        self.thread = threading.Thread(target=reader, daemon=True)
-        self.thread.start()
+            def run():
+                while not self.stop_evt.is_set():
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        pw = pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0
+                        self.samples.append((float(sm), float(mx), int(rs), pw))
+                    except Exception:  # pragma: no cover - driver dependent
+                        pass
+                    time.sleep(0.005)
+
+            self.thread = threading.Thread(target=run, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.thread = None
         return self
 
-    def stop(self) -> dict | None:
-        if self.proc is None:
-            return None
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        if self.thread:
+    def stop(self, window: tuple[str, str] | None = None) -> dict | None:
+        self.stop_evt.set()
+        if self.thread is not None:
             self.thread.join(timeout=2)
-        rows = [s for s in self.samples if len(s) == 7]
+        rows = self.samples
+        if window is not None:
+            idx = dict(self.marks)
+            lo, hi = idx.get(window[0], 0), idx.get(window[1], len(rows))
+            if hi > lo:
+                rows = rows[lo:hi]
         if not rows:
             return None
-
-        def num(v):
-            try:
-                return float(v)
-            except ValueError:
-                return float("nan")
-
-        sm = [num(r[0]) for r in rows]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower().startswith("active")})
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(num(r[1]) for r in rows),
-                "power_w_max": max(num(r[2]) for r in rows), "samples": len(rows), "reasons": reasons}
+        reasons = sorted({n for r in rows for n, bit in self.REASONS.items() if r[2] & bit})
+        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
+                "power_w_max": round(max(r[3] for r in rows), 1), "samples": len(rows),
+                "window": "timed steps" if window else "whole run", "reasons": reasons}
 
 
 # ---------------------------------------------------------- CPU reference arm
@@ -213,7 +216,7 @@ def setup_problem(name: str, n_lo: int, n_hi: int, device, pf_bcast=None, mr: in
     return w, x, xh, pf, ib, y, tile
 
 
-def time_steps(fn, steps: int, warmup: int, flush=None):
+def time_steps(fn, steps: int, warmup: int, flush=None, on_timed=None):
     """Per-step CUDA-event times (ms) of fn() on the current stream, with an
     optional L2 flush before every step (outside the events)."""
     import torch
@@ -223,6 +226,8 @@ def time_steps(fn, steps: int, warmup: int, flush=None):
             flush()
         fn()
     torch.cuda.synchronize()
+    if on_timed is not None:
+        on_timed()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
     for i in range(steps):
@@ -254,12 +259,14 @@ def roofline_for(w, ms: float, peaks: dict, sustained: bool = False) -> dict:
 
 
 def load_traffic(name: str):
-    """dram bytes per launch of the conv kernel from the committed ncu capture
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the conv
+    kernel from the committed ncu --set full capture
     (profiles/ncu_traffic.json, written by tools/ncu_summary.py), or None."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            return json.load(f).get(name)
-    except (OSError, ValueError):
+            entry = json.load(f).get(name)
+        return None if entry is None else entry["bytes"]
+    except (OSError, ValueError, KeyError):
         return None
 
 
@@ -309,7 +316,10 @@ def gpu_bench(args) -> None:
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = _lib.launch_count()
-    times = time_steps(step, args.steps, args.warmup, flush)
+    times = time_steps(step, args.steps, args.warmup, flush,
+                       on_timed=(lambda: sampler.mark("t0")) if sampler else None)
+    if sampler:
+        sampler.mark("t1")
     launches = _lib.launch_count() - launches0 - args.warmup
     total_ms = sum(times)
     if world > 1:
@@ -336,7 +346,7 @@ def gpu_bench(args) -> None:
         t = torch.tensor([e2e_total], dtype=torch.float64, device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_total = float(t.item())
-    clocks = sampler.stop() if sampler else None
+    clocks = sampler.stop(("t0", "t1")) if sampler else None
 
     # correctness gate on the benchmarked output (bench.py:124-142 protocol): sampled pixels vs the oracle
     gate = None
