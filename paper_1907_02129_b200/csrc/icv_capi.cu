@@ -58,7 +58,9 @@ int family_for(int32_t dtype, int C, int RS, int K) {
   const bool tc_ok = RS <= kMaxRsTc && K <= 2048;
   switch (dtype) {
     case ICV_F32: return kFamF32Exact;
-    case ICV_BF16: return (C % 8 == 0 && tc_ok) ? kFamTcBf16 : kFamCoreBf16;
+    case ICV_BF16:
+      if (C % 8 == 0 && tc_ok) return kFamTcBf16;
+      return stem_kernel_eligible(C, RS, K) ? kFamStemBf16 : kFamCoreBf16;
     case ICV_U8: return (C % 16 == 0 && tc_ok) ? kFamTcU8 : kFamCoreU8;
     default: return -1;
   }
@@ -67,6 +69,7 @@ int family_for(int32_t dtype, int C, int RS, int K) {
 int tc_block_n(int family, int K) {
   if (family == kFamTcBf16) return K <= 64 ? 64 : (K <= 128 ? 128 : 256);
   if (family == kFamTcU8) return K <= 64 ? 64 : 128;   // + 16 TMEM columns for the row sums
+  if (family == kFamStemBf16) return K <= 64 ? 64 : 128;
   return 0;
 }
 
@@ -87,6 +90,18 @@ int packed_layout(const icv_conv_desc* d, int32_t dtype, PackedLayout* L) {
     L->n_pad = (int)align_up(K, L->block_n);
     L->cblocks = (int)((C * eb + 127) / 128);
     L->row_bytes = RS * L->cblocks * 128;
+    L->w_off = 0;
+    L->w_bytes = (int64_t)L->n_pad * L->row_bytes;
+    L->bias_off = align_up(L->w_bytes, 256);
+    L->bias_bytes = 4 * (int64_t)L->n_pad;
+  } else if (fam == kFamStemBf16) {
+    // one row per output channel: k = e*C + c over the whole receptive field,
+    // zero padded to whole 128-byte blocks of 16-element MMA steps
+    L->block_n = tc_block_n(fam, (int)K);
+    L->n_pad = L->block_n;
+    const int64_t ksteps = (RS * C + 15) / 16;
+    L->cblocks = (int)((ksteps * 16 + 63) / 64);
+    L->row_bytes = (int64_t)L->cblocks * 128;
     L->w_off = 0;
     L->w_bytes = (int64_t)L->n_pad * L->row_bytes;
     L->bias_off = align_up(L->w_bytes, 256);
@@ -217,6 +232,7 @@ static const char* kernel_name_for(const ConvArgs& a) {
     case kFamCoreU8: return "icv_conv_core<u8>";
     case kFamTcBf16:
     case kFamTcU8: return tc_kernel_name(a);
+    case kFamStemBf16: return "icv_igemm_stem<bf16>";
   }
   return "?";
 }
@@ -270,6 +286,7 @@ ICV_API int icv_conv(const icv_conv_desc* desc, const icv_shape4* in, int64_t ba
     case kFamCoreU8: return launch_conv_core(a, st);
     case kFamTcBf16:
     case kFamTcU8: return launch_conv_tc(a, st);
+    case kFamStemBf16: return launch_conv_stem(a, st);
   }
   return fail(ICV_ERR_UNSUPPORTED, "no kernel family");
 }

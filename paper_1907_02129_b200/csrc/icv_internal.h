@@ -26,7 +26,8 @@ struct Geom {
 int make_geom(const icv_conv_desc* d, const icv_shape4* in, Geom* g);
 
 // ---- kernel families ---------------------------------------------------------
-enum Family { kFamF32Exact = 0, kFamTcBf16 = 1, kFamTcU8 = 2, kFamCoreBf16 = 3, kFamCoreU8 = 4 };
+enum Family { kFamF32Exact = 0, kFamTcBf16 = 1, kFamTcU8 = 2, kFamCoreBf16 = 3, kFamCoreU8 = 4, kFamStemBf16 = 5 };
+bool stem_kernel_eligible(int C, int RS, int K);
 constexpr int kMaxRsTc = 24;   // taps per pixel handled by the tensor-core kernels
 int family_for(int32_t dtype, int C, int RS, int K);
 // Output-channel tile width of the tensor-core kernels for this problem.
@@ -66,5 +67,6 @@ int launch_conv_f32_exact(const ConvArgs& a, cudaStream_t st);
 int launch_conv_core(const ConvArgs& a, cudaStream_t st);       // bf16 / u8, any C (CUDA cores)
 int launch_conv_tc(const ConvArgs& a, cudaStream_t st);         // bf16 / u8 tcgen05
 const char* tc_kernel_name(const ConvArgs& a);
+int launch_conv_stem(const ConvArgs& a, cudaStream_t st);   // channel-poor bf16 (tcgen05)
 
 }  // namespace icv

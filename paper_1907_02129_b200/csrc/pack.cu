@@ -51,6 +51,17 @@ __global__ void pack_tc_u8(const uint8_t* __restrict__ w, uint8_t* __restrict__ 
   }
 }
 
+// channel-poor layout: out[n][k] = w[n][k] for k < R*S*C (KRSC order = e*C + c), else 0
+template <typename Tin>
+__global__ void pack_kpacked_bf16(const Tin* __restrict__ w, __nv_bfloat16* __restrict__ out, int K, int kk,
+                                  int kpad, int64_t total) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(i % kpad);
+    const int n = (int)(i / kpad);
+    out[i] = __float2bfloat16_rn((n < K && k < kk) ? to_f32<Tin>(w[(int64_t)n * kk + k]) : 0.f);
+  }
+}
+
 template <typename Tin, typename Tout>
 __global__ void pack_copy(const Tin* __restrict__ w, Tout* __restrict__ out, int64_t total) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -113,6 +124,21 @@ int launch_pack(const Geom& g, const PackedLayout& L, int32_t w_dtype, const voi
       else
         pack_tc_bf16<__nv_bfloat16><<<grid_for(total), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(w), out, g.K,
                                                                        RS, g.C, cpad, total);
+      pack_bias_f32<<<grid_for(L.n_pad), 256, 0, st>>>(static_cast<const float*>(bias),
+                                                         reinterpret_cast<float*>(base + L.bias_off), g.K, L.n_pad);
+      launches = 2;
+      break;
+    }
+    case kFamStemBf16: {
+      const int kpad = L.cblocks * 64;
+      const int64_t total = (int64_t)L.n_pad * kpad;
+      auto* out = reinterpret_cast<__nv_bfloat16*>(base + L.w_off);
+      if (w_dtype == ICV_F32)
+        pack_kpacked_bf16<float><<<grid_for(total), 256, 0, st>>>(static_cast<const float*>(w), out, g.K, (int)kk,
+                                                                   kpad, total);
+      else
+        pack_kpacked_bf16<__nv_bfloat16><<<grid_for(total), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(w), out,
+                                                                           g.K, (int)kk, kpad, total);
       pack_bias_f32<<<grid_for(L.n_pad), 256, 0, st>>>(static_cast<const float*>(bias),
                                                          reinterpret_cast<float*>(base + L.bias_off), g.K, L.n_pad);
       launches = 2;

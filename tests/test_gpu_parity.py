@@ -192,7 +192,11 @@ def test_bf16_full_config_sampled_pixels(w):
     dict(r=1, s=1, c=256, k=512, n=3, h=7, w=7, mr=128),                # pointwise, 2 N tiles
     dict(r=3, s=2, sy=2, sx=1, dy=2, dx=1, pt=2, pl=1, pb=0, pr=2, c=16, k=40, n=2, h=10, w=9, mr=1),
     dict(r=5, s=5, pt=2, pl=2, c=8, k=24, n=1, h=6, w=6, mr=4),         # C=8: single 16-byte chunk
-    dict(r=7, s=7, sy=2, sx=2, pt=3, pl=3, c=3, k=64, n=2, h=20, w=18, mr=4),   # channel-poor (CUDA cores)
+    dict(r=7, s=7, sy=2, sx=2, pt=3, pl=3, c=3, k=64, n=2, h=20, w=18, mr=4),   # channel-poor stem (tcgen05)
+    dict(r=7, s=7, sy=2, sx=2, pt=3, pl=3, c=3, k=100, n=1, h=15, w=17, mr=128),  # stem, K tail in a 128 tile
+    dict(r=3, s=3, pt=1, pl=1, c=3, k=24, n=3, h=9, w=11, mr=3),        # 3x3 first layer, K < tile
+    dict(r=3, s=3, sy=2, sx=2, pt=0, pl=1, pb=2, pr=0, c=1, k=40, n=2, h=13, w=10, mr=1),   # C=1
+    dict(r=5, s=5, pt=2, pl=2, c=5, k=16, n=1, h=8, w=8, mr=4),         # channel-poor, CUDA-core variant
 ])
 @pytest.mark.parametrize("index_dtype", [torch.int64, torch.int32])
 def test_bf16_edge_geometries(geom, index_dtype):
