@@ -180,7 +180,7 @@ def cpu_reference(name: str, steps: int, warmup: int, cores: int | None = None) 
 
 
 # ---------------------------------------------------------------- GPU arm
-def setup_problem(name: str, n_lo: int, n_hi: int, device, pf_bcast=None, mr: int = 128):
+def setup_problem(name: str, n_lo: int, n_hi: int, device, pf_bcast=None, mr: int = 128, per_image: bool = True):
     """Upload images [n_lo, n_hi) of workload `name`, build the IB on the
     device, pack (or receive) the filter."""
     import torch
@@ -211,7 +211,7 @@ def setup_problem(name: str, n_lo: int, n_hi: int, device, pf_bcast=None, mr: in
         pf_bcast(pf)
     zero = icv.make_zero_row(p.in_channels, dtype=dt, device=device, fill=zero_fill)
     out_shape = icv.conv_output_shape(p, shape)
-    ib = icv.init_indirection_buffer(x, zero, p, out_shape, tile)
+    ib = icv.init_indirection_buffer(x, zero, p, out_shape, tile, per_image=per_image)
     y = icv.NhwcTensor.empty(out_shape, dtype=dt, device=device)
     return w, x, xh, pf, ib, y, tile
 
@@ -301,7 +301,7 @@ def gpu_bench(args) -> None:
     import paper_1907_02129_b200.workloads as wl
     wl.CONFIGS["_bench"] = big
     w, x, xh, pf, ib, y, tile = setup_problem("_bench", rank * per_rank, (rank + 1) * per_rank, device, bcast,
-                                              mr=args.mr)
+                                              mr=args.mr, per_image=args.ib == "per-image")
     flush_buf = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=device)
 
     def flush():
@@ -359,7 +359,7 @@ def gpu_bench(args) -> None:
             if oname == name:
                 continue
             ow_, ox, _, opf, oib_, oy, otile = setup_problem(oname, 0, CONFIGS[oname].in_shape.n, device,
-                                                             mr=args.mr)
+                                                             mr=args.mr, per_image=args.ib == "per-image")
             ot = time_steps(lambda: icv.indirect_conv(ox, opf, oib_, ow_.params, otile, out=oy),
                             max(10, args.steps // 5), 3, flush)
             oms = statistics.median(ot)
@@ -401,7 +401,7 @@ def gpu_bench(args) -> None:
         "config": {"workload": w0.name, "batch_per_gpu": per_rank, "global_batch": per_rank * world,
                    "H": w0.in_shape.h, "W": w0.in_shape.w, "C": w0.in_shape.c, "K": w0.params.out_channels,
                    "kernel": f"{w0.params.kernel_h}x{w0.params.kernel_w}", "parallelism": f"dp{world} (batch-sharded)",
-                   "mr": args.mr, "index_dtype": "int64",
+                   "mr": args.mr, "index_dtype": "int64", "ib_layout": args.ib,
                    "l2": "flushed between steps (256 MiB device write, outside the timed events)",
                    "conv_kernel": _lib.kernel_name(w0.params, w0.in_shape, x.dtype)},
         "roofline": roof,
@@ -470,6 +470,8 @@ def main() -> None:
     ap.add_argument("--impl", choices=["icv", "reference"], default="icv")
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--mr", type=int, default=128)
+    ap.add_argument("--ib", choices=["per-image", "canonical"], default="per-image",
+                    help="indirection-buffer form the kernels read (DESIGN.md §3)")
     ap.add_argument("--no-other", action="store_true", help="skip the per-config extra measurements")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-gate", action="store_true")

@@ -51,6 +51,15 @@ typedef enum icv_dtype {
   ICV_I64 = 4
 } icv_dtype;
 
+/* Indirection-buffer layout flag, OR-ed into the `ib_dtype` arguments.
+ * Canonical (flag clear): the reference's (T, R*S, mr) buffer over all
+ * `batch` images, T = ceil(batch*Ho*Wo / mr).  Per-image (flag set): the
+ * buffer of image 0 only, T = ceil(Ho*Wo / mr); entry (n, q, e) of the
+ * canonical buffer equals entry (0, q, e) + n*H*W*C (ZERO_REF kept), so one
+ * small, L2-resident buffer serves any batch (SPEC.md:325 leaves the row
+ * reference representation to the implementation). */
+#define ICV_IB_PER_IMAGE 0x100
+
 /* Convolution geometry; field-for-field convbench.tensors.ConvParams
  * (tensors.py:41-72). */
 typedef struct icv_conv_desc {
@@ -105,7 +114,8 @@ ICV_API int icv_ib_entries(const icv_conv_desc* desc, const icv_shape4* in, int6
  * Replaces _compute_offsets (indirect.py:98-126) as called by
  * init_indirection_buffer (:129-164; first_tile = 0) and
  * update_for_batch_growth (:185-192; first_tile = old full-tile count).
- * `ib` points at the START of the buffer (tile 0). */
+ * `ib` points at the START of the buffer (tile 0).  With ICV_IB_PER_IMAGE
+ * in `ib_dtype` the per-image buffer is written and `batch` is ignored. */
 ICV_API int icv_ib_build(const icv_conv_desc* desc, const icv_shape4* in, int64_t batch, int32_t mr,
                  int64_t first_tile, int32_t ib_dtype, void* ib, void* stream);
 

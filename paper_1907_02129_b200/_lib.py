@@ -21,6 +21,7 @@ LIB_PATH = os.environ.get("ICV_LIB") or os.path.join(os.path.dirname(os.path.abs
 
 ICV_OK, ICV_ERR_ARG, ICV_ERR_GEOMETRY, ICV_ERR_STALE, ICV_ERR_UNSUPPORTED, ICV_ERR_CUDA = 0, -1, -2, -3, -4, -5
 ICV_F32, ICV_BF16, ICV_U8, ICV_I32, ICV_I64 = 0, 1, 2, 3, 4
+ICV_IB_PER_IMAGE = 0x100
 
 TORCH_TO_ICV = {torch.float32: ICV_F32, torch.bfloat16: ICV_BF16, torch.uint8: ICV_U8,
                 torch.int32: ICV_I32, torch.int64: ICV_I64}

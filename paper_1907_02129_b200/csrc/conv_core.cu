@@ -57,7 +57,8 @@ struct CoreArgs {
   const void* zero_row;
   const void* ib;
   int ib_is_i32;
-  int64_t mr, P;
+  int ib_per_image;
+  int64_t mr, P, ohw, img_elems;
   int RS, C, K;
   const void* w;       // KRSC, compute dtype
   const void* bias;    // f32 (float modes) / int32 (u8)
@@ -113,9 +114,16 @@ __global__ void __launch_bounds__(NT) conv_core_kernel(CoreArgs a) {
     if (tid < BM) {
       int64_t p = m0 + tid;
       p = p < a.P ? p : a.P - 1;                        // clamped lane (indirect.py:111)
+      int64_t base = 0;
+      if (a.ib_per_image) {                             // image-relative buffer of image 0
+        const int64_t n = p / a.ohw;
+        p -= n * a.ohw;
+        base = n * a.img_elems;
+      }
       const int64_t ent = ((p / a.mr) * a.RS + e) * a.mr + p % a.mr;
-      const int64_t off = a.ib_is_i32 ? (int64_t) static_cast<const int32_t*>(a.ib)[ent]
-                                      : static_cast<const int64_t*>(a.ib)[ent];
+      int64_t off = a.ib_is_i32 ? (int64_t) static_cast<const int32_t*>(a.ib)[ent]
+                                : static_cast<const int64_t*>(a.ib)[ent];
+      if (off >= 0) off += base;
       rows[tid] = off < 0 ? zero : x + off;             // ZERO_REF -> zero row (indirect.py:291)
     }
     for (int c0 = 0; c0 < a.C; c0 += BK) {
@@ -168,6 +176,9 @@ int launch_mode(const ConvArgs& c, cudaStream_t st) {
   a.zero_row = c.zero_row;
   a.ib = c.ib;
   a.ib_is_i32 = c.ib_is_i32;
+  a.ib_per_image = c.ib_per_image;
+  a.ohw = c.g.OH * c.g.OW;
+  a.img_elems = c.g.H * c.g.W * (int64_t)c.g.C;
   a.mr = c.mr;
   a.P = c.P;
   a.RS = c.g.RS();

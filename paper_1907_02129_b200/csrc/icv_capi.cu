@@ -169,8 +169,11 @@ ICV_API int icv_ib_build(const icv_conv_desc* desc, const icv_shape4* in, int64_
   if (int s = make_geom(desc, in, &g)) return s;
   if (mr < 1) return fail(ICV_ERR_ARG, "mr must be >= 1");
   if (batch < 1 || batch > in->n) return fail(ICV_ERR_ARG, "batch must be within the physical input batch");
+  const bool per_image = (ib_dtype & ICV_IB_PER_IMAGE) != 0;
+  ib_dtype &= ~ICV_IB_PER_IMAGE;
   if (ib_dtype != ICV_I64 && ib_dtype != ICV_I32) return fail(ICV_ERR_ARG, "ib dtype must be int64 or int32");
   if (!ib) return fail(ICV_ERR_ARG, "null ib");
+  if (per_image) batch = 1;   // image 0's buffer serves every image
   const int64_t pixels = batch * g.OH * g.OW;
   const int64_t tiles = (pixels + mr - 1) / mr;
   if (first_tile < 0 || first_tile > tiles) return fail(ICV_ERR_ARG, "first_tile out of range");
@@ -253,6 +256,8 @@ ICV_API int icv_conv(const icv_conv_desc* desc, const icv_shape4* in, int64_t ba
   if (int s = make_geom(desc, in, &a.g)) return s;
   if (batch < 1 || batch > in->n) return fail(ICV_ERR_ARG, "batch must be within the physical input batch");
   if (mr < 1) return fail(ICV_ERR_ARG, "mr must be >= 1");
+  a.ib_per_image = (ib_dtype & ICV_IB_PER_IMAGE) != 0;
+  ib_dtype &= ~ICV_IB_PER_IMAGE;
   if (ib_dtype != ICV_I64 && ib_dtype != ICV_I32) return fail(ICV_ERR_ARG, "ib dtype must be int64 or int32");
   if (!x || !zero_row || !ib || !packed || !y) return fail(ICV_ERR_ARG, "null tensor pointer");
   if (int s = packed_layout(desc, dtype, &a.L)) return s;

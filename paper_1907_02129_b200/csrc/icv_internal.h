@@ -57,6 +57,7 @@ struct ConvArgs {
   const void* zero_row;
   const void* ib;
   int32_t ib_is_i32;
+  int32_t ib_per_image;  // entries are image-relative (ICV_IB_PER_IMAGE)
   const uint8_t* packed;
   PackedLayout L;
   void* y;

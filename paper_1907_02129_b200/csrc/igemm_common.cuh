@@ -51,17 +51,33 @@ struct TcArgs {
   int32_t c_tz;              // C = odd << c_tz
   uint32_t c_inv;            // odd^-1 mod 2^32
   int32_t use_tma_x;         // input tensor map valid (TMA gathers allowed)
+  int32_t ib_per_image;      // buffer holds image 0's (image-relative) references
+  int64_t ohw, img_elems;    // Ho*Wo, H*W*C
 };
 
-// First buffer entry of output pixel p = tile_m*128 + row, clamped to the
-// last real pixel (indirect.py:111): ((p / mr) * RS) * mr + p % mr.  Tap e
-// adds e * mr (layout: tile-major, kernel element, lane; indirect.py:14-16).
-__device__ __forceinline__ int64_t first_entry(const TcArgs& a, int64_t tile_m, int row) {
+// Where the references of output pixel p = tile_m*128 + row live: entry of
+// tap 0 (tap e adds e*mr; layout tile-major, kernel element, lane,
+// indirect.py:14-16) and the element offset to add to non-ZERO_REF entries.
+// p is clamped to the last real pixel (indirect.py:111).  Canonical buffer:
+// entry ((p / mr) * RS) * mr + p % mr, base 0.  Per-image buffer: the same for
+// q = p mod (Ho*Wo) in image 0's buffer, base n*H*W*C.
+struct RowRef {
+  int64_t ent0;
+  int64_t base;
+};
+__device__ __forceinline__ RowRef row_ref(const TcArgs& a, int64_t tile_m, int row) {
   int64_t p = tile_m * kBM + row;
   p = p < a.P ? p : a.P - 1;
+  int64_t base = 0;
+  if (a.ib_per_image) {
+    const int64_t n = p / a.ohw;
+    p -= n * a.ohw;
+    base = n * a.img_elems;
+  }
   const int64_t t = p / a.mr;
-  return t * a.RS * a.mr + (p - t * a.mr);
+  return {t * a.RS * a.mr + (p - t * a.mr), base};
 }
+__device__ __forceinline__ int64_t resolve_ref(int64_t raw, int64_t base) { return raw < 0 ? raw : raw + base; }
 
 // Pixel-row index of an element offset (offsets are multiples of C).
 __device__ __forceinline__ int32_t pixel_row(const TcArgs& a, int64_t off) {

@@ -14,28 +14,49 @@
 // x K) stays resident in smem for the whole kernel (one TMA load), the MMA
 // warp issues ceil(R*S*C/16) tcgen05.mma per 128-pixel tile, and the shared
 // epilogue streams the bf16 output (the dominant HBM traffic of the layer).
+#include <climits>
+
 #include "igemm_common.cuh"
 
 namespace icv {
 namespace {
 
+constexpr int kProdWarpsStem = 8;        // two producer threads per A row (tap halves)
+constexpr int kProdThreads = 32 * kProdWarpsStem;
 constexpr int kEpiWarpsStem = 4;
-constexpr int kMmaWarpStem = 8;
+constexpr int kMmaWarpStem = kProdWarpsStem + kEpiWarpsStem;
 constexpr int kThreadsStem = 32 * (kMmaWarpStem + 1);
-constexpr int kStagesStem = 3;
+constexpr int kStagesStem = 2;          // A tiles in flight
+constexpr int kWinBufs = 3;             // input windows in flight (tile k assembling, k+1 landing, k+2 issued)
 
 template <int C, int RS, int BN>
 struct CfgStem {
   static constexpr int kK = RS * C;                         // real reduction length
   static constexpr int kKSteps = (kK + 15) / 16;            // MMA K steps (16 bf16 each)
   static constexpr int kBlocks = (kKSteps * 16 + 63) / 64;  // 128-byte K blocks per row
-  static constexpr int kWords = kBlocks * 32;               // 32-bit words per A row
   static constexpr int kABytes = kBM * kBlocks * 128;       // one A tile
   static constexpr int kBBytes = BN * kBlocks * 128;        // resident filter
   static constexpr int kEpiBytes = kEpiWarpsStem * 32 * 80;
-  static constexpr int kSmemBytes = 1024 + kStagesStem * kABytes + kBBytes + kEpiBytes + 4 * 256 + 256;
+  // Taps are assembled in groups of 8: 8 taps x C elements = C whole 16-byte
+  // chunks of the A row.  kGroups groups cover the kKSteps*16 elements the
+  // MMA reads (taps past R*S read a zero slot); the two producer halves take
+  // groups [0, kG0) and [kG0, kGroups).
+  static constexpr int kGroups = (kKSteps * 2 + C - 1) / C;
+  static constexpr int kG0 = (kGroups + 1) / 2;
+  static constexpr int kTapsHalf = kG0 * 8;                 // taps per producer thread (max)
+  static constexpr int kTaps = kGroups * 8;
+  // elements per staged input window: 16 KB of bf16 (8 KB when a 128-wide
+  // resident filter leaves less room); two 8-element slots follow it: the
+  // bound zero row (ZERO_REF taps) and true zeros (taps past R*S)
+  static constexpr int kWinElems = (BN <= 64 || RS * C <= 64) ? 8192 : 4096;
+  static constexpr int kWinBytes = kWinElems * 2 + 32;
+  static constexpr int kRelBytes = kTaps * kBM * 2;         // [kTaps/2][128][2] uint16 window indices
+  static constexpr int kMiscBytes = 1024;                   // bias, reductions, window bases
+  static constexpr int kSmemBytes = 1024 + kStagesStem * kABytes + kBBytes + kEpiBytes + kWinBufs * kWinBytes +
+                                    kWinBufs * kRelBytes + kMiscBytes + 256;
   static_assert(kSmemBytes <= 232448, "shared memory overflow");
   static_assert(C >= 1 && C <= 4, "channel-poor kernel handles 1..4 channels");
+  static_assert(kGroups * C * 8 <= kBlocks * 64, "tap groups overflow the A row");
 };
 
 // 16-byte chunk q (elements 8q .. 8q+7) of row `row` in the swizzled A tile.
@@ -44,17 +65,49 @@ __device__ __forceinline__ uint32_t a_chunk_addr(uint32_t tile, int row, int q) 
   return tile + blk * (kBM * 128) + row * 128 + ((j ^ (row & 7)) << 4);
 }
 
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
+// Place tap i (0..7) of a group -- its C elements are the low 16*C bits of
+// (hi:lo) -- at element i*C of the group's 4*C words.
+template <int C>
+__device__ __forceinline__ void place_tap(uint32_t (&w)[4 * C], int i, uint32_t lo, uint32_t hi) {
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    const uint32_t v = c < 2 ? (lo >> (16 * c)) & 0xFFFFu : (hi >> (16 * (c - 2))) & 0xFFFFu;
+    const int k = i * C + c;
+    if (k & 1) w[k >> 1] |= v << 16;
+    else w[k >> 1] = v;
+  }
+}
+
+template <int C>
+__device__ __forceinline__ void store_group(const uint32_t (&w)[4 * C], uint32_t tileA, int row, int g) {
+#pragma unroll
+  for (int j = 0; j < C; ++j)
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a_chunk_addr(tileA, row, g * C + j)),
+                 "r"(w[4 * j]), "r"(w[4 * j + 1]), "r"(w[4 * j + 2]), "r"(w[4 * j + 3]) : "memory");
+}
+
 template <int C, int RS, int BN, typename IbT>
 __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __grid_constant__ CUtensorMap tmap_b,
-                                                                     const TcArgs a, int64_t x_elems) {
+                                                                     const TcArgs a, int32_t x_elems) {
   using Cf = CfgStem<C, RS, BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = sA + kStagesStem * Cf::kABytes;
   uint8_t* sEpi = sB + Cf::kBBytes;
-  uint32_t* sBias = reinterpret_cast<uint32_t*>(sEpi + Cf::kEpiBytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sBias) + 4 * 256);
+  uint8_t* sWin = sEpi + Cf::kEpiBytes;                              // [3] windows (+ zero slots)
+  uint8_t* sRel = sWin + kWinBufs * Cf::kWinBytes;                   // [3][kTaps/2][128][2] uint16
+  uint8_t* sMisc = sRel + kWinBufs * Cf::kRelBytes;
+  uint32_t* sBias = reinterpret_cast<uint32_t*>(sMisc);                         // 128 x 4 B
+  int32_t* sRed = reinterpret_cast<int32_t*>(sMisc + 512);                      // [3][2][8] min/max per warp
+  int32_t* sWinLo = reinterpret_cast<int32_t*>(sMisc + 512 + 192);              // [3] window start (or -1)
+  uint64_t* full = reinterpret_cast<uint64_t*>(sMisc + Cf::kMiscBytes);
   uint64_t* empty = full + kStagesStem;
   uint64_t* tfull = empty + kStagesStem;
   uint64_t* tempty = tfull + 2;
@@ -65,7 +118,7 @@ __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __gri
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStagesStem; ++s) {
-      mbar_init(&full[s], 128);   // every producer thread (st.shared + proxy fence + arrive)
+      mbar_init(&full[s], kProdThreads);   // every producer thread (st.shared + proxy fence + arrive)
       mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
@@ -77,6 +130,13 @@ __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __gri
     tma_prefetch_desc(&tmap_b);
   }
   for (int i = threadIdx.x; i < a.n_pad; i += blockDim.x) sBias[i] = __ldg(static_cast<const uint32_t*>(a.bias) + i);
+  if (threadIdx.x < kWinBufs * 8) {   // zero slots behind every window: bound zero row, then true zeros
+    const int b = threadIdx.x >> 3, j = threadIdx.x & 7;
+    const uint16_t* z = reinterpret_cast<const uint16_t*>(a.zero_row);
+    uint16_t* slot = reinterpret_cast<uint16_t*>(sWin + b * Cf::kWinBytes) + Cf::kWinElems;
+    slot[j] = j < C ? __ldg(z + j) : (uint16_t)0;
+    slot[8 + j] = 0;
+  }
   if (warp == kMmaWarpStem) tmem_alloc<(2 * BN <= 128 ? 128 : 256)>(tmem_slot);
   tc_fence_before();
   __syncthreads();
@@ -90,62 +150,176 @@ __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __gri
     for (int b = 0; b < Cf::kBlocks; ++b) tma_load_2d(sB_u32 + b * BN * 128, &tmap_b, bfull, b * 128, 0);
   }
 
-  if (warp < 4) {
+  if (warp < kProdWarpsStem) {
     // ------------------------------------------------------------ producers
-    const int row = threadIdx.x;
+    // Thread (half, row) assembles half of A row `row` (one output pixel).
+    // Per tile, the row references of its 128 pixels (indirection buffer)
+    // bound the span of input elements the tile reads; that span (the
+    // "window") is copied into smem with coalesced 16-byte cp.async two
+    // tiles ahead, the references become 16-bit window indices, and rows are
+    // assembled from the window with shared-memory loads.  A window larger
+    // than the buffer (never for the ResNet stem) falls back to reading the
+    // taps straight from global memory.
+    const int half = warp >> 2;
+    const int row = threadIdx.x & (kBM - 1);
+    const int g_begin = half ? Cf::kG0 : 0;
+    const int g_end = half ? Cf::kGroups : Cf::kG0;
+    const int e_begin = g_begin * 8;
+    const int n_taps = (g_end - g_begin) * 8;
     const uint32_t* x32 = reinterpret_cast<const uint32_t*>(a.x);
-    const uint16_t* x16 = reinterpret_cast<const uint16_t*>(a.x);
-    const uint16_t* z16 = reinterpret_cast<const uint16_t*>(a.zero_row);
+    const uint32_t sWin_u32 = smem_u32(sWin);
+    const uint32_t sRel_u32 = smem_u32(sRel);
+    const int64_t my_tiles = blockIdx.x < a.total_tiles ? (a.total_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    constexpr int32_t kPad = -2;        // tap past R*S
+    int32_t ref[Cf::kTapsHalf];         // resolved element offsets (ZERO_REF = -1, padding = -2)
+
+    auto load_refs = [&](int64_t k) {   // row references of local tile k -> registers
+      if (k >= my_tiles) return;
+      const RowRef rr = row_ref(a, blockIdx.x + k * gridDim.x, row);
+      const IbT* ib = static_cast<const IbT*>(a.ib) + rr.ent0 + (int64_t)e_begin * a.mr;
+      const int32_t base = (int32_t)rr.base;
+#pragma unroll
+      for (int i = 0; i < Cf::kTapsHalf; ++i) {
+        if (i < n_taps && e_begin + i < RS) {
+          const int32_t raw = (int32_t)__ldg(ib + (int64_t)i * a.mr);
+          ref[i] = raw + (base & ~(raw >> 31));          // ZERO_REF (-1) stays -1
+        } else {
+          ref[i] = kPad;
+        }
+      }
+    };
+    // window of local tile k: CTA-wide min/max of the valid offsets, window
+    // indices -> sRel, 16-byte cp.async copies -> sWin
+    auto prepare = [&](int64_t k) {
+      const int buf = (int)(k % kWinBufs);
+      if (k < my_tiles) {
+        uint32_t lo = 0xFFFFFFFFu;
+        int32_t hi = -1;
+#pragma unroll
+        for (int i = 0; i < Cf::kTapsHalf; ++i) {
+          lo = min(lo, ref[i] >= 0 ? (uint32_t)ref[i] : 0xFFFFFFFFu);
+          hi = max(hi, ref[i]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+          hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        if (lane == 0) { sRed[buf * 16 + warp] = (int32_t)lo; sRed[buf * 16 + 8 + warp] = hi; }
+      }
+      named_bar_sync(1, kProdThreads);
+      if (k < my_tiles) {
+        uint32_t lo = 0xFFFFFFFFu;
+        int32_t hi = -1;
+#pragma unroll
+        for (int i = 0; i < kProdWarpsStem; ++i) {
+          lo = min(lo, (uint32_t)sRed[buf * 16 + i]);
+          hi = max(hi, sRed[buf * 16 + 8 + i]);
+        }
+        const int32_t w0 = hi < 0 ? 0 : (int32_t)(lo & ~7u);        // 16-byte aligned start
+        const int32_t w1 = hi < 0 ? 0 : ((hi + C + 7) & ~7);          // covers the last reference's C elements
+        const bool fits = w1 - w0 <= Cf::kWinElems;
+        if (threadIdx.x == 0) sWinLo[buf] = fits ? w0 : -1;
+        const uint32_t rel_base = sRel_u32 + buf * Cf::kRelBytes + ((g_begin * 4) * kBM + row) * 4;
+#pragma unroll
+        for (int i = 0; i < Cf::kTapsHalf; i += 2) {
+          if (i < n_taps) {
+            uint32_t r2 = 0;
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const int32_t r = ref[i + j];
+              const uint32_t rel = r >= 0 ? (uint32_t)(r - w0) : (r == -1 ? Cf::kWinElems : Cf::kWinElems + 8);
+              r2 |= rel << (16 * j);
+            }
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(rel_base + (i / 2) * kBM * 4), "r"(r2) : "memory");
+          }
+        }
+        if (fits) {
+          const uint32_t dst = sWin_u32 + buf * Cf::kWinBytes;
+          for (int32_t ch = threadIdx.x; ch * 8 < w1 - w0; ch += kProdThreads) {
+            const int32_t e0 = w0 + ch * 8;
+            int32_t valid = (x_elems - e0) * 2;
+            valid = valid < 0 ? 0 : (valid > 16 ? 16 : valid);
+            cp_async_16(dst + (uint32_t)ch * 16, a.x + (valid ? (int64_t)e0 * 2 : 0), (uint32_t)valid);
+          }
+        }
+      }
+      cp_async_commit();
+    };
+
+    // prologue: windows of tiles 0 and 1
+    load_refs(0);
+    prepare(0);
+    load_refs(1);
+    prepare(1);
     int stage = 0;
     uint32_t phase = 0;
-    for (int64_t tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
-      const IbT* ref = static_cast<const IbT*>(a.ib) + first_entry(a, tile, row);
-      int64_t offs[RS];
-#pragma unroll
-      for (int e = 0; e < RS; ++e) offs[e] = (int64_t)__ldg(ref + (int64_t)e * a.mr);
+    for (int64_t k = 0; k < my_tiles; ++k) {
+      load_refs(k + 2);                       // lands while tile k is assembled
+      asm volatile("cp.async.wait_group 1;" ::: "memory");   // window k (window k+1 may still fly)
+      named_bar_sync(1, kProdThreads);
+      const int buf = (int)(k % kWinBufs);
+      const bool in_window = sWinLo[buf] >= 0;
       mbar_wait(&empty[stage], phase ^ 1);
       const uint32_t tileA = sA_u32 + stage * Cf::kABytes;
-      uint32_t w[Cf::kWords];
+      if (in_window) {
+        const uint32_t win = sWin_u32 + buf * Cf::kWinBytes;
+        const uint32_t rel_base = sRel_u32 + buf * Cf::kRelBytes + row * 4;
+#pragma unroll 1
+        for (int g = g_begin; g < g_end; ++g) {
+          uint32_t w[4 * C];
 #pragma unroll
-      for (int i = 0; i < Cf::kWords; ++i) w[i] = 0u;
+          for (int i = 0; i < 8; i += 2) {
+            const uint32_t r2 = lds32(rel_base + (g * 4 + i / 2) * kBM * 4);
 #pragma unroll
-      for (int e = 0; e < RS; ++e) {
-        const int64_t off = offs[e];
-        uint32_t h[C];
-        if (off >= 0) {
-          // C elements at element offset `off`: two aligned words + funnel shift
-          const int64_t wi = off >> 1;
-          const uint32_t w0 = __ldg(x32 + wi);
-          uint32_t w1 = 0u;
-          if (2 * (wi + 1) + 1 < x_elems) w1 = __ldg(x32 + wi + 1);
-          else if (2 * (wi + 1) < x_elems) w1 = (uint32_t)__ldg(x16 + 2 * (wi + 1));
-          const uint64_t v = ((uint64_t)w1 << 32 | w0) >> ((off & 1) * 16);
-#pragma unroll
-          for (int c = 0; c < C; ++c) h[c] = (uint32_t)(v >> (16 * c)) & 0xFFFFu;
-        } else {
-#pragma unroll
-          for (int c = 0; c < C; ++c) h[c] = __ldg(z16 + c);    // ZERO_REF -> bound zero row
+            for (int j = 0; j < 2; ++j) {
+              const uint32_t rel = j ? r2 >> 16 : r2 & 0xFFFFu;
+              const uint32_t addr = win + ((rel * 2) & ~3u);
+              const uint32_t sh = (rel & 1) * 16;
+              const uint32_t lo = lds32(addr), hi = lds32(addr + 4);
+              place_tap<C>(w, i + j, __funnelshift_r(lo, hi, sh), hi >> sh);
+            }
+          }
+          store_group<C>(w, tileA, row, g);
         }
+      } else {
+        // window too large: read the taps from global memory
+        const RowRef rr = row_ref(a, blockIdx.x + k * gridDim.x, row);
+        const IbT* ib = static_cast<const IbT*>(a.ib) + rr.ent0;
+#pragma unroll 1
+        for (int g = g_begin; g < g_end; ++g) {
+          uint32_t w[4 * C];
 #pragma unroll
-        for (int c = 0; c < C; ++c) {
-          const int k = e * C + c;
-          w[k >> 1] |= h[c] << (16 * (k & 1));
+          for (int i = 0; i < 8; ++i) {
+            const int e = g * 8 + i;
+            uint32_t lo = 0, hi = 0;
+            if (e < RS) {
+              const int64_t raw = (int64_t)__ldg(ib + (int64_t)e * a.mr);
+              if (raw >= 0) {
+                const int64_t off = raw + rr.base;
+                const int64_t wi = off >> 1;
+                const uint32_t sh = (uint32_t)(off & 1) * 16;
+                const uint32_t l = __ldg(x32 + wi);
+                uint32_t h = 0u;
+                if (2 * (wi + 1) + 1 < x_elems) h = __ldg(x32 + wi + 1);
+                else if (2 * (wi + 1) < x_elems) h = __ldg(reinterpret_cast<const uint16_t*>(a.x) + 2 * (wi + 1));
+                lo = __funnelshift_r(l, h, sh);
+                hi = h >> sh;
+              } else {
+                const uint32_t* z = reinterpret_cast<const uint32_t*>(sWin + buf * Cf::kWinBytes) + Cf::kWinElems / 2;
+                lo = z[0];
+                hi = z[1];
+              }
+            }
+            place_tap<C>(w, i, lo, hi);
+          }
+          store_group<C>(w, tileA, row, g);
         }
-        // flush the 16-byte chunks completed by this tap
-        const int q_lo = e == 0 ? 0 : ((e * C) >> 3);
-        const int q_hi = ((e + 1) * C) >> 3;   // chunks [q_lo, q_hi) are complete
-#pragma unroll
-        for (int q = q_lo; q < q_hi; ++q)
-          asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a_chunk_addr(tileA, row, q)),
-                       "r"(w[4 * q]), "r"(w[4 * q + 1]), "r"(w[4 * q + 2]), "r"(w[4 * q + 3]) : "memory");
       }
-#pragma unroll
-      for (int q = (RS * C) >> 3; q < Cf::kBlocks * 8; ++q)   // the partial last chunk and zero padding
-        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a_chunk_addr(tileA, row, q)),
-                     "r"(w[4 * q]), "r"(w[4 * q + 1]), "r"(w[4 * q + 2]), "r"(w[4 * q + 3]) : "memory");
       fence_proxy_async_smem();   // generic-proxy smem writes -> visible to the tensor core
       mbar_arrive(&full[stage]);
       if (++stage == kStagesStem) { stage = 0; phase ^= 1; }
+      prepare(k + 2);              // every producer finished reading window k+2's buffer (tile k-1)
     }
   } else if (warp == kMmaWarpStem) {
     // ------------------------------------------------------------ MMA issuer
@@ -177,7 +351,7 @@ __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __gri
       if (++as == 2) { as = 0; aphase ^= 1; }
     }
   } else {
-    epilogue_loop<false, BN, kEpiWarpsStem, BN>(a, warp - 4, lane, tmem_base, sEpi, sBias, tfull, tempty);
+    epilogue_loop<false, BN, kEpiWarpsStem, BN>(a, warp - kProdWarpsStem, lane, tmem_base, sEpi, sBias, tfull, tempty);
   }
 
   tc_fence_before();
@@ -191,10 +365,14 @@ __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __gri
 template <int C, int RS, int BN, typename IbT>
 int launch_stem_t(const ConvArgs& c, cudaStream_t st) {
   using Cf = CfgStem<C, RS, BN>;
+  const int64_t x_elems = c.g.N * c.g.H * c.g.W * (int64_t)c.g.C;
+  if (x_elems >= (int64_t(1) << 31)) return fail(ICV_ERR_UNSUPPORTED, "stem kernel: input too large");
   auto kernel = igemm_stem_kernel<C, RS, BN, IbT>;
   static std::once_flag once;
   static cudaError_t err = cudaSuccess;
-  std::call_once(once, [&] { err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::kSmemBytes); });
+  std::call_once(once, [&] {
+    err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::kSmemBytes);
+  });
   if (err != cudaSuccess) return cuda_check(err, "cudaFuncSetAttribute(stem smem)");
   CUtensorMap tmap;
   if (int s = make_filter_tmap(c, BN, &tmap)) return s;
@@ -202,7 +380,7 @@ int launch_stem_t(const ConvArgs& c, cudaStream_t st) {
   fill_tc_args(c, BN, &a);
   const int sms = sm_count();
   const int grid = (int)(a.total_tiles < sms ? a.total_tiles : sms);
-  kernel<<<grid, kThreadsStem, Cf::kSmemBytes, st>>>(tmap, a, c.g.N * c.g.H * c.g.W * (int64_t)c.g.C);
+  kernel<<<grid, kThreadsStem, Cf::kSmemBytes, st>>>(tmap, a, (int32_t)x_elems);
   note_launch();
   return cuda_check(cudaGetLastError(), "igemm_stem launch");
 }

@@ -68,7 +68,7 @@ template <bool kI8, int BN, typename IbT>
 bool plan_smem(int rs, int n_pad, PlanS* p) {
   using C = CfgS<kI8, BN>;
   const int bias = (n_pad * 4 + 15) / 16 * 16;
-  const int ib = 2 * rs * kBM * (int)sizeof(IbT);
+  const int ib = 2 * rs * kBM * (int)sizeof(IbT) + 2 * kBM * 8;   // index slices + per-row bases
   const int fixed = 1024 + C::kOnesBytes + C::kEpiBytes + bias + ib + C::kBarBytes;
   int slots = (232448 - fixed) / C::kSlotBytes;
   slots = (slots > C::kMaxSlots ? C::kMaxSlots : slots) / C::kKB * C::kKB;
@@ -97,7 +97,8 @@ __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_c
   uint8_t* sOnes = smem + pl.off_ones;
   uint8_t* sEpi = smem + pl.off_epi;
   uint32_t* sBias = reinterpret_cast<uint32_t*>(smem + pl.off_bias);
-  IbT* sIB = reinterpret_cast<IbT*>(smem + pl.off_ib);          // [2][RS][128] index slices
+  int64_t* sRowBase = reinterpret_cast<int64_t*>(smem + pl.off_ib);   // [2][128] per-image base offsets
+  IbT* sIB = reinterpret_cast<IbT*>(smem + pl.off_ib + 2 * kBM * 8);  // [2][RS][128] index slices
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + pl.off_bar);
   const int kStages = pl.stages;
   uint64_t* empty = full + kStages;
@@ -162,7 +163,9 @@ __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_c
       if (k < my_tiles) {
         const int64_t mt = (blockIdx.x + k * gridDim.x) / a.n_tiles;
         const uint32_t base = smem_u32(sIB + (k & 1) * slice_elems) + threadIdx.x * (int)sizeof(IbT);
-        const IbT* src = static_cast<const IbT*>(a.ib) + first_entry(a, mt, threadIdx.x);   // row = threadIdx.x
+        const RowRef rr = row_ref(a, mt, threadIdx.x);                        // row = threadIdx.x
+        const IbT* src = static_cast<const IbT*>(a.ib) + rr.ent0;
+        sRowBase[(k & 1) * kBM + threadIdx.x] = rr.base;
         for (int e = 0; e < a.RS; ++e)
           cp_async_ca<sizeof(IbT)>(base + e * kBM * (int)sizeof(IbT), src + (int64_t)e * a.mr);
       }
@@ -181,6 +184,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_c
       if (threadIdx.x == 0 && k < 8) TRACE(26 + k);
       stage_index_slice(k + 1);
       const IbT* slice = sIB + (k & 1) * slice_elems;
+      const int64_t* rbase = sRowBase + (k & 1) * kBM;
       const int nt = (int)(tile % a.n_tiles);
       if (tma_gather) {
         // TMA path: warp 0 issues, per K block, one tile::gather4 per lane
@@ -193,7 +197,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_c
             int32_t rows4[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-              const int64_t off = (int64_t)slice[e * kBM + 4 * lane + i];
+              const int64_t off = resolve_ref((int64_t)slice[e * kBM + 4 * lane + i], rbase[4 * lane + i]);
               rows4[i] = off < 0 ? -1 : pixel_row(a, off);
             }
             for (int cb = 0; cb < a.cblocks; ++cb, ++kb) {
@@ -228,7 +232,8 @@ __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_c
           const uint8_t* src[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            const int64_t off = (int64_t)slice[e * kBM + warp * 32 + 4 * i + sub];
+            const int r = warp * 32 + 4 * i + sub;
+            const int64_t off = resolve_ref((int64_t)slice[e * kBM + r], rbase[r]);
             src[i] = off < 0 ? a.zero_row : a.x + off * a.elem_bytes;  // ZERO_REF -> bound zero row
           }
           for (int cb = 0; cb < a.cblocks; ++cb, ++kb) {
@@ -487,6 +492,9 @@ void fill_tc_args(const ConvArgs& c, int block_n, TcArgs* a) {
   a->c_tz = (int32_t)tz;
   a->c_inv = inv;
   a->use_tma_x = 0;
+  a->ib_per_image = c.ib_per_image;
+  a->ohw = c.g.OH * c.g.OW;
+  a->img_elems = c.g.H * c.g.W * (int64_t)c.g.C;
 }
 
 int sm_count() {

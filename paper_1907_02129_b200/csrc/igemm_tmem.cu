@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(kThreadsT, 1) igemm_tmem_kernel(const __grid_c
       const uint32_t base = sIB_u32 + (uint32_t)((k & 1) * C::kIbBytes);
       for (int idx = ptid; idx < kBM * a.RS; idx += 32 * kProdWarpsT) {
         const int e = idx / kBM, row = idx - e * kBM;
-        const int64_t ent = first_entry(a, mt, row) + (int64_t)e * a.mr;
+        const int64_t ent = row_ref(a, mt, row).ent0 + (int64_t)e * a.mr;
         cp_async_ca<sizeof(IbT)>(base + (uint32_t)((e * kBM + row) * sizeof(IbT)), static_cast<const IbT*>(a.ib) + ent);
       }
     };
@@ -311,6 +311,7 @@ int dispatch_tmem(const ConvArgs& c, cudaStream_t st) {
 }  // namespace
 
 bool tmem_kernel_eligible(const ConvArgs& c) {
+  if (c.ib_per_image) return false;                    // canonical buffers only
   if (c.L.block_n > 128) return false;                 // two 256-column accumulators leave no TMEM for A
   if (c.g.RS() > kMaxRST) return false;                // per-tile index slice must fit in smem
   return c.g.RS() * c.L.cblocks >= kMinKBT;

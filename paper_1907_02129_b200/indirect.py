@@ -14,6 +14,14 @@ Buffer layout is the reference's: (T, R*S, mr) element offsets of the pixel
 row each (output pixel, kernel tap) reads, ZERO_REF (-1) for padding taps,
 tile-major then kernel element then lane (indirect.py:14-16), int64 by
 default (``index_dtype=torch.int32`` halves its footprint).
+
+``per_image=True`` stores only image 0's buffer, T = ceil(Ho*Wo/mr): the
+canonical entry of image n is entry(0) + n*H*W*C (ZERO_REF kept), which the
+kernels apply on the fly.  The reference leaves the row-reference
+representation to the implementation; this form makes the
+buffer independent of the batch (growth needs no rebuild) and small enough
+to stay in L2 — for the 3-channel 7x7 stem the canonical buffer is 2.6x the
+layer's compulsory HBM traffic.
 """
 
 from __future__ import annotations
@@ -56,6 +64,7 @@ class IndirectionBuffer:
     input_data: torch.Tensor   # flat buffer of the bound input tensor
     zero_row: torch.Tensor
     offsets: torch.Tensor      # (tiles, R*S, mr) int64 (or int32), device resident
+    per_image: bool = False    # offsets cover image 0 only (image-relative form)
 
     @property
     def pixel_count(self) -> int:
@@ -63,25 +72,39 @@ class IndirectionBuffer:
 
     @property
     def tile_count(self) -> int:
-        return self.offsets.shape[0]
+        """Tiles of the canonical buffer this one represents."""
+        return _tile_count(self.pixel_count, self.mr)
 
     @property
     def entry_count(self) -> int:
-        return self.offsets.numel()
+        """Entries of the canonical buffer (indirect.py:72-73)."""
+        return self.tile_count * self.params.kernel_elems * self.mr
 
     @property
     def allocated_bytes(self) -> int:
         return self.offsets.numel() * self.offsets.element_size()
 
     def offsets_host(self) -> np.ndarray:
-        """Host copy of the buffer as int64 (the reference's canonical form)."""
-        return self.offsets.cpu().numpy().astype(np.int64)
+        """Host copy as the reference's canonical int64 (T, R*S, mr) buffer
+        (a per-image buffer is expanded: entry(n) = entry(0) + n*H*W*C)."""
+        offs = self.offsets.cpu().numpy().astype(np.int64)
+        if not self.per_image:
+            return offs
+        ohw = self.out_h * self.out_w
+        rs, mr = offs.shape[1], self.mr
+        img = offs.transpose(0, 2, 1).reshape(-1, rs)[:ohw]             # (Ho*Wo, RS) per pixel of image 0
+        p = np.minimum(np.arange(self.tile_count * mr), self.pixel_count - 1)
+        n, q = p // ohw, p % ohw
+        rows = img[q]
+        step = self.in_shape.h * self.in_shape.w * self.in_shape.c
+        rows = np.where(rows < 0, rows, rows + (n * step)[:, None])
+        return rows.reshape(self.tile_count, mr, rs).transpose(0, 2, 1).copy()
 
     def rows_for_tile(self, t: int) -> list[torch.Tensor]:
         """Dereference tile t: R*S*mr pixel-row views in kernel-element order,
         mr rows per element; padding entries yield the zero row (:79-91)."""
         c = self.params.in_channels
-        offs = self.offsets[t].cpu().tolist()
+        offs = self.offsets_host()[t].tolist()
         rows = []
         for e in range(self.params.kernel_elems):
             for m in range(self.mr):
@@ -95,20 +118,22 @@ def _tile_count(pixels: int, mr: int) -> int:
 
 
 def _build(in_shape: Shape4, params: ConvParams, batch: int, mr: int, offsets: torch.Tensor,
-           first_tile: int) -> None:
+           first_tile: int, per_image: bool = False) -> None:
     d, s = L.desc_of(params), L.shape_of(in_shape)
+    fmt = L.TORCH_TO_ICV[offsets.dtype] | (L.ICV_IB_PER_IMAGE if per_image else 0)
     with torch.cuda.device(offsets.device):
-        L.check(L.lib().icv_ib_build(ctypes.byref(d), ctypes.byref(s), batch, mr, first_tile,
-                                     L.TORCH_TO_ICV[offsets.dtype], L.ptr(offsets), L.stream_of(offsets.device)),
+        L.check(L.lib().icv_ib_build(ctypes.byref(d), ctypes.byref(s), batch, mr, first_tile, fmt,
+                                     L.ptr(offsets), L.stream_of(offsets.device)),
                 "icv_ib_build")
 
 
 def init_indirection_buffer(input: NhwcTensor, zero_row: torch.Tensor, params: ConvParams, out_shape: Shape4,
                             tile: TileConfig, batch: int | None = None, *,
-                            index_dtype: torch.dtype = torch.int64) -> IndirectionBuffer:
+                            index_dtype: torch.dtype = torch.int64, per_image: bool = False) -> IndirectionBuffer:
     """Build the buffer for ``input`` under ``params`` on the input's device
     (indirect.py:129-164).  ``batch`` limits initialization to the first
-    images (extend later with update_for_batch_growth)."""
+    images (extend later with update_for_batch_growth).  ``per_image=True``
+    builds the batch-invariant image-relative form (module docstring)."""
     expected = conv_output_shape(params, input.shape)
     if out_shape != expected:
         raise ValueError(f"out_shape {out_shape} != computed {expected}")                 # :143-145
@@ -123,11 +148,12 @@ def init_indirection_buffer(input: NhwcTensor, zero_row: torch.Tensor, params: C
     L.require_cuda(input.data, "input")
     if zero_row.device != input.data.device:
         raise ValueError("zero row must live on the input's device")
-    tiles = _tile_count(batch * out_shape.h * out_shape.w, tile.mr)
+    pixels = (1 if per_image else batch) * out_shape.h * out_shape.w
+    tiles = _tile_count(pixels, tile.mr)
     offsets = torch.empty((tiles, params.kernel_elems, tile.mr), dtype=index_dtype, device=input.data.device)
-    _build(input.shape, params, batch, tile.mr, offsets, 0)
+    _build(input.shape, params, batch, tile.mr, offsets, 0, per_image)
     return IndirectionBuffer(tile.mr, batch, out_shape.h, out_shape.w, params, input.shape, input.data,
-                             zero_row, offsets)
+                             zero_row, offsets, per_image)
 
 
 def update_for_batch_growth(ib: IndirectionBuffer, new_batch: int) -> IndirectionBuffer:
@@ -142,6 +168,8 @@ def update_for_batch_growth(ib: IndirectionBuffer, new_batch: int) -> Indirectio
         raise ValueError("new batch exceeds the bound input tensor's batch")
     if new_batch == ib.batch:
         return ib
+    if ib.per_image:                       # image-relative entries serve every image: nothing to build
+        return replace(ib, batch=new_batch)
     keep = ib.pixel_count // ib.mr                                                        # :185
     tiles = _tile_count(new_batch * ib.out_h * ib.out_w, ib.mr)
     offsets = torch.empty((tiles, ib.params.kernel_elems, ib.mr), dtype=ib.offsets.dtype, device=ib.offsets.device)
@@ -159,7 +187,7 @@ def rebind_input(ib: IndirectionBuffer, new_input: NhwcTensor, new_zero: torch.T
                          f"new input has {new_input.shape}")
     out_shape = Shape4(new_input.shape.n, ib.out_h, ib.out_w, ib.params.out_channels)
     return init_indirection_buffer(new_input, new_zero, ib.params, out_shape, TileConfig(mr=ib.mr),
-                                   batch=ib.batch, index_dtype=ib.offsets.dtype)
+                                   batch=ib.batch, index_dtype=ib.offsets.dtype, per_image=ib.per_image)
 
 
 def _check_filter(pf: PackedFilter, params: ConvParams) -> None:
@@ -218,7 +246,8 @@ def indirect_conv(input: NhwcTensor, pf: PackedFilter, ib: IndirectionBuffer, pa
     with torch.cuda.device(dev):
         L.check(L.lib().icv_conv(ctypes.byref(d), ctypes.byref(s), batch, L.TORCH_TO_ICV[input.dtype],
                                  L.ptr(input.data), L.ptr(ib.zero_row), L.ptr(ib.offsets),
-                                 L.TORCH_TO_ICV[ib.offsets.dtype], ib.mr, L.ptr(pf.packed),
+                                 L.TORCH_TO_ICV[ib.offsets.dtype] | (L.ICV_IB_PER_IMAGE if ib.per_image else 0),
+                                 ib.mr, L.ptr(pf.packed),
                                  ctypes.byref(q) if q is not None else None, L.ptr(out.data), L.stream_of(dev)),
                 "icv_conv")
     return out

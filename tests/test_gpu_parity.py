@@ -364,3 +364,60 @@ def test_kernel_selection_is_native_tensor_core_for_baseline_configs():
     before = L.launch_count()
     bf16_problem(CFG2, n_img=1)
     assert L.launch_count() > before
+
+
+# ------------------------------------------------- per-image (batch-invariant) IB
+def test_per_image_ib_expands_to_canonical(golden):
+    for row in golden["ib_sweep"][::5]:
+        p = to_params(row["params"])
+        shape = icv.Shape4(*row["in_shape"])
+        for mr, (oshape, digest) in row["mr"].items():
+            x = icv.tensor_fill_random(shape, 0, device=DEV)
+            zero = icv.make_zero_row(p.in_channels, device=DEV)
+            ib = icv.init_indirection_buffer(x, zero, p, icv.conv_output_shape(p, shape), icv.TileConfig(mr=int(mr)),
+                                             per_image=True, index_dtype=torch.int32)
+            assert ib.offsets.shape[0] == -(-(ib.out_h * ib.out_w) // int(mr))
+            assert sha(ib.offsets_host().astype("<i8")) == digest, (row["i"], mr)
+
+
+@pytest.mark.parametrize("w", [CFG1, CFG2, CFG3A, CFG3B, CFG4], ids=lambda w: w.name)
+def test_per_image_ib_gives_identical_outputs(w):
+    """Same bytes out of every kernel family whichever buffer form it reads
+    (2 images of each config; the stem reads 157 MB less with per-image)."""
+    n = 2
+    w = w.with_batch(max(n, w.in_shape.n))
+    shape = icv.Shape4(n, w.in_shape.h, w.in_shape.w, w.in_shape.c)
+    p = w.params
+    dt = {"f32": torch.float32, "bf16": torch.bfloat16, "u8": torch.uint8}[w.dtype]
+    x = icv.NhwcTensor(shape, torch.from_numpy(w.input_host(0, n)).to(DEV).to(dt))
+    qp, fill = None, 0
+    if w.quant is not None:
+        q = w.quant
+        qp = icv.QuantParams(q.input_zero_point, q.input_scale, q.kernel_zero_point, q.kernel_scale,
+                             q.output_zero_point, q.output_scale)
+        fill = q.input_zero_point
+    bias = w.bias_host()
+    filt = icv.FilterTensor(p.out_channels, p.kernel_h, p.kernel_w, p.in_channels,
+                            torch.from_numpy(w.filter_host()).to(DEV).to(dt))
+    outs = []
+    for mr in (4, 128):
+        tile = icv.TileConfig(mr=mr)
+        pf = icv.pack_filter(filt, None if bias is None else torch.from_numpy(bias), p, tile, quant=qp)
+        zero = icv.make_zero_row(p.in_channels, dtype=dt, device=DEV, fill=fill)
+        for per_image in (False, True):
+            ib = icv.init_indirection_buffer(x, zero, p, icv.conv_output_shape(p, shape), tile, per_image=per_image)
+            outs.append(icv.indirect_conv(x, pf, ib, p, tile).data.clone())
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])
+
+
+def test_per_image_growth_needs_no_rebuild():
+    p = make_params(r=3, s=3, pt=1, pl=1, c=8, k=8)
+    x = icv.tensor_fill_random(icv.Shape4(3, 5, 6, 8), 3, device=DEV, dtype=torch.bfloat16)
+    zero = icv.make_zero_row(8, dtype=torch.bfloat16, device=DEV)
+    out_shape = icv.conv_output_shape(p, x.shape)
+    ib1 = icv.init_indirection_buffer(x, zero, p, out_shape, icv.TileConfig(), batch=1, per_image=True)
+    grown = icv.update_for_batch_growth(ib1, 3)
+    assert grown.offsets is ib1.offsets and grown.batch == 3
+    fresh = icv.init_indirection_buffer(x, zero, p, out_shape, icv.TileConfig())
+    assert np.array_equal(grown.offsets_host(), fresh.offsets_host())

@@ -19,7 +19,8 @@ def main():
     dev = torch.device("cuda", 0)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     for name in names:
-        w, x, xh, pf, ib, y, tile = bench.setup_problem(name, 0, CONFIGS[name].in_shape.n, dev)
+        w, x, xh, pf, ib, y, tile = bench.setup_problem(name, 0, CONFIGS[name].in_shape.n, dev,
+                                                        per_image=os.environ.get("ICV_IB", "per-image") == "per-image")
         t = bench.time_steps(lambda: icv.indirect_conv(x, pf, ib, w.params, tile, out=y), 50, 5,
                              lambda: flush.fill_(1))
         ms = statistics.median(t)
