@@ -4,6 +4,7 @@
 // TMEM -> registers -> HBM epilogue, and the TMA descriptor of the packed
 // filter.
 #pragma once
+#include <type_traits>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
@@ -98,9 +99,31 @@ __device__ __forceinline__ int64_t load_ref(const TcArgs& a, int64_t ent) {
 // bf16 or requantize to uint8, stage the 32 x 32 block in smem and write it out
 // with row-contiguous 16-byte stores.  Tail rows (>= P) and columns (>= K) are
 // never stored (indirect.py:299).
-template <bool kI8, int BN, int kEpiWarps, int kAccStride>
+// Epilogue store of the first min(n, 16) bytes of `val` (misaligned or
+// ragged output rows); a rolled loop, so the fast path is not if-converted
+// into predicated byte stores.
+__device__ __forceinline__ void store_partial(uint8_t* dst, uint4 val, int n) {
+#pragma unroll 1
+  for (int j = 0; j < 16 && j < n; ++j) {
+    const uint32_t word = j < 4 ? val.x : j < 8 ? val.y : j < 12 ? val.z : val.w;
+    dst[j] = (uint8_t)(word >> (8 * (j & 3)));
+  }
+}
+
+// Tile schedule: local tile k of this CTA is tile_of(k), k < n_local
+// (default: tiles blockIdx.x, blockIdx.x + gridDim.x, ...).
+struct StridedTiles {
+  int64_t total;
+  __device__ __forceinline__ int64_t count() const {
+    return blockIdx.x < total ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  }
+  __device__ __forceinline__ int64_t operator()(int64_t k) const { return blockIdx.x + k * gridDim.x; }
+};
+
+template <bool kI8, int BN, int kEpiWarps, int kAccStride, typename Sched = StridedTiles>
 __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane, uint32_t tmem_base, uint8_t* sEpi,
-                                              const uint32_t* sBias, uint64_t* tfull, uint64_t* tempty) {
+                                              const uint32_t* sBias, uint64_t* tfull, uint64_t* tempty,
+                                              Sched sched = Sched{0}) {
   constexpr int kOutRowBytes = kI8 ? 32 : 64;
   constexpr int kStageRowBytes = kI8 ? 48 : 80;  // padded: row-per-lane staging writes are conflict free
   const int slot = ew & 3;
@@ -111,12 +134,25 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
   const bool vec_ok = kI8 ? (a.K & 15) == 0 : (a.K & 7) == 0;
   int as = 0;
   uint32_t aphase = 0;
-  for (int64_t tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
+  if constexpr (std::is_same<Sched, StridedTiles>::value) sched.total = a.total_tiles;
+  const int64_t n_local = sched.count();
+#ifdef ICV_TRACE
+  long long t_prev = clock64(), t_wait = 0, t_work = 0;
+#endif
+  for (int64_t ti = 0; ti < n_local; ++ti) {
+    const int64_t tile = sched(ti);
     const int64_t mt = tile / a.n_tiles;
     const int nt = (int)(tile - mt * a.n_tiles);
     mbar_wait(&tfull[as], aphase);
     tc_fence_after();
-    const int ti_ = (int)((tile - blockIdx.x) / gridDim.x);
+#ifdef ICV_TRACE
+    {   // slot 28: cycles waiting for accumulators, 29: cycles working (warp 0, lane 0)
+      const long long t = clock64();
+      t_wait += t - t_prev;
+      t_prev = t;
+    }
+#endif
+    const int ti_ = (int)ti;
     if (ew == 0 && lane == 0 && ti_ < 8) TRACE(10 + ti_);
     const int64_t row0 = mt * kBM + slot * 32;  // first pixel of this warp's rows
     const uint32_t taddr = tmem_base + ((uint32_t)(slot * 32) << 16) + as * kAccStride;
@@ -185,14 +221,8 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
           const uint4 val = *reinterpret_cast<const uint4*>(stg + rr * kStageRowBytes + q * 16);
           const int col = n + q * (16 / eb);
           uint8_t* dst = static_cast<uint8_t*>(a.y) + (p * a.K + col) * eb;
-          if (vec_ok && col + 16 / eb <= a.K) {
-            *reinterpret_cast<uint4*>(dst) = val;
-          } else {
-            const uint8_t* bytes = reinterpret_cast<const uint8_t*>(&val);
-            for (int j = 0; j < 16 / eb; ++j)
-              if (col + j < a.K)
-                for (int t = 0; t < eb; ++t) dst[j * eb + t] = bytes[j * eb + t];
-          }
+          if (vec_ok && col + 16 / eb <= a.K) *reinterpret_cast<uint4*>(dst) = val;
+          else store_partial(dst, val, (a.K - col) * eb);   // ragged / misaligned rows only
         }
       }
       __syncwarp();
@@ -204,9 +234,22 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
     }
     tc_fence_before();
     mbar_arrive(&tempty[as]);
+#ifdef ICV_TRACE
+    {
+      const long long t = clock64();
+      t_work += t - t_prev;
+      t_prev = t;
+    }
+#endif
     if (ew == 0 && lane == 0 && ti_ < 8) TRACE(18 + ti_);
     if (++as == 2) { as = 0; aphase ^= 1; }
   }
+#ifdef ICV_TRACE
+  if (ew == 0 && lane == 0) {
+    g_icv_trace[blockIdx.x][28] = (unsigned long long)t_wait;
+    g_icv_trace[blockIdx.x][29] = (unsigned long long)t_work;
+  }
+#endif
 }
 
 // ----------------------------------------------------------------------------

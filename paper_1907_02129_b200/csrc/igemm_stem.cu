@@ -27,7 +27,71 @@ constexpr int kEpiWarpsStem = 4;
 constexpr int kMmaWarpStem = kProdWarpsStem + kEpiWarpsStem;
 constexpr int kThreadsStem = 32 * (kMmaWarpStem + 1);
 constexpr int kStagesStem = 2;          // A tiles in flight
-constexpr int kWinBufs = 3;             // input windows in flight (tile k assembling, k+1 landing, k+2 issued)
+constexpr int kWinPix = 2048;           // input-window capacity in pixels (cfg3a needs <= 1834)
+
+// Byte offset of element offset `d` (a multiple of C) in the pixel-slot
+// window (8 bytes per pixel): d / C * 8 = d * kSlotMul (mod 2^32).
+__host__ __device__ constexpr uint32_t inv_odd(uint32_t c) {
+  uint32_t x = c;   // Newton iterations for the inverse of an odd c mod 2^32
+  for (int i = 0; i < 5; ++i) x *= 2u - c * x;
+  return x;
+}
+template <int C>
+constexpr uint32_t kSlotMul = (C & 1) ? 8u * inv_odd(C) : 8u / C;
+
+// Tile schedule of the stem kernel: CTA b owns the contiguous virtual tiles
+// [V*b/G, V*(b+1)/G).  With a per-image indirection buffer and whole tiles
+// per image (Ho*Wo % 128 == 0), virtual tile v is pattern j = v / N of image
+// n = v % N: consecutive tiles of a CTA share one reference pattern (the
+// buffer is batch invariant), so its window layout and slot offsets are
+// computed once per pattern and only the window's image offset changes.
+struct StemTiles {
+  int32_t total;     // tiles
+  int32_t n_img;     // images sharing a pattern (1 unless image-major)
+  int32_t tpi;       // tiles per image (image-major)
+};
+struct StemPos {
+  int32_t key, img;  // pattern (image-0 tile, or the tile itself) and image of a local tile
+};
+struct StemSched {
+  int32_t begin, n, n_img, tpi;
+  __device__ __forceinline__ explicit StemSched(const StemTiles& t)
+      : begin((int32_t)((int64_t)t.total * blockIdx.x / gridDim.x)),
+        n((int32_t)((int64_t)t.total * (blockIdx.x + 1) / gridDim.x) - begin),
+        n_img(t.n_img),
+        tpi(t.tpi) {}
+  __device__ __forceinline__ int64_t count() const { return n; }
+  __device__ __forceinline__ StemPos pos(int64_t k) const {
+    const int32_t v = begin + (int32_t)k;
+    return n_img > 1 ? StemPos{v / n_img, v % n_img} : StemPos{v, 0};
+  }
+  __device__ __forceinline__ void advance(StemPos& p) const {
+    if (++p.img == n_img) { p.img = 0; ++p.key; }
+  }
+  __device__ __forceinline__ int64_t tile(StemPos p) const {
+    return n_img > 1 ? (int64_t)p.img * tpi + p.key : (int64_t)p.key;
+  }
+  __device__ __forceinline__ int64_t operator()(int64_t k) const { return tile(pos(k)); }
+};
+
+#ifdef ICV_TRACE
+// debug build: per-CTA cycle accumulators of the producer / MMA phases
+// (slots 26..39 of g_icv_trace, tools/trace_stem.py), kept in registers
+#define STEM_T0(cond) long long _t = clock64(), _acc[5] = {0, 0, 0, 0, 0}; const bool _tr = (cond)
+#define STEM_ACC(i)                    \
+  do {                                 \
+    const long long _n = clock64();    \
+    _acc[i] += _n - _t;                \
+    _t = _n;                           \
+  } while (0)
+#define STEM_FLUSH(slot0, n) \
+  if (_tr)                   \
+    for (int _i = 0; _i < (n); ++_i) g_icv_trace[blockIdx.x][(slot0) + _i] = (unsigned long long)_acc[_i]
+#else
+#define STEM_T0(cond)
+#define STEM_ACC(i)
+#define STEM_FLUSH(slot0, n)
+#endif
 
 template <int C, int RS, int BN>
 struct CfgStem {
@@ -45,18 +109,20 @@ struct CfgStem {
   static constexpr int kG0 = (kGroups + 1) / 2;
   static constexpr int kTapsHalf = kG0 * 8;                 // taps per producer thread (max)
   static constexpr int kTaps = kGroups * 8;
-  // elements per staged input window: 16 KB of bf16 (8 KB when a 128-wide
-  // resident filter leaves less room); two 8-element slots follow it: the
-  // bound zero row (ZERO_REF taps) and true zeros (taps past R*S)
-  static constexpr int kWinElems = (BN <= 64 || RS * C <= 64) ? 8192 : 4096;
-  static constexpr int kWinBytes = kWinElems * 2 + 32;
-  static constexpr int kRelBytes = kTaps * kBM * 2;         // [kTaps/2][128][2] uint16 window indices
+  // staged input window: raw NHWC bytes of up to kWinPix pixels (cp.async)
+  static constexpr int kStageBytes = kWinPix * C * 2;
+  // pixel-slot window: 8 bytes per pixel (C elements, zero padded), then two
+  // slots: the bound zero row (ZERO_REF taps) and true zeros (taps past R*S)
+  static constexpr int kSlotBytes = (kWinPix + 2) * 8;
+  static constexpr int kRelBytes = kTaps * kBM * 2;         // [kTaps/2][128][2] uint16 slot byte offsets
+  static constexpr int kHalfPix = kWinPix / 2;              // even pixels, then odd pixels
   static constexpr int kMiscBytes = 1024;                   // bias, reductions, window bases
-  static constexpr int kSmemBytes = 1024 + kStagesStem * kABytes + kBBytes + kEpiBytes + kWinBufs * kWinBytes +
-                                    kWinBufs * kRelBytes + kMiscBytes + 256;
+  static constexpr int kSmemBytes = 1024 + kStagesStem * kABytes + kBBytes + kEpiBytes + 2 * kStageBytes +
+                                    kSlotBytes + 2 * kRelBytes + kMiscBytes + 256;
   static_assert(kSmemBytes <= 232448, "shared memory overflow");
   static_assert(C >= 1 && C <= 4, "channel-poor kernel handles 1..4 channels");
   static_assert(kGroups * C * 8 <= kBlocks * 64, "tap groups overflow the A row");
+  static_assert(kSlotBytes < 65536, "slot offsets are 16-bit");
 };
 
 // 16-byte chunk q (elements 8q .. 8q+7) of row `row` in the swizzled A tile.
@@ -69,6 +135,25 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
   uint32_t v;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
   return v;
+}
+__device__ __forceinline__ uint2 lds64(uint32_t addr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
+// element j (0 .. 2*N-1) of a little-endian array of N packed bf16 pairs
+template <int N>
+__device__ __forceinline__ uint32_t elem16(const uint32_t (&v)[N], int j) {
+  return (v[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
 }
 
 // Place tap i (0..7) of a group -- its C elements are the low 16*C bits of
@@ -87,26 +172,30 @@ __device__ __forceinline__ void place_tap(uint32_t (&w)[4 * C], int i, uint32_t 
 template <int C>
 __device__ __forceinline__ void store_group(const uint32_t (&w)[4 * C], uint32_t tileA, int row, int g) {
 #pragma unroll
-  for (int j = 0; j < C; ++j)
-    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a_chunk_addr(tileA, row, g * C + j)),
-                 "r"(w[4 * j]), "r"(w[4 * j + 1]), "r"(w[4 * j + 2]), "r"(w[4 * j + 3]) : "memory");
+  for (int j = 0; j < C; ++j) sts128(a_chunk_addr(tileA, row, g * C + j), w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
 }
 
 template <int C, int RS, int BN, typename IbT>
 __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __grid_constant__ CUtensorMap tmap_b,
-                                                                     const TcArgs a, int32_t x_elems) {
+                                                                     const TcArgs a, int32_t x_elems,
+                                                                     const StemTiles tiles) {
   using Cf = CfgStem<C, RS, BN>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned base (SW128 atoms); pointer arithmetic keeps the
+  // shared address space visible to the compiler (no generic loads)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = sA + kStagesStem * Cf::kABytes;
   uint8_t* sEpi = sB + Cf::kBBytes;
-  uint8_t* sWin = sEpi + Cf::kEpiBytes;                              // [3] windows (+ zero slots)
-  uint8_t* sRel = sWin + kWinBufs * Cf::kWinBytes;                   // [3][kTaps/2][128][2] uint16
-  uint8_t* sMisc = sRel + kWinBufs * Cf::kRelBytes;
+  uint8_t* sStage = sEpi + Cf::kEpiBytes;                            // [2] raw input windows
+  uint8_t* sSlot = sStage + 2 * Cf::kStageBytes;                     // pixel-slot window (+ 2 zero slots)
+  uint8_t* sRel = sSlot + Cf::kSlotBytes;                            // [2][kTaps/2][128][2] slot offsets
+  uint8_t* sMisc = sRel + 2 * Cf::kRelBytes;
   uint32_t* sBias = reinterpret_cast<uint32_t*>(sMisc);                         // 128 x 4 B
-  int32_t* sRed = reinterpret_cast<int32_t*>(sMisc + 512);                      // [3][2][8] min/max per warp
-  int32_t* sWinLo = reinterpret_cast<int32_t*>(sMisc + 512 + 192);              // [3] window start (or -1)
+  int32_t* sRed = reinterpret_cast<int32_t*>(sMisc + 512);                      // [2][2][8] min/max per warp
+  int32_t* sWin = reinterpret_cast<int32_t*>(sMisc + 512 + 128);                // [2] pixel groups (or -1)
+  int32_t* sKeyW0 = reinterpret_cast<int32_t*>(sMisc + 512 + 144);              // [2] pattern window start
+  int32_t* sKeyGroups = reinterpret_cast<int32_t*>(sMisc + 512 + 160);          // [2] pattern window groups
   uint64_t* full = reinterpret_cast<uint64_t*>(sMisc + Cf::kMiscBytes);
   uint64_t* empty = full + kStagesStem;
   uint64_t* tfull = empty + kStagesStem;
@@ -116,6 +205,7 @@ __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __gri
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const StemSched sched(tiles);
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStagesStem; ++s) {
       mbar_init(&full[s], kProdThreads);   // every producer thread (st.shared + proxy fence + arrive)
@@ -130,12 +220,11 @@ __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __gri
     tma_prefetch_desc(&tmap_b);
   }
   for (int i = threadIdx.x; i < a.n_pad; i += blockDim.x) sBias[i] = __ldg(static_cast<const uint32_t*>(a.bias) + i);
-  if (threadIdx.x < kWinBufs * 8) {   // zero slots behind every window: bound zero row, then true zeros
-    const int b = threadIdx.x >> 3, j = threadIdx.x & 7;
+  if (threadIdx.x < 8) {   // the two fixed slots: bound zero row, then true zeros
+    const int j = threadIdx.x;
     const uint16_t* z = reinterpret_cast<const uint16_t*>(a.zero_row);
-    uint16_t* slot = reinterpret_cast<uint16_t*>(sWin + b * Cf::kWinBytes) + Cf::kWinElems;
-    slot[j] = j < C ? __ldg(z + j) : (uint16_t)0;
-    slot[8 + j] = 0;
+    uint16_t* slot = reinterpret_cast<uint16_t*>(sSlot + kWinPix * 8);
+    slot[j] = (j < 4 && j < C) ? __ldg(z + j) : (uint16_t)0;
   }
   if (warp == kMmaWarpStem) tmem_alloc<(2 * BN <= 128 ? 128 : 256)>(tmem_slot);
   tc_fence_before();
@@ -154,93 +243,111 @@ __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __gri
     // ------------------------------------------------------------ producers
     // Thread (half, row) assembles half of A row `row` (one output pixel).
     // Per tile, the row references of its 128 pixels (indirection buffer)
-    // bound the span of input elements the tile reads; that span (the
-    // "window") is copied into smem with coalesced 16-byte cp.async two
-    // tiles ahead, the references become 16-bit window indices, and rows are
-    // assembled from the window with shared-memory loads.  A window larger
-    // than the buffer (never for the ResNet stem) falls back to reading the
-    // taps straight from global memory.
+    // bound the span of input pixels the tile reads (the "window").  Two
+    // tiles ahead, the window's raw NHWC bytes are copied into smem with
+    // coalesced 16-byte cp.async and every reference becomes a 16-bit slot
+    // offset; when the tile comes up, the window is re-laid out as one
+    // 8-byte slot per pixel, so each tap is a single aligned 8-byte shared
+    // load.  A window wider than kWinPix pixels (never for the ResNet stem)
+    // falls back to reading the taps straight from global memory.
     const int half = warp >> 2;
     const int row = threadIdx.x & (kBM - 1);
     const int g_begin = half ? Cf::kG0 : 0;
     const int g_end = half ? Cf::kGroups : Cf::kG0;
     const int e_begin = g_begin * 8;
-    const int n_taps = (g_end - g_begin) * 8;
+    const int n_real = min((g_end - g_begin) * 8, RS - e_begin);   // taps below R*S
     const uint32_t* x32 = reinterpret_cast<const uint32_t*>(a.x);
-    const uint32_t sWin_u32 = smem_u32(sWin);
+    const uint32_t sStage_u32 = smem_u32(sStage);
+    const uint32_t sSlot_u32 = smem_u32(sSlot);
     const uint32_t sRel_u32 = smem_u32(sRel);
-    const int64_t my_tiles = blockIdx.x < a.total_tiles ? (a.total_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-    constexpr int32_t kPad = -2;        // tap past R*S
-    int32_t ref[Cf::kTapsHalf];         // resolved element offsets (ZERO_REF = -1, padding = -2)
+    const int64_t my_tiles = sched.count();
+    constexpr int kWordsPerRef = sizeof(IbT) / 4;   // low word of an int64 reference (offsets < 2^31)
+    int32_t ref[Cf::kTapsHalf];        // raw references of this thread's taps (image-relative if per-image)
+    int32_t base = 0;                  // element offset of this row's image (per-image buffers)
+    // a new reference pattern starts at local tile k (position p)
+    auto new_key = [&](int64_t k, StemPos p) { return k == 0 || p.img == 0; };
 
-    auto load_refs = [&](int64_t k) {   // row references of local tile k -> registers
-      if (k >= my_tiles) return;
-      const RowRef rr = row_ref(a, blockIdx.x + k * gridDim.x, row);
-      const IbT* ib = static_cast<const IbT*>(a.ib) + rr.ent0 + (int64_t)e_begin * a.mr;
-      const int32_t base = (int32_t)rr.base;
+    auto load_refs = [&](int64_t k, StemPos p) {  // row references of local tile k's pattern -> registers
+      if (k >= my_tiles || !new_key(k, p)) return;
+      const RowRef rr = row_ref(a, p.key, row);     // image 0's tile (image-major) or the tile itself
+      const int32_t* ib = reinterpret_cast<const int32_t*>(static_cast<const IbT*>(a.ib) + rr.ent0 +
+                                                           (int64_t)e_begin * a.mr);
+      const int64_t stride = a.mr * kWordsPerRef;
+      base = (int32_t)rr.base;
 #pragma unroll
-      for (int i = 0; i < Cf::kTapsHalf; ++i) {
-        if (i < n_taps && e_begin + i < RS) {
-          const int32_t raw = (int32_t)__ldg(ib + (int64_t)i * a.mr);
-          ref[i] = raw + (base & ~(raw >> 31));          // ZERO_REF (-1) stays -1
-        } else {
-          ref[i] = kPad;
-        }
-      }
+      for (int i = 0; i < Cf::kTapsHalf; ++i) ref[i] = i < n_real ? __ldg(ib + i * stride) : -2;
     };
-    // window of local tile k: CTA-wide min/max of the valid offsets, window
-    // indices -> sRel, 16-byte cp.async copies -> sWin
-    auto prepare = [&](int64_t k) {
-      const int buf = (int)(k % kWinBufs);
+    // Window of local tile k.  For a new pattern: the CTA-wide pixel span of
+    // its valid references -> (sKeyW0, sKeyGroups)[key & 1] and the slot
+    // offsets -> sRel[key & 1].  Then the raw window bytes of tile k (the
+    // pattern's window moved to tile k's image) -> sStage[k & 1].
+    auto prepare = [&](int64_t k, StemPos p) {
       if (k < my_tiles) {
-        uint32_t lo = 0xFFFFFFFFu;
-        int32_t hi = -1;
+        const int buf = (int)(k & 1);
+        const int ks = p.key & 1;
+        int32_t kw_groups = 0, kw_w0 = 0;
+        if (new_key(k, p)) {
+          uint32_t lo = 0xFFFFFFFFu;   // ZERO_REF (-1) and padding (-2) are the largest as unsigned
+          int32_t hi = -1;
 #pragma unroll
-        for (int i = 0; i < Cf::kTapsHalf; ++i) {
-          lo = min(lo, ref[i] >= 0 ? (uint32_t)ref[i] : 0xFFFFFFFFu);
-          hi = max(hi, ref[i]);
-        }
+          for (int i = 0; i < Cf::kTapsHalf; ++i) {
+            lo = min(lo, (uint32_t)ref[i]);
+            hi = max(hi, ref[i]);
+          }
+          const bool row_valid = hi >= 0;
+          if (row_valid) { lo += base; hi += base; }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-          hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-        }
-        if (lane == 0) { sRed[buf * 16 + warp] = (int32_t)lo; sRed[buf * 16 + 8 + warp] = hi; }
-      }
-      named_bar_sync(1, kProdThreads);
-      if (k < my_tiles) {
-        uint32_t lo = 0xFFFFFFFFu;
-        int32_t hi = -1;
+          for (int o = 16; o > 0; o >>= 1) {
+            lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+          }
+          if (lane == 0) { sRed[ks * 16 + warp] = (int32_t)lo; sRed[ks * 16 + 8 + warp] = hi; }
+          named_bar_sync(1, kProdThreads);   // also: every producer finished assembling tile k-2
+          lo = 0xFFFFFFFFu;
+          hi = -1;
 #pragma unroll
-        for (int i = 0; i < kProdWarpsStem; ++i) {
-          lo = min(lo, (uint32_t)sRed[buf * 16 + i]);
-          hi = max(hi, sRed[buf * 16 + 8 + i]);
-        }
-        const int32_t w0 = hi < 0 ? 0 : (int32_t)(lo & ~7u);        // 16-byte aligned start
-        const int32_t w1 = hi < 0 ? 0 : ((hi + C + 7) & ~7);          // covers the last reference's C elements
-        const bool fits = w1 - w0 <= Cf::kWinElems;
-        if (threadIdx.x == 0) sWinLo[buf] = fits ? w0 : -1;
-        const uint32_t rel_base = sRel_u32 + buf * Cf::kRelBytes + ((g_begin * 4) * kBM + row) * 4;
+          for (int i = 0; i < kProdWarpsStem; ++i) {
+            lo = min(lo, (uint32_t)sRed[ks * 16 + i]);
+            hi = max(hi, sRed[ks * 16 + 8 + i]);
+          }
+          const int32_t w0 = hi < 0 ? 0 : (int32_t)(lo / (8 * C) * (8 * C));   // 8-pixel (16C-byte) aligned
+          const int32_t groups = hi < 0 ? 0 : ((hi - w0) / C + 8) / 8;           // 8-pixel groups spanned
+          if (threadIdx.x == 0) { sKeyW0[ks] = w0; sKeyGroups[ks] = groups; }
+          kw_groups = groups;
+          kw_w0 = w0;
+          // pixel s of the window lives in slot (s & 1) * kHalfPix + (s >> 1); ZERO_REF -> slot kWinPix
+          // (pixel 2 * kWinPix), taps past R*S -> slot kWinPix + 1
+          const int32_t d = row_valid ? w0 - base : -2 * kWinPix * C;
+          const uint32_t zc = (uint32_t)(2 * kWinPix * C + d);
+          const uint32_t rel_base = sRel_u32 + ks * Cf::kRelBytes + ((g_begin * 4) * kBM + row) * 4;
 #pragma unroll
-        for (int i = 0; i < Cf::kTapsHalf; i += 2) {
-          if (i < n_taps) {
-            uint32_t r2 = 0;
+          for (int i = 0; i < Cf::kTapsHalf; i += 2) {
+            if (i < (g_end - g_begin) * 8) {
+              uint32_t r2 = 0;
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-              const int32_t r = ref[i + j];
-              const uint32_t rel = r >= 0 ? (uint32_t)(r - w0) : (r == -1 ? Cf::kWinElems : Cf::kWinElems + 8);
-              r2 |= rel << (16 * j);
+              for (int j = 0; j < 2; ++j) {
+                const uint32_t px = (min((uint32_t)ref[i + j], zc) - (uint32_t)d) * kSlotMul<C> / 8;
+                const uint32_t off = i + j < n_real ? ((px & 1) * Cf::kHalfPix + (px >> 1)) * 8
+                                                    : (uint32_t)(kWinPix + 1) * 8;
+                r2 |= (off & 0xFFFFu) << (16 * j);
+              }
+              asm volatile("st.shared.u32 [%0], %1;" ::"r"(rel_base + (i / 2) * kBM * 4), "r"(r2) : "memory");
             }
-            asm volatile("st.shared.u32 [%0], %1;" ::"r"(rel_base + (i / 2) * kBM * 4), "r"(r2) : "memory");
           }
         }
+        // (a reused pattern's window was published to smem before an earlier barrier)
+        int32_t groups = sKeyGroups[ks], w0 = sKeyW0[ks];
+        if (new_key(k, p)) { groups = kw_groups; w0 = kw_w0; }
+        w0 += p.img * (int32_t)a.img_elems;
+        const bool fits = groups * 8 <= kWinPix;
+        if (threadIdx.x == 0) sWin[buf] = fits ? groups : -1;
         if (fits) {
-          const uint32_t dst = sWin_u32 + buf * Cf::kWinBytes;
-          for (int32_t ch = threadIdx.x; ch * 8 < w1 - w0; ch += kProdThreads) {
-            const int32_t e0 = w0 + ch * 8;
-            int32_t valid = (x_elems - e0) * 2;
+          const uint32_t dst = sStage_u32 + buf * Cf::kStageBytes;
+          const uint8_t* src = a.x + (int64_t)w0 * 2;
+          for (int32_t ch = threadIdx.x; ch < groups * C; ch += kProdThreads) {
+            int32_t valid = (x_elems - (w0 + ch * 8)) * 2;
             valid = valid < 0 ? 0 : (valid > 16 ? 16 : valid);
-            cp_async_16(dst + (uint32_t)ch * 16, a.x + (valid ? (int64_t)e0 * 2 : 0), (uint32_t)valid);
+            cp_async_16(dst + (uint32_t)ch * 16, valid ? src + ch * 16 : a.x, (uint32_t)valid);
           }
         }
       }
@@ -248,44 +355,72 @@ __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __gri
     };
 
     // prologue: windows of tiles 0 and 1
-    load_refs(0);
-    prepare(0);
-    load_refs(1);
-    prepare(1);
+    StemPos pb = sched.pos(0);       // tile being assembled (k)
+    StemPos pp = pb;                 // tile being prepared (k + 2)
+    load_refs(0, pp);
+    prepare(0, pp);
+    sched.advance(pp);
+    load_refs(1, pp);
+    prepare(1, pp);
+    sched.advance(pp);
     int stage = 0;
     uint32_t phase = 0;
+    STEM_T0(threadIdx.x == 0 || threadIdx.x == 128);
     for (int64_t k = 0; k < my_tiles; ++k) {
-      load_refs(k + 2);                       // lands while tile k is assembled
+      load_refs(k + 2, pp);                   // lands while tile k is assembled
+      const int buf = (int)(k & 1);
       asm volatile("cp.async.wait_group 1;" ::: "memory");   // window k (window k+1 may still fly)
-      named_bar_sync(1, kProdThreads);
-      const int buf = (int)(k % kWinBufs);
-      const bool in_window = sWinLo[buf] >= 0;
+      named_bar_sync(1, kProdThreads);        // window k landed for every thread; tile k-1 assembled
+      STEM_ACC(0);
+      const int32_t groups = sWin[buf];
+      if (groups > 0) {                       // raw window -> pixel slots (even pixels, then odd pixels)
+        const uint32_t src = sStage_u32 + buf * Cf::kStageBytes;
+        for (int g = threadIdx.x; g < groups; g += kProdThreads) {
+          uint32_t v[4 * C];                  // 8 pixels x C elements
+#pragma unroll
+          for (int q = 0; q < C; ++q) {
+            const uint4 t = lds128(src + (g * C + q) * 16);
+            v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+          }
+          uint32_t s[16];                     // 8 slots x 2 words
+#pragma unroll
+          for (int p = 0; p < 8; ++p) {
+            s[2 * p] = elem16(v, p * C) | (C > 1 ? elem16(v, p * C + 1) << 16 : 0u);
+            s[2 * p + 1] = (C > 2 ? elem16(v, p * C + 2) : 0u) | (C > 3 ? elem16(v, p * C + 3) << 16 : 0u);
+          }
+#pragma unroll
+          for (int par = 0; par < 2; ++par) {
+            const uint32_t dst = sSlot_u32 + (par * Cf::kHalfPix + g * 4) * 8;
+            sts128(dst, s[2 * par], s[2 * par + 1], s[2 * par + 4], s[2 * par + 5]);
+            sts128(dst + 16, s[2 * par + 8], s[2 * par + 9], s[2 * par + 12], s[2 * par + 13]);
+          }
+        }
+      }
+      named_bar_sync(1, kProdThreads);        // slots ready; every thread has read sWin[buf]
+      STEM_ACC(1);
       mbar_wait(&empty[stage], phase ^ 1);
+      STEM_ACC(2);
       const uint32_t tileA = sA_u32 + stage * Cf::kABytes;
-      if (in_window) {
-        const uint32_t win = sWin_u32 + buf * Cf::kWinBytes;
-        const uint32_t rel_base = sRel_u32 + buf * Cf::kRelBytes + row * 4;
-#pragma unroll 1
+      if (groups >= 0) {
+        const uint32_t rel_base = sRel_u32 + (pb.key & 1) * Cf::kRelBytes + row * 4;
+#pragma unroll 2
         for (int g = g_begin; g < g_end; ++g) {
           uint32_t w[4 * C];
 #pragma unroll
           for (int i = 0; i < 8; i += 2) {
             const uint32_t r2 = lds32(rel_base + (g * 4 + i / 2) * kBM * 4);
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-              const uint32_t rel = j ? r2 >> 16 : r2 & 0xFFFFu;
-              const uint32_t addr = win + ((rel * 2) & ~3u);
-              const uint32_t sh = (rel & 1) * 16;
-              const uint32_t lo = lds32(addr), hi = lds32(addr + 4);
-              place_tap<C>(w, i + j, __funnelshift_r(lo, hi, sh), hi >> sh);
-            }
+            const uint2 v0 = lds64(sSlot_u32 + (r2 & 0xFFFFu));
+            const uint2 v1 = lds64(sSlot_u32 + (r2 >> 16));
+            place_tap<C>(w, i, v0.x, v0.y);
+            place_tap<C>(w, i + 1, v1.x, v1.y);
           }
           store_group<C>(w, tileA, row, g);
         }
       } else {
-        // window too large: read the taps from global memory
-        const RowRef rr = row_ref(a, blockIdx.x + k * gridDim.x, row);
+        // window too wide: read the taps from global memory
+        const RowRef rr = row_ref(a, sched.tile(pb), row);
         const IbT* ib = static_cast<const IbT*>(a.ib) + rr.ent0;
+        const uint2 zr = lds64(sSlot_u32 + kWinPix * 8);
 #pragma unroll 1
         for (int g = g_begin; g < g_end; ++g) {
           uint32_t w[4 * C];
@@ -306,9 +441,8 @@ __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __gri
                 lo = __funnelshift_r(l, h, sh);
                 hi = h >> sh;
               } else {
-                const uint32_t* z = reinterpret_cast<const uint32_t*>(sWin + buf * Cf::kWinBytes) + Cf::kWinElems / 2;
-                lo = z[0];
-                hi = z[1];
+                lo = zr.x;
+                hi = zr.y;
               }
             }
             place_tap<C>(w, i, lo, hi);
@@ -318,9 +452,14 @@ __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __gri
       }
       fence_proxy_async_smem();   // generic-proxy smem writes -> visible to the tensor core
       mbar_arrive(&full[stage]);
+      STEM_ACC(3);
       if (++stage == kStagesStem) { stage = 0; phase ^= 1; }
-      prepare(k + 2);              // every producer finished reading window k+2's buffer (tile k-1)
+      prepare(k + 2, pp);
+      sched.advance(pp);
+      sched.advance(pb);
+      STEM_ACC(4);
     }
+    STEM_FLUSH(30 + 5 * half, 5);
   } else if (warp == kMmaWarpStem) {
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t idesc = make_idesc<false>(kBM, BN);
@@ -329,9 +468,13 @@ __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __gri
     uint32_t phase = 0;
     int as = 0;
     uint32_t aphase = 0;
-    for (int64_t tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
+    const int64_t n_local = sched.count();
+    STEM_T0(lane == 0);
+    for (int64_t k = 0; k < n_local; ++k) {
       mbar_wait(&tempty[as], aphase ^ 1);
+      STEM_ACC(0);
       mbar_wait(&full[stage], phase);
+      STEM_ACC(1);
       tc_fence_after();
       if (elect_one()) {
         const uint32_t d = tmem_base + as * BN;
@@ -350,8 +493,10 @@ __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __gri
       if (++stage == kStagesStem) { stage = 0; phase ^= 1; }
       if (++as == 2) { as = 0; aphase ^= 1; }
     }
+    STEM_FLUSH(26, 2);
   } else {
-    epilogue_loop<false, BN, kEpiWarpsStem, BN>(a, warp - kProdWarpsStem, lane, tmem_base, sEpi, sBias, tfull, tempty);
+    epilogue_loop<false, BN, kEpiWarpsStem, BN>(a, warp - kProdWarpsStem, lane, tmem_base, sEpi, sBias, tfull, tempty,
+                                                 sched);
   }
 
   tc_fence_before();
@@ -380,7 +525,13 @@ int launch_stem_t(const ConvArgs& c, cudaStream_t st) {
   fill_tc_args(c, BN, &a);
   const int sms = sm_count();
   const int grid = (int)(a.total_tiles < sms ? a.total_tiles : sms);
-  kernel<<<grid, kThreadsStem, Cf::kSmemBytes, st>>>(tmap, a, (int32_t)x_elems);
+  if (a.total_tiles >= (int64_t(1) << 31)) return fail(ICV_ERR_UNSUPPORTED, "stem kernel: too many tiles");
+  StemTiles tiles{(int32_t)a.total_tiles, 1, (int32_t)a.total_tiles};
+  if (a.ib_per_image && a.ohw % kBM == 0 && a.P / a.ohw > 1 && a.total_tiles == a.P / kBM) {
+    tiles.n_img = (int32_t)(a.P / a.ohw);   // image-major: consecutive tiles share one reference pattern
+    tiles.tpi = (int32_t)(a.ohw / kBM);
+  }
+  kernel<<<grid, kThreadsStem, Cf::kSmemBytes, st>>>(tmap, a, (int32_t)x_elems, tiles);
   note_launch();
   return cuda_check(cudaGetLastError(), "igemm_stem launch");
 }

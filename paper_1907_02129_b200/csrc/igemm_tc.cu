@@ -91,7 +91,9 @@ __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_c
                                                                   const TcArgs a, const PlanS pl) {
   using C = CfgS<kI8, BN>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned base (SW128 atoms); pointer arithmetic keeps the
+  // shared address space visible to the compiler (no generic loads)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + pl.off_b;
   uint8_t* sOnes = smem + pl.off_ones;

@@ -70,7 +70,9 @@ __global__ void __launch_bounds__(kThreadsT, 1) igemm_tmem_kernel(const __grid_c
                                                                   const TcArgs a) {
   using C = CfgT<kI8, BN, IbT>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned base (SW128 atoms); pointer arithmetic keeps the
+  // shared address space visible to the compiler (no generic loads)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sB = smem;
   uint8_t* sOnes = sB + C::kSlots * C::kBBytes;
   IbT* sIB = reinterpret_cast<IbT*>(sOnes + C::kOnesBytes);              // [2][kMaxRST][128]

@@ -421,3 +421,37 @@ def test_per_image_growth_needs_no_rebuild():
     assert grown.offsets is ib1.offsets and grown.batch == 3
     fresh = icv.init_indirection_buffer(x, zero, p, out_shape, icv.TileConfig())
     assert np.array_equal(grown.offsets_host(), fresh.offsets_host())
+
+
+@pytest.mark.parametrize("geom", [
+    dict(r=7, s=7, sy=2, sx=2, pt=3, pl=3, c=3, k=64, n=5, h=32, w=32),    # Ho*Wo = 256: image-major schedule
+    dict(r=7, s=7, sy=2, sx=2, pt=3, pl=3, c=3, k=64, n=4, h=30, w=26),    # tiles straddle images
+    dict(r=7, s=7, sy=2, sx=2, pt=3, pl=3, c=3, k=128, n=3, h=64, w=32),   # 128-wide filter, image-major
+    dict(r=3, s=3, pt=1, pl=1, c=1, k=40, n=7, h=16, w=8),                 # C = 1, image-major
+    dict(r=3, s=3, pt=1, pl=1, c=3, k=32, n=2, h=200, w=190),              # wide rows
+    dict(r=3, s=3, pt=1, pl=1, c=3, k=32, n=2, h=5, w=1500),               # window > 2048 pixels: global path
+])
+@pytest.mark.parametrize("index_dtype", [torch.int64, torch.int32])
+def test_stem_per_image_schedules(geom, index_dtype):
+    """Channel-poor kernel with a per-image buffer: pattern reuse across
+    images (image-major schedule) and tiles straddling two images."""
+    g = dict(geom)
+    n, h, wd = g.pop("n"), g.pop("h"), g.pop("w")
+    p = make_params(**g)
+    shape = icv.Shape4(n, h, wd, p.in_channels)
+    rng = np.random.default_rng(11)
+    xh = rng.standard_normal(shape.numel, dtype=np.float32)
+    wh = rng.standard_normal(p.out_channels * p.kernel_elems * p.in_channels, dtype=np.float32)
+    bias = rng.standard_normal(p.out_channels, dtype=np.float32)
+    tile = icv.TileConfig(mr=128)
+    x = icv.NhwcTensor(shape, torch.from_numpy(xh).to(DEV).to(torch.bfloat16))
+    filt = icv.FilterTensor(p.out_channels, p.kernel_h, p.kernel_w, p.in_channels, torch.from_numpy(wh).to(DEV))
+    pf = icv.pack_filter(filt, torch.from_numpy(bias), p, tile, compute_dtype=torch.bfloat16)
+    zero = icv.make_zero_row(p.in_channels, dtype=torch.bfloat16, device=DEV)
+    out_shape = icv.conv_output_shape(p, shape)
+    assert L.kernel_name(p, shape, torch.bfloat16) == "icv_igemm_stem<bf16>"
+    ib = icv.init_indirection_buffer(x, zero, p, out_shape, tile, index_dtype=index_dtype, per_image=True)
+    y = icv.indirect_conv(x, pf, ib, p, tile).numpy().reshape(-1, p.out_channels)
+    ref = oconv.indirect_conv_f32(oconv.bf16_round(xh), np.zeros(shape.c, np.float32), ib.offsets_host(), p,
+                                  oconv.bf16_round(wh), bias, n, out_shape.h, out_shape.w)
+    assert_bf16_close(y, ref)
