@@ -26,7 +26,7 @@ constexpr int kMaxBias = 2048;          // output channels whose epilogue consta
 // kernel entry [0], after setup [1], MMA warp's last commit of tile i [2+i],
 // epilogue's tmem-full wakeup of tile i [10+i] and release [18+i], producer
 // start of tile i [26+i] (i < 8).  Never compiled into the shipped library.
-extern __device__ unsigned long long g_icv_trace[1024][40];
+extern __device__ unsigned long long g_icv_trace[1024][128];
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -256,7 +256,7 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
 // Host side: TMA map of the packed filter rows (K-major, 128-byte column
 // blocks, 128-byte swizzle) and the common argument block.
 PFN_cuTensorMapEncodeTiled_v12000 get_tensor_map_encoder();
-int make_filter_tmap(const ConvArgs& c, int block_n, CUtensorMap* tmap);
+int make_filter_tmap(const ConvArgs& c, int block_n, int depth, CUtensorMap* tmap);
 int make_input_tmap(const ConvArgs& c, CUtensorMap* tmap);
 void fill_tc_args(const ConvArgs& c, int block_n, TcArgs* a);
 int sm_count();

@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __gri
 
   if (threadIdx.x == 0) {   // resident filter: one TMA box per 128-byte K block
     mbar_arrive_expect_tx(bfull, Cf::kBBytes);
-    for (int b = 0; b < Cf::kBlocks; ++b) tma_load_2d(sB_u32 + b * BN * 128, &tmap_b, bfull, b * 128, 0);
+    tma_load_3d(sB_u32, &tmap_b, bfull, 0, 0, 0);   // all kBlocks K blocks in one box
   }
 
   if (warp < kProdWarpsStem) {
@@ -520,7 +520,7 @@ int launch_stem_t(const ConvArgs& c, cudaStream_t st) {
   });
   if (err != cudaSuccess) return cuda_check(err, "cudaFuncSetAttribute(stem smem)");
   CUtensorMap tmap;
-  if (int s = make_filter_tmap(c, BN, &tmap)) return s;
+  if (int s = make_filter_tmap(c, BN, Cf::kBlocks, &tmap)) return s;
   TcArgs a;
   fill_tc_args(c, BN, &a);
   const int sms = sm_count();

@@ -30,7 +30,7 @@
 namespace icv {
 
 #ifdef ICV_TRACE
-__device__ unsigned long long g_icv_trace[1024][40];
+__device__ unsigned long long g_icv_trace[1024][128];
 #endif
 
 namespace {
@@ -47,7 +47,10 @@ struct CfgS {
   // warp pays one barrier round trip per kKB*4 MMAs.
   static constexpr int kKB = BN >= 256 ? 1 : 2;
   static constexpr int kSlotBytes = kABytes + kBBytes;
-  static constexpr int kMaxSlots = 8;
+#ifndef ICV_MAX_SLOTS
+#define ICV_MAX_SLOTS 8
+#endif
+  static constexpr int kMaxSlots = ICV_MAX_SLOTS;
   static constexpr int kOnesBytes = kI8 ? 16 * 128 : 0;
   static constexpr int kAccStride = kI8 ? 2 * BN : BN;  // TMEM columns per accumulator stage
   static constexpr int kTmemNeed = 2 * kAccStride;
@@ -85,11 +88,39 @@ bool plan_smem(int rs, int n_pad, PlanS* p) {
   return true;
 }
 
-template <bool kI8, int BN, typename IbT>
+// Tile schedule.  kCS = 1: CTA b takes tiles b, b + G, ...  kCS > 1: a
+// cluster of kCS CTAs takes groups of kCS consecutive M tiles with the same
+// N tile (CTA rank r takes M tile group*kCS + r), so the cluster shares
+// every filter block: each CTA TMA-loads 1/kCS of a stage's filter blocks
+// and multicasts it to all kCS CTAs.  M tiles past the end are dummies
+// (clamped references, nothing stored) so the CTAs of a cluster stay in
+// step.
+template <int kCS>
+struct ClusterTiles {
+  int64_t m_tiles;
+  int32_t n_tiles;
+  __device__ __forceinline__ int64_t groups() const { return (m_tiles + kCS - 1) / kCS * n_tiles; }
+  __device__ __forceinline__ int64_t count() const {
+    const int64_t nc = gridDim.x / kCS, c = blockIdx.x / kCS, g = groups();
+    return c < g ? (g - c + nc - 1) / nc : 0;
+  }
+  __device__ __forceinline__ int64_t operator()(int64_t k) const {
+    const int64_t g = blockIdx.x / kCS + k * (gridDim.x / kCS);
+    const int64_t mg = g / n_tiles;
+    const int64_t nt = g - mg * n_tiles;
+    return (mg * kCS + blockIdx.x % kCS) * n_tiles + nt;
+  }
+};
+
+template <bool kI8, int BN, typename IbT, int kCS>
 __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_constant__ CUtensorMap tmap_b,
                                                                   const __grid_constant__ CUtensorMap tmap_x,
                                                                   const TcArgs a, const PlanS pl) {
   using C = CfgS<kI8, BN>;
+  static_assert(kCS == 1 || C::kKB == kCS, "a cluster splits each stage's K blocks across its CTAs");
+  constexpr uint16_t kMask = (uint16_t)((1u << kCS) - 1);
+  const ClusterTiles<kCS> sched{a.total_tiles / a.n_tiles, a.n_tiles};
+  const uint32_t crank = kCS > 1 ? cluster_ctarank() : 0;
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte aligned base (SW128 atoms); pointer arithmetic keeps the
   // shared address space visible to the compiler (no generic loads)
@@ -121,12 +152,12 @@ __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_c
       const uint4 z = __ldg(reinterpret_cast<const uint4*>(a.zero_row) + i);
       nonzero |= (z.x | z.y | z.z | z.w) != 0;
     }
-  const bool tma_gather = a.use_tma_x && !__syncthreads_or(nonzero);
+  const bool tma_gather = kCS == 1 && a.use_tma_x && !__syncthreads_or(nonzero);
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       // TMA path: 1 expect_tx arrival; cp.async path: 128 producer arrivals + 1
       mbar_init(&full[s], tma_gather ? 1 : 128 + 1);
-      mbar_init(&empty[s], 1);       // tcgen05.commit
+      mbar_init(&empty[s], kCS);     // tcgen05.commit of every CTA whose filter blocks land here
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);                   // tcgen05.commit after the last K block
@@ -146,7 +177,8 @@ __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_c
   for (int i = threadIdx.x; i < a.n_pad; i += blockDim.x) sBias[i] = __ldg(static_cast<const uint32_t*>(a.bias) + i);
   if (warp == kMmaWarpS) tmem_alloc<C::kTmemCols>(tmem_slot);
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kCS > 1) cluster_sync_all();   // peers' barriers initialised before any multicast
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) TRACE(1);
@@ -159,11 +191,11 @@ __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_c
     const int chunk = lane & 7;
     const int sub = lane >> 3;
     const int slice_elems = a.RS * kBM;
-    const int64_t my_tiles = blockIdx.x < a.total_tiles ? (a.total_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const int64_t my_tiles = sched.count();
     // cp.async the (R*S taps x 128 pixels) index slice of local tile k into buffer k&1
     auto stage_index_slice = [&](int64_t k) {
       if (k < my_tiles) {
-        const int64_t mt = (blockIdx.x + k * gridDim.x) / a.n_tiles;
+        const int64_t mt = sched(k) / a.n_tiles;
         const uint32_t base = smem_u32(sIB + (k & 1) * slice_elems) + threadIdx.x * (int)sizeof(IbT);
         const RowRef rr = row_ref(a, mt, threadIdx.x);                        // row = threadIdx.x
         const IbT* src = static_cast<const IbT*>(a.ib) + rr.ent0;
@@ -182,7 +214,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_c
     long long p_begin = clock64(), p_wait = 0;
 #endif
     for (int64_t k = 0; k < my_tiles; ++k) {
-      const int64_t tile = blockIdx.x + k * gridDim.x;
+      const int64_t tile = sched(k);
       if (threadIdx.x == 0 && k < 8) TRACE(26 + k);
       stage_index_slice(k + 1);
       const IbT* slice = sIB + (k & 1) * slice_elems;
@@ -212,12 +244,13 @@ __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_c
 #ifdef ICV_TRACE
                 p_wait += clock64() - pw0;
 #endif
-                if (lane == 0)
-                  mbar_arrive_expect_tx(&full[stage], min(C::kKB, num_kb - kb) * (kABytes + C::kBBytes));
+                if (lane == 0) {
+                  mbar_arrive_expect_tx(&full[stage], min(C::kKB, num_kb - kb) * kABytes + C::kKB * C::kBBytes);
+                  tma_load_3d(sB_u32 + stage * C::kKB * C::kBBytes, &tmap_b, &full[stage], 0, nt * BN, kb);
+                }
                 __syncwarp();
               }
               const int slot = stage * C::kKB + j;
-              if (lane == 0) tma_load_2d(sB_u32 + slot * C::kBBytes, &tmap_b, &full[stage], kb * 128, nt * BN);
               tma_gather4(sA_u32 + slot * kABytes + lane * 512, &tmap_x, &full[stage], cb * a.cblock_elems,
                           rows4[0], rows4[1], rows4[2], rows4[3]);
               if (j == C::kKB - 1 || kb == num_kb - 1) {
@@ -227,50 +260,95 @@ __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_c
           }
         }
       } else {
-        // cp.async path (any zero row): 8 lanes per 128-byte row, 4 rows per
-        // instruction, completion tracked by cp.async.mbarrier.arrive
-        int kb = 0;
-        for (int e = 0; e < a.RS; ++e) {
-          const uint8_t* src[8];
+        // cp.async path (any zero row): 8 lanes per 128-byte row (lane & 7 =
+        // 16-byte chunk), 4 rows per instruction -- whole 128-byte lines per
+        // request, which the LSU/L2 path moves fastest.  Per tap each lane
+        // resolves ONE row reference (its own row of the warp's 32) and the 8
+        // row pointers an instruction needs are exchanged by shuffles; rows
+        // 4i+sub with the same i&1 share one swizzle pattern, so the shared
+        // destinations are two registers plus immediates, and with the
+        // channel-block count known at compile time the source offsets are
+        // immediates too.
+        const int myrow = warp * 32 + lane;
+        const int64_t mybase = rbase[myrow];
+        const bool c_full = (a.c_bytes & 127) == 0;
+        uint32_t dofs[2];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int r = warp * 32 + 4 * i + sub;
-            const int64_t off = resolve_ref((int64_t)slice[e * kBM + r], rbase[r]);
-            src[i] = off < 0 ? a.zero_row : a.x + off * a.elem_bytes;  // ZERO_REF -> bound zero row
-          }
-          for (int cb = 0; cb < a.cblocks; ++cb, ++kb) {
-            const int j = kb % C::kKB;
-            if (j == 0) {
-#ifdef ICV_TRACE
-              long long pw0 = clock64();
-#endif
-              mbar_wait(&empty[stage], phase ^ 1);
-#ifdef ICV_TRACE
-              p_wait += clock64() - pw0;
-#endif
-              if (threadIdx.x == 0) mbar_arrive_expect_tx(&full[stage], min(C::kKB, num_kb - kb) * C::kBBytes);
-            }
-            const int slot = stage * C::kKB + j;
-            if (threadIdx.x == 0) tma_load_2d(sB_u32 + slot * C::kBBytes, &tmap_b, &full[stage], kb * 128, nt * BN);
-            const int b = cb * 128 + chunk * 16;
-            int valid = a.c_bytes - b;
-            valid = valid < 0 ? 0 : (valid > 16 ? 16 : valid);
-            const uint32_t dst0 = sA_u32 + slot * kABytes;
+        for (int b = 0; b < 2; ++b) dofs[b] = (warp * 32 + 4 * b + sub) * 128 + ((chunk ^ (4 * b + sub)) << 4);
+        auto gather_tile = [&](auto cbc) {
+          constexpr int kCBc = decltype(cbc)::value;   // 0: runtime channel-block count
+          const int cblocks = kCBc ? kCBc : a.cblocks;
+          int kb = 0;
+          int stage_seq = (int)(k * ((num_kb + C::kKB - 1) / C::kKB));
+          for (int e = 0; e < a.RS; ++e) {
+            const int64_t off = resolve_ref((int64_t)slice[e * kBM + myrow], mybase);
+            const uint8_t* mine = off < 0 ? a.zero_row : a.x + off * a.elem_bytes;   // ZERO_REF -> zero row
+            const uint8_t* src[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int row = warp * 32 + 4 * i + sub;
-              cp_async_16(dst0 + row * 128 + ((chunk ^ (row & 7)) << 4), src[i] + (valid ? b : 0), (uint32_t)valid);
-            }
-            if (j == C::kKB - 1 || kb == num_kb - 1) {
-              cp_async_mbar_arrive_noinc(&full[stage]);
-              if (++stage == kStages) { stage = 0; phase ^= 1; }
+            for (int i = 0; i < 8; ++i)
+              src[i] = reinterpret_cast<const uint8_t*>(
+                           __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(mine), 4 * i + sub)) +
+                       chunk * 16;
+#pragma unroll(kCBc ? kCBc : 1)
+            for (int cb = 0; cb < cblocks; ++cb, ++kb) {
+              const int j = kb % C::kKB;
+              if (j == 0) {
+#ifdef ICV_TRACE
+                long long pw0 = clock64();
+#endif
+                mbar_wait(&empty[stage], phase ^ 1);
+#ifdef ICV_TRACE
+                p_wait += clock64() - pw0;
+                if (threadIdx.x == 0 && k == 1 && kb / C::kKB < 16) TRACE(64 + kb / C::kKB);   // stage free
+#endif
+                // the stage's filter blocks: one 3-D box (kKB K blocks; a tail
+                // block past the filter is zero-filled and never multiplied),
+                // issued by the producer warps in turn
+                if (lane == 0 && warp == (stage_seq & 3)) {
+                  mbar_arrive_expect_tx(&full[stage], C::kKB * C::kBBytes);
+                  if constexpr (kCS == 1)
+                    tma_load_3d(sB_u32 + stage * C::kKB * C::kBBytes, &tmap_b, &full[stage], 0, nt * BN, kb);
+                  else   // this CTA's K block of the stage, to every CTA of the cluster
+                    tma_load_3d_mc(sB_u32 + (stage * C::kKB + crank) * C::kBBytes, &tmap_b, &full[stage], 0,
+                                   nt * BN, kb + (int)crank, kMask);
+                }
+                ++stage_seq;
+              }
+              const uint32_t slot_base = sA_u32 + (stage * C::kKB + j) * kABytes;
+              const uint32_t d0 = slot_base + dofs[0], d1 = slot_base + dofs[1];
+#ifndef ICV_EXP_NOA   // experiment: no A gathers
+              if (c_full || cb + 1 < cblocks) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                  cp_async_16_full((i & 1 ? d1 : d0) + (i >> 1) * 1024, src[i] + cb * 128);
+              } else {   // partial last channel block: zero-fill past C
+                int valid = a.c_bytes - (cb * 128 + chunk * 16);
+                valid = valid < 0 ? 0 : (valid > 16 ? 16 : valid);
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                  cp_async_16((i & 1 ? d1 : d0) + (i >> 1) * 1024, valid ? src[i] + cb * 128 : a.x, (uint32_t)valid);
+              }
+#endif
+              if (j == C::kKB - 1 || kb == num_kb - 1) {
+#ifdef ICV_TRACE
+                if (threadIdx.x == 0 && k == 1 && kb / C::kKB < 16) TRACE(96 + kb / C::kKB);   // stage issued
+#endif
+                cp_async_mbar_arrive_noinc(&full[stage]);
+                if (++stage == kStages) { stage = 0; phase ^= 1; }
+              }
             }
           }
-        }
+        };
+        if (c_full && a.cblocks == 1) gather_tile(std::integral_constant<int, 1>{});
+        else if (c_full && a.cblocks == 2) gather_tile(std::integral_constant<int, 2>{});
+        else if (c_full && a.cblocks == 4) gather_tile(std::integral_constant<int, 4>{});
+        else gather_tile(std::integral_constant<int, 0>{});
       }
+      if (threadIdx.x == 0 && k < 8) TRACE(40 + k);   // producer: all of tile k's loads issued
       // slice k+1 landed (its group was committed before this tile's gathers)
       // and every producer is done reading slice k
       cp_async_wait_committed();
+      if (threadIdx.x == 0 && k < 8) TRACE(48 + k);   // producer: next slice landed
       named_bar_sync(1, 128);
     }
 #ifdef ICV_TRACE
@@ -292,7 +370,8 @@ __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_c
 #ifdef ICV_TRACE
     long long c_wait_full = 0, c_wait_tempty = 0, c_begin = clock64();
 #endif
-    for (int64_t tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
+    const int64_t n_local = sched.count();
+    for (int64_t ti_local = 0; ti_local < n_local; ++ti_local) {
 #ifdef ICV_TRACE
       long long c0 = clock64();
 #endif
@@ -310,6 +389,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_c
         mbar_wait(&full[stage], phase);
 #ifdef ICV_TRACE
         c_wait_full += clock64() - c1;
+        if (lane == 0 && ti_local == 1 && si < 16) TRACE(80 + si);   // stage full (MMA warp wakes)
 #endif
         tc_fence_after();
         if (elect_one()) {
@@ -320,18 +400,21 @@ __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_c
 #pragma unroll
             for (int k = 0; k < 4; ++k) {  // 4 x 32-byte K steps per 128-byte block
               const uint32_t acc = (si | j | k) != 0;
+#ifndef ICV_EXP_NOMMA   // experiment: fills only
               tc_mma<kI8>(d, adesc + 2 * k, bdesc + 2 * k, idesc, acc);
+#endif
               if constexpr (kI8) tc_mma<true>(d + BN, adesc + 2 * k, ones_desc + 2 * k, idesc_ones, acc);
             }
           }
-          tc_commit(&empty[stage]);
+          if constexpr (kCS == 1) tc_commit(&empty[stage]);
+          else tc_commit_mc(&empty[stage], kMask);   // the stage is free in every CTA that fills it
           if (si == stages_per_tile - 1) tc_commit(&tfull[as]);
         }
         __syncwarp();
         if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
       if (lane == 0) {
-        const int ti = (int)((tile - blockIdx.x) / gridDim.x);
+        const int ti = (int)ti_local;
         if (ti < 8) TRACE(2 + ti);
       }
       if (++as == 2) { as = 0; aphase ^= 1; }
@@ -344,7 +427,8 @@ __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_c
     }
 #endif
   } else {
-    epilogue_loop<kI8, BN, kEpiWarpsS, C::kAccStride>(a, warp - 4, lane, tmem_base, sEpi, sBias, tfull, tempty);
+    epilogue_loop<kI8, BN, kEpiWarpsS, C::kAccStride>(a, warp - 4, lane, tmem_base, sEpi, sBias, tfull, tempty,
+                                                      sched);
   }
 
   tc_fence_before();
@@ -353,34 +437,90 @@ __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_c
     tc_fence_after();
     tmem_dealloc<C::kTmemCols>(tmem_base);
   }
+  if constexpr (kCS > 1) cluster_sync_all();   // no peer still signals or writes into this CTA
 }
 
-template <bool kI8, int BN, typename IbT>
-int launch_smem(const ConvArgs& c, cudaStream_t st) {
-  auto kernel = igemm_smem_kernel<kI8, BN, IbT>;
+template <bool kI8, int BN, typename IbT, int kCS>
+int launch_smem_cs(const ConvArgs& c, cudaStream_t st) {
+  auto kernel = igemm_smem_kernel<kI8, BN, IbT, kCS>;
   static std::once_flag attr_once;
   static cudaError_t attr_err = cudaSuccess;
-  std::call_once(attr_once, [&] {
-    attr_err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-  });
-  if (attr_err != cudaSuccess) return cuda_check(attr_err, "cudaFuncSetAttribute(smem)");
+  static int max_clusters = 0;
   PlanS pl;
   if (!plan_smem<kI8, BN, IbT>(c.g.RS(), c.L.n_pad, &pl))
     return fail(ICV_ERR_UNSUPPORTED, "indirection slice of this kernel size does not fit in shared memory");
+  std::call_once(attr_once, [&] {
+    attr_err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    if (attr_err == cudaSuccess && kCS > 1) {
+      // how many clusters fit at once (some GPCs may not hold a whole pair)
+      cudaLaunchConfig_t q = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = kCS;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      q.gridDim = dim3(kCS * 74);
+      q.blockDim = dim3(kThreadsS);
+      q.dynamicSmemBytes = pl.bytes;
+      q.attrs = at;
+      q.numAttrs = 1;
+      attr_err = cudaOccupancyMaxActiveClusters(&max_clusters, kernel, &q);
+    }
+  });
+  if (attr_err != cudaSuccess) return cuda_check(attr_err, "kernel attributes (smem / clusters)");
   CUtensorMap tmap, tmap_x;
-  if (int s = make_filter_tmap(c, BN, &tmap)) return s;
+  if (int s = make_filter_tmap(c, BN, kCS > 1 ? 1 : CfgS<kI8, BN>::kKB, &tmap)) return s;
   TcArgs a;
   fill_tc_args(c, BN, &a);
   // TMA tile::gather4 for A is correct but ~2.5x slower than the cp.async
   // gather on B200 (measured); kept behind ICV_TMA_GATHER=1 for experiments.
   static const char* tg = getenv("ICV_TMA_GATHER");
-  a.use_tma_x = (tg && tg[0] == '1') && make_input_tmap(c, &tmap_x) == ICV_OK;
+  a.use_tma_x = kCS == 1 && (tg && tg[0] == '1') && make_input_tmap(c, &tmap_x) == ICV_OK;
   if (!a.use_tma_x) tmap_x = tmap;   // unused placeholder
   const int sms = sm_count();
-  const int grid = (int)(a.total_tiles < sms ? a.total_tiles : sms);
-  kernel<<<grid, kThreadsS, pl.bytes, st>>>(tmap, tmap_x, a, pl);
+  if constexpr (kCS == 1) {
+    const int grid = (int)(a.total_tiles < sms ? a.total_tiles : sms);
+    kernel<<<grid, kThreadsS, pl.bytes, st>>>(tmap, tmap_x, a, pl);
+  } else {
+    const int64_t groups = (a.total_tiles / a.n_tiles + kCS - 1) / kCS * a.n_tiles;
+    int64_t clusters = sms / kCS;
+    if (max_clusters > 0 && clusters > max_clusters) clusters = max_clusters;
+    if (clusters > groups) clusters = groups;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kCS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3((unsigned)(clusters * kCS));
+    cfg.blockDim = dim3(kThreadsS);
+    cfg.dynamicSmemBytes = pl.bytes;
+    cfg.stream = st;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, tmap, tmap_x, a, pl); e != cudaSuccess)
+      return cuda_check(e, "igemm_smem cluster launch");
+  }
   note_launch();
   return cuda_check(cudaGetLastError(), "igemm_smem launch");
+}
+
+// Filter-sharing clusters of 2 CTAs for BLOCK_N <= 128 (each CTA TMA-loads
+// half of a stage's filter blocks and multicasts them).  Correct, but on
+// B200 it measured slower than independent CTAs (the mainloop is bound by
+// L2->SM delivery into each SM, which multicast does not reduce), so it is
+// opt-in: ICV_CLUSTER=2.
+bool use_clusters() {
+  static const char* v = getenv("ICV_CLUSTER");
+  return v && v[0] == '2';
+}
+
+template <bool kI8, int BN, typename IbT>
+int launch_smem(const ConvArgs& c, cudaStream_t st) {
+  if constexpr (CfgS<kI8, BN>::kKB == 2) {
+    if (use_clusters()) return launch_smem_cs<kI8, BN, IbT, 2>(c, st);
+  }
+  return launch_smem_cs<kI8, BN, IbT, 1>(c, st);
 }
 
 template <typename IbT>
@@ -428,14 +568,15 @@ PFN_cuTensorMapEncodeTiled_v12000 get_tensor_map_encoder() {
   return fn;
 }
 
-int make_filter_tmap(const ConvArgs& c, int block_n, CUtensorMap* tmap) {
+int make_filter_tmap(const ConvArgs& c, int block_n, int depth, CUtensorMap* tmap) {
   auto encode = get_tensor_map_encoder();
   if (!encode) return fail(ICV_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  const cuuint64_t dims[2] = {(cuuint64_t)c.L.row_bytes, (cuuint64_t)c.L.n_pad};
-  const cuuint64_t strides[1] = {(cuuint64_t)c.L.row_bytes};
-  const cuuint32_t box[2] = {128, (cuuint32_t)block_n};
-  const cuuint32_t estr[2] = {1, 1};
-  CUresult cr = encode(tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(c.packed + c.L.w_off), dims,
+  // packed rows viewed as [K blocks][n_pad rows][128 B]; box = depth K blocks of block_n rows
+  const cuuint64_t dims[3] = {128, (cuuint64_t)c.L.n_pad, (cuuint64_t)(c.L.row_bytes / 128)};
+  const cuuint64_t strides[2] = {(cuuint64_t)c.L.row_bytes, 128};
+  const cuuint32_t box[3] = {128, (cuuint32_t)block_n, (cuuint32_t)depth};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult cr = encode(tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(c.packed + c.L.w_off), dims,
                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return fail(ICV_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
@@ -537,7 +678,7 @@ extern "C" ICV_API int icv_debug_trace(unsigned long long* host, int reset) {
   if (host && cudaMemcpyFromSymbol(host, icv::g_icv_trace, sizeof(icv::g_icv_trace)) != cudaSuccess)
     return ICV_ERR_CUDA;
   if (reset) {
-    static unsigned long long zeros[1024][40];
+    static unsigned long long zeros[1024][128];
     if (cudaMemcpyToSymbol(icv::g_icv_trace, zeros, sizeof(zeros)) != cudaSuccess) return ICV_ERR_CUDA;
   }
   return ICV_OK;

@@ -171,9 +171,9 @@ __global__ void __launch_bounds__(kThreadsT, 1) igemm_tmem_kernel(const __grid_c
         const int64_t tile = blockIdx.x + k * gridDim.x;
         const int nt = (int)(tile % a.n_tiles);
         const int nsub = min(C::kKB, num_kb - 2 * si);
-        mbar_arrive_expect_tx(&full[stage], nsub * C::kBBytes);
-        for (int j = 0; j < nsub; ++j)
-          tma_load_2d(sB_u32 + (stage * C::kKB + j) * C::kBBytes, &tmap_b, &full[stage], (2 * si + j) * 128, nt * BN);
+        (void)nsub;
+        mbar_arrive_expect_tx(&full[stage], C::kKB * C::kBBytes);   // tail blocks past the filter are zero-filled
+        tma_load_3d(sB_u32 + stage * C::kKB * C::kBBytes, &tmap_b, &full[stage], 0, nt * BN, C::kKB * si);
       }
       if (kb < num_kb) {
         const uint32_t col = C::kABase + (uint32_t)(stage * C::kKB + h) * 32;
@@ -287,7 +287,7 @@ int launch_tmem(const ConvArgs& c, cudaStream_t st) {
   });
   if (attr_err != cudaSuccess) return cuda_check(attr_err, "cudaFuncSetAttribute(smem)");
   CUtensorMap tmap;
-  if (int s = make_filter_tmap(c, BN, &tmap)) return s;
+  if (int s = make_filter_tmap(c, BN, Cf::kKB, &tmap)) return s;
   TcArgs a;
   fill_tc_args(c, BN, &a);
   const int sms = sm_count();

@@ -33,7 +33,7 @@ def main():
     icv.indirect_conv(x, pf, ib, w.params, tile, out=y)
     e.record()
     torch.cuda.synchronize()
-    buf = np.zeros((1024, 40), np.uint64)
+    buf = np.zeros((1024, 128), np.uint64)
     fn(buf.ctypes.data, 0)
     tr = buf[:148].astype(np.int64)
     t0 = tr[:, 0][tr[:, 0] > 0].min()
@@ -45,8 +45,9 @@ def main():
     for cta in (0, 1, 73, 147):
         r = rel[cta]
         tiles = [i for i in range(8) if r[2 + i] >= 0]
-        row = " | ".join(f"t{i}: prod {r[26 + i] / 1e3:.2f} mma_end {r[2 + i] / 1e3:.2f} "
-                         f"epi {r[10 + i] / 1e3:.2f}-{r[18 + i] / 1e3:.2f}" for i in tiles)
+        row = " | ".join(f"t{i}: prod {r[26 + i] / 1e3:.2f}-{r[40 + i] / 1e3:.2f} slice {r[48 + i] / 1e3:.2f} "
+                         f"mma_end {r[2 + i] / 1e3:.2f} epi {r[10 + i] / 1e3:.2f}-{r[18 + i] / 1e3:.2f}"
+                         for i in tiles)
         print(f"cta {cta:3d} entry {r[0] / 1e3:.2f} setup {r[1] / 1e3:.2f} :: {row}")
     cyc = buf[:148, 34].astype(np.float64)
     wf = buf[:148, 35].astype(np.float64)
@@ -62,5 +63,36 @@ def main():
           f"median epilogue {np.median((rel[:, 18] - rel[:, 10])[rel[:, 10] >= 0]) / 1e3:.2f} us")
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and not (len(sys.argv) > 2 and sys.argv[2] == "stages"):
     main()
+
+
+def stages(name="cfg2"):
+    """Per-stage timeline of tile 1 (CTA 0..3): stage free -> issued -> full."""
+    from paper_1907_02129_b200.workloads import CONFIGS
+
+    dev = torch.device("cuda", 0)
+    w, x, xh, pf, ib, y, tile = bench.setup_problem(name, 0, CONFIGS[name].in_shape.n, dev)
+    fn = L.lib().icv_debug_trace
+    fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for _ in range(3):
+        icv.indirect_conv(x, pf, ib, w.params, tile, out=y)
+    fn(None, 1)
+    flush.fill_(1)
+    icv.indirect_conv(x, pf, ib, w.params, tile, out=y)
+    torch.cuda.synchronize()
+    buf = np.zeros((1024, 128), np.uint64)
+    fn(buf.ctypes.data, 0)
+    for cta in range(4):
+        r = buf[cta].astype(np.int64)
+        t0 = r[0]
+        print(f"cta {cta}: (us after entry) free / issued / full per stage")
+        for s_ in range(12):
+            if r[64 + s_] == 0:
+                break
+            print(f"   s{s_:2d}: {(r[64 + s_] - t0) / 1e3:7.2f} {(r[96 + s_] - t0) / 1e3:7.2f} {(r[80 + s_] - t0) / 1e3:7.2f}")
+
+
+if __name__ == "__main__" and len(sys.argv) > 2 and sys.argv[2] == "stages":
+    stages(sys.argv[1])

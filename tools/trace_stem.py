@@ -35,7 +35,7 @@ def main():
     icv.indirect_conv(x, pf, ib, w.params, tile, out=y)
     e.record()
     torch.cuda.synchronize()
-    buf = np.zeros((1024, 40), np.uint64)
+    buf = np.zeros((1024, 128), np.uint64)
     fn(buf.ctypes.data, 0)
     oh, ow = w.out_hw
     tiles = w.in_shape.n * oh * ow / 128 / 148
