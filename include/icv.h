@@ -163,6 +163,13 @@ ICV_API int icv_conv_kernel_name(const icv_conv_desc* desc, const icv_shape4* in
  * process (all entry points).  For the bench's gpu_launches claim. */
 ICV_API int64_t icv_launch_count(void);
 
+/* NHWC max pooling (bf16 / f32), padding taps skipped (-inf padding).  Not
+ * part of the reference operator: the ResNet-50 conv stack (cfg5, SURVEY.md
+ * §8(d)) pools the stem output 3x3 / stride 2 / pad 1 before stage 1.
+ * Output shape (n, (h + 2*ph - kh)/sh + 1, (w + 2*pw - kw)/sw + 1, c). */
+ICV_API int icv_maxpool2d(const icv_shape4* in, int32_t kh, int32_t kw, int32_t sh, int32_t sw, int32_t ph,
+                          int32_t pw, int32_t dtype, const void* x, void* y, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -63,6 +63,7 @@ SIGNATURES = {
     "icv_conv_kernel_name": (ctypes.c_int, [ctypes.POINTER(Desc), ctypes.POINTER(Shape), _I32,
                                             ctypes.POINTER(ctypes.c_char_p)]),
     "icv_launch_count": (_I64, []),
+    "icv_maxpool2d": (ctypes.c_int, [ctypes.POINTER(Shape), _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P, _P, _P]),
 }
 
 _lock = threading.Lock()

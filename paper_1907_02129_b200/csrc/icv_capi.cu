@@ -131,6 +131,16 @@ ICV_API const char* icv_last_error(void) { return g_last_error.c_str(); }
 
 ICV_API int64_t icv_launch_count(void) { return g_launches.load(); }
 
+ICV_API int icv_maxpool2d(const icv_shape4* in, int32_t kh, int32_t kw, int32_t sh, int32_t sw, int32_t ph,
+                          int32_t pw, int32_t dtype, const void* x, void* y, void* stream) {
+  if (!in || !x || !y) return fail(ICV_ERR_ARG, "icv_maxpool2d: null argument");
+  if (in->n < 1 || in->h < 1 || in->w < 1 || in->c < 1 || kh < 1 || kw < 1 || sh < 1 || sw < 1 || ph < 0 || pw < 0 ||
+      ph >= kh || pw >= kw)
+    return fail(ICV_ERR_ARG, "icv_maxpool2d: invalid geometry");
+  if (in->h + 2 * ph < kh || in->w + 2 * pw < kw) return fail(ICV_ERR_GEOMETRY, "icv_maxpool2d: window does not fit");
+  return launch_maxpool(*in, kh, kw, sh, sw, ph, pw, dtype, x, y, static_cast<cudaStream_t>(stream));
+}
+
 ICV_API int icv_device_info(int32_t device, int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor) {
   int v;
   if (int s = cuda_check(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device), "sm count")) return s;

@@ -53,6 +53,7 @@ struct TcArgs {
   uint32_t c_inv;            // odd^-1 mod 2^32
   int32_t use_tma_x;         // input tensor map valid (TMA gathers allowed)
   int32_t ib_per_image;      // buffer holds image 0's (image-relative) references
+  int32_t use_tma_y;         // output tensor map valid: epilogue stores tiles with TMA
   int64_t ohw, img_elems;    // Ho*Wo, H*W*C
 };
 
@@ -120,18 +121,26 @@ struct StridedTiles {
   __device__ __forceinline__ int64_t operator()(int64_t k) const { return blockIdx.x + k * gridDim.x; }
 };
 
+// Epilogue staging per warp: two 32-row tiles of one 32-column chunk (the
+// TMA-store path double-buffers them; the fallback path uses 80/48-byte
+// padded rows in the same space).  1024-byte aligned in the TMA kernels.
+template <bool kI8>
+constexpr int kEpiWarpBytes = kI8 ? 2048 : 4096;
+
 template <bool kI8, int BN, int kEpiWarps, int kAccStride, typename Sched = StridedTiles>
 __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane, uint32_t tmem_base, uint8_t* sEpi,
                                               const uint32_t* sBias, uint64_t* tfull, uint64_t* tempty,
-                                              Sched sched = Sched{0}) {
+                                              Sched sched = Sched{0}, const CUtensorMap* tmap_y = nullptr) {
   constexpr int kOutRowBytes = kI8 ? 32 : 64;
   constexpr int kStageRowBytes = kI8 ? 48 : 80;  // padded: row-per-lane staging writes are conflict free
   const int slot = ew & 3;
   constexpr int kColGroups = kEpiWarps / 4;
   constexpr int kColsPerWarp = BN / kColGroups;
   const int col0 = (ew / 4) * kColsPerWarp;
-  uint8_t* stg = sEpi + ew * 32 * kStageRowBytes;
+  uint8_t* stg = sEpi + ew * kEpiWarpBytes<kI8>;
   const bool vec_ok = kI8 ? (a.K & 15) == 0 : (a.K & 7) == 0;
+  const bool use_tma = tmap_y != nullptr;
+  int chunk_seq = 0;
   int as = 0;
   uint32_t aphase = 0;
   if constexpr (std::is_same<Sched, StridedTiles>::value) sched.total = a.total_tiles;
@@ -205,6 +214,36 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
           w[q] = word;
         }
       }
+      if (use_tma) {
+        // stage the 32 x 32 block as the TMA box (bf16: 64-byte rows with the
+        // 64-byte swizzle, conflict-free row-per-lane writes; u8: dense
+        // 32-byte rows) and let one lane store it; TMA clips rows >= P and
+        // columns >= K.  Two buffers: wait until the store issued two chunks
+        // ago has read its source.
+        const uint32_t sb = smem_u32(stg) + (chunk_seq & 1) * (32 * kOutRowBytes);
+        if (chunk_seq >= 2) {
+          if (lane == 0) bulk_wait_group_read<1>();
+          __syncwarp();
+        }
+#pragma unroll
+        for (int q = 0; q < kOutRowBytes / 16; ++q) {
+          const int phys = kI8 ? q : (q ^ ((lane >> 1) & 3));
+          sts128(sb + lane * kOutRowBytes + phys * 16, w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(tmap_y, sb, n, (int32_t)row0);
+          bulk_commit_group();
+        }
+        ++chunk_seq;
+        if (ci + 1 < nchunks) {
+          tmem_ld_wait_regs(vn);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = vn[i];
+        }
+        continue;
+      }
       uint4* my = reinterpret_cast<uint4*>(stg + lane * kStageRowBytes);
 #pragma unroll
       for (int q = 0; q < kOutRowBytes / 16; ++q) my[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
@@ -244,6 +283,7 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
     if (ew == 0 && lane == 0 && ti_ < 8) TRACE(18 + ti_);
     if (++as == 2) { as = 0; aphase ^= 1; }
   }
+  if (use_tma && lane == 0) bulk_wait_group<0>();   // output written before the CTA exits
 #ifdef ICV_TRACE
   if (ew == 0 && lane == 0) {
     g_icv_trace[blockIdx.x][28] = (unsigned long long)t_wait;
@@ -258,6 +298,7 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
 PFN_cuTensorMapEncodeTiled_v12000 get_tensor_map_encoder();
 int make_filter_tmap(const ConvArgs& c, int block_n, int depth, CUtensorMap* tmap);
 int make_input_tmap(const ConvArgs& c, CUtensorMap* tmap);
+int make_output_tmap(const ConvArgs& c, CUtensorMap* tmap);
 void fill_tc_args(const ConvArgs& c, int block_n, TcArgs* a);
 int sm_count();
 

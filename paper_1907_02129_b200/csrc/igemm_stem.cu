@@ -27,7 +27,6 @@ constexpr int kEpiWarpsStem = 4;
 constexpr int kMmaWarpStem = kProdWarpsStem + kEpiWarpsStem;
 constexpr int kThreadsStem = 32 * (kMmaWarpStem + 1);
 constexpr int kStagesStem = 2;          // A tiles in flight
-constexpr int kWinPix = 2048;           // input-window capacity in pixels (cfg3a needs <= 1834)
 
 // Byte offset of element offset `d` (a multiple of C) in the pixel-slot
 // window (8 bytes per pixel): d / C * 8 = d * kSlotMul (mod 2^32).
@@ -100,7 +99,7 @@ struct CfgStem {
   static constexpr int kBlocks = (kKSteps * 16 + 63) / 64;  // 128-byte K blocks per row
   static constexpr int kABytes = kBM * kBlocks * 128;       // one A tile
   static constexpr int kBBytes = BN * kBlocks * 128;        // resident filter
-  static constexpr int kEpiBytes = kEpiWarpsStem * 32 * 80;
+  static constexpr int kEpiBytes = kEpiWarpsStem * kEpiWarpBytes<false>;
   // Taps are assembled in groups of 8: 8 taps x C elements = C whole 16-byte
   // chunks of the A row.  kGroups groups cover the kKSteps*16 elements the
   // MMA reads (taps past R*S read a zero slot); the two producer halves take
@@ -109,6 +108,9 @@ struct CfgStem {
   static constexpr int kG0 = (kGroups + 1) / 2;
   static constexpr int kTapsHalf = kG0 * 8;                 // taps per producer thread (max)
   static constexpr int kTaps = kGroups * 8;
+  // input-window capacity in pixels (cfg3a needs <= 1834; a 128-wide
+  // resident 7x7x3 filter leaves room for half of that)
+  static constexpr int kWinPix = (BN > 64 && RS * C > 64) ? 1024 : 2048;
   // staged input window: raw NHWC bytes of up to kWinPix pixels (cp.async)
   static constexpr int kStageBytes = kWinPix * C * 2;
   // pixel-slot window: 8 bytes per pixel (C elements, zero padded), then two
@@ -146,9 +148,6 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
   return v;
 }
-__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
-}
 
 // element j (0 .. 2*N-1) of a little-endian array of N packed bf16 pairs
 template <int N>
@@ -177,6 +176,7 @@ __device__ __forceinline__ void store_group(const uint32_t (&w)[4 * C], uint32_t
 
 template <int C, int RS, int BN, typename IbT>
 __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __grid_constant__ CUtensorMap tmap_b,
+                                                                     const __grid_constant__ CUtensorMap tmap_y,
                                                                      const TcArgs a, int32_t x_elems,
                                                                      const StemTiles tiles) {
   using Cf = CfgStem<C, RS, BN>;
@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __gri
   if (threadIdx.x < 8) {   // the two fixed slots: bound zero row, then true zeros
     const int j = threadIdx.x;
     const uint16_t* z = reinterpret_cast<const uint16_t*>(a.zero_row);
-    uint16_t* slot = reinterpret_cast<uint16_t*>(sSlot + kWinPix * 8);
+    uint16_t* slot = reinterpret_cast<uint16_t*>(sSlot + Cf::kWinPix * 8);
     slot[j] = (j < 4 && j < C) ? __ldg(z + j) : (uint16_t)0;
   }
   if (warp == kMmaWarpStem) tmem_alloc<(2 * BN <= 128 ? 128 : 256)>(tmem_slot);
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __gri
     // coalesced 16-byte cp.async and every reference becomes a 16-bit slot
     // offset; when the tile comes up, the window is re-laid out as one
     // 8-byte slot per pixel, so each tap is a single aligned 8-byte shared
-    // load.  A window wider than kWinPix pixels (never for the ResNet stem)
+    // load.  A window wider than Cf::kWinPix pixels (never for the ResNet stem)
     // falls back to reading the taps straight from global memory.
     const int half = warp >> 2;
     const int row = threadIdx.x & (kBM - 1);
@@ -315,10 +315,10 @@ __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __gri
           if (threadIdx.x == 0) { sKeyW0[ks] = w0; sKeyGroups[ks] = groups; }
           kw_groups = groups;
           kw_w0 = w0;
-          // pixel s of the window lives in slot (s & 1) * kHalfPix + (s >> 1); ZERO_REF -> slot kWinPix
-          // (pixel 2 * kWinPix), taps past R*S -> slot kWinPix + 1
-          const int32_t d = row_valid ? w0 - base : -2 * kWinPix * C;
-          const uint32_t zc = (uint32_t)(2 * kWinPix * C + d);
+          // pixel s of the window lives in slot (s & 1) * kHalfPix + (s >> 1); ZERO_REF -> slot Cf::kWinPix
+          // (pixel 2 * Cf::kWinPix), taps past R*S -> slot Cf::kWinPix + 1
+          const int32_t d = row_valid ? w0 - base : -2 * Cf::kWinPix * C;
+          const uint32_t zc = (uint32_t)(2 * Cf::kWinPix * C + d);
           const uint32_t rel_base = sRel_u32 + ks * Cf::kRelBytes + ((g_begin * 4) * kBM + row) * 4;
 #pragma unroll
           for (int i = 0; i < Cf::kTapsHalf; i += 2) {
@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __gri
               for (int j = 0; j < 2; ++j) {
                 const uint32_t px = (min((uint32_t)ref[i + j], zc) - (uint32_t)d) * kSlotMul<C> / 8;
                 const uint32_t off = i + j < n_real ? ((px & 1) * Cf::kHalfPix + (px >> 1)) * 8
-                                                    : (uint32_t)(kWinPix + 1) * 8;
+                                                    : (uint32_t)(Cf::kWinPix + 1) * 8;
                 r2 |= (off & 0xFFFFu) << (16 * j);
               }
               asm volatile("st.shared.u32 [%0], %1;" ::"r"(rel_base + (i / 2) * kBM * 4), "r"(r2) : "memory");
@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __gri
         int32_t groups = sKeyGroups[ks], w0 = sKeyW0[ks];
         if (new_key(k, p)) { groups = kw_groups; w0 = kw_w0; }
         w0 += p.img * (int32_t)a.img_elems;
-        const bool fits = groups * 8 <= kWinPix;
+        const bool fits = groups * 8 <= Cf::kWinPix;
         if (threadIdx.x == 0) sWin[buf] = fits ? groups : -1;
         if (fits) {
           const uint32_t dst = sStage_u32 + buf * Cf::kStageBytes;
@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __gri
         // window too wide: read the taps from global memory
         const RowRef rr = row_ref(a, sched.tile(pb), row);
         const IbT* ib = static_cast<const IbT*>(a.ib) + rr.ent0;
-        const uint2 zr = lds64(sSlot_u32 + kWinPix * 8);
+        const uint2 zr = lds64(sSlot_u32 + Cf::kWinPix * 8);
 #pragma unroll 1
         for (int g = g_begin; g < g_end; ++g) {
           uint32_t w[4 * C];
@@ -496,7 +496,7 @@ __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __gri
     STEM_FLUSH(26, 2);
   } else {
     epilogue_loop<false, BN, kEpiWarpsStem, BN>(a, warp - kProdWarpsStem, lane, tmem_base, sEpi, sBias, tfull, tempty,
-                                                 sched);
+                                                 sched, a.use_tma_y ? &tmap_y : nullptr);
   }
 
   tc_fence_before();
@@ -531,7 +531,10 @@ int launch_stem_t(const ConvArgs& c, cudaStream_t st) {
     tiles.n_img = (int32_t)(a.P / a.ohw);   // image-major: consecutive tiles share one reference pattern
     tiles.tpi = (int32_t)(a.ohw / kBM);
   }
-  kernel<<<grid, kThreadsStem, Cf::kSmemBytes, st>>>(tmap, a, (int32_t)x_elems, tiles);
+  CUtensorMap tmap_y;
+  a.use_tma_y = make_output_tmap(c, &tmap_y) == ICV_OK;
+  if (!a.use_tma_y) tmap_y = tmap;   // unused placeholder
+  kernel<<<grid, kThreadsStem, Cf::kSmemBytes, st>>>(tmap, tmap_y, a, (int32_t)x_elems, tiles);
   note_launch();
   return cuda_check(cudaGetLastError(), "igemm_stem launch");
 }

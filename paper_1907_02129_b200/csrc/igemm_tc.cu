@@ -55,7 +55,7 @@ struct CfgS {
   static constexpr int kAccStride = kI8 ? 2 * BN : BN;  // TMEM columns per accumulator stage
   static constexpr int kTmemNeed = 2 * kAccStride;
   static constexpr uint32_t kTmemCols = kTmemNeed <= 64 ? 64 : kTmemNeed <= 128 ? 128 : kTmemNeed <= 256 ? 256 : 512;
-  static constexpr int kEpiBytes = kEpiWarpsS * 32 * (kI8 ? 48 : 80);
+  static constexpr int kEpiBytes = kEpiWarpsS * kEpiWarpBytes<kI8>;
   static constexpr int kBarBytes = 256;
   static_assert(kTmemNeed <= 512, "TMEM overflow");
 };
@@ -71,7 +71,7 @@ template <bool kI8, int BN, typename IbT>
 bool plan_smem(int rs, int n_pad, PlanS* p) {
   using C = CfgS<kI8, BN>;
   const int bias = (n_pad * 4 + 15) / 16 * 16;
-  const int ib = 2 * rs * kBM * (int)sizeof(IbT) + 2 * kBM * 8;   // index slices + per-row bases
+  const int ib = 2 * rs * kBM * 4 + 2 * kBM * 4;   // int32 index slices + per-row bases
   const int fixed = 1024 + C::kOnesBytes + C::kEpiBytes + bias + ib + C::kBarBytes;
   int slots = (232448 - fixed) / C::kSlotBytes;
   slots = (slots > C::kMaxSlots ? C::kMaxSlots : slots) / C::kKB * C::kKB;
@@ -115,6 +115,7 @@ struct ClusterTiles {
 template <bool kI8, int BN, typename IbT, int kCS>
 __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_constant__ CUtensorMap tmap_b,
                                                                   const __grid_constant__ CUtensorMap tmap_x,
+                                                                  const __grid_constant__ CUtensorMap tmap_y,
                                                                   const TcArgs a, const PlanS pl) {
   using C = CfgS<kI8, BN>;
   static_assert(kCS == 1 || C::kKB == kCS, "a cluster splits each stage's K blocks across its CTAs");
@@ -130,8 +131,10 @@ __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_c
   uint8_t* sOnes = smem + pl.off_ones;
   uint8_t* sEpi = smem + pl.off_epi;
   uint32_t* sBias = reinterpret_cast<uint32_t*>(smem + pl.off_bias);
-  int64_t* sRowBase = reinterpret_cast<int64_t*>(smem + pl.off_ib);   // [2][128] per-image base offsets
-  IbT* sIB = reinterpret_cast<IbT*>(smem + pl.off_ib + 2 * kBM * 8);  // [2][RS][128] index slices
+  int32_t* sRowBase = reinterpret_cast<int32_t*>(smem + pl.off_ib);   // [2][128] per-image base offsets
+  // [2][RS][128] index slices and [2][128] per-row image bases, 32-bit (the
+  // launcher requires N*H*W*C < 2^31; an int64 entry's low word is its value)
+  int32_t* sIB = reinterpret_cast<int32_t*>(smem + pl.off_ib + 2 * kBM * 4);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + pl.off_bar);
   const int kStages = pl.stages;
   uint64_t* empty = full + kStages;
@@ -196,12 +199,12 @@ __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_c
     auto stage_index_slice = [&](int64_t k) {
       if (k < my_tiles) {
         const int64_t mt = sched(k) / a.n_tiles;
-        const uint32_t base = smem_u32(sIB + (k & 1) * slice_elems) + threadIdx.x * (int)sizeof(IbT);
+        const uint32_t base = smem_u32(sIB + (k & 1) * slice_elems) + threadIdx.x * 4;
         const RowRef rr = row_ref(a, mt, threadIdx.x);                        // row = threadIdx.x
         const IbT* src = static_cast<const IbT*>(a.ib) + rr.ent0;
-        sRowBase[(k & 1) * kBM + threadIdx.x] = rr.base;
+        sRowBase[(k & 1) * kBM + threadIdx.x] = (int32_t)rr.base;
         for (int e = 0; e < a.RS; ++e)
-          cp_async_ca<sizeof(IbT)>(base + e * kBM * (int)sizeof(IbT), src + (int64_t)e * a.mr);
+          cp_async_ca<4>(base + e * kBM * 4, src + (int64_t)e * a.mr);
       }
       cp_async_commit();
     };
@@ -217,8 +220,8 @@ __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_c
       const int64_t tile = sched(k);
       if (threadIdx.x == 0 && k < 8) TRACE(26 + k);
       stage_index_slice(k + 1);
-      const IbT* slice = sIB + (k & 1) * slice_elems;
-      const int64_t* rbase = sRowBase + (k & 1) * kBM;
+      const int32_t* slice = sIB + (k & 1) * slice_elems;
+      const int32_t* rbase = sRowBase + (k & 1) * kBM;
       const int nt = (int)(tile % a.n_tiles);
       if (tma_gather) {
         // TMA path: warp 0 issues, per K block, one tile::gather4 per lane
@@ -428,7 +431,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_c
 #endif
   } else {
     epilogue_loop<kI8, BN, kEpiWarpsS, C::kAccStride>(a, warp - 4, lane, tmem_base, sEpi, sBias, tfull, tempty,
-                                                      sched);
+                                                      sched, a.use_tma_y ? &tmap_y : nullptr);
   }
 
   tc_fence_before();
@@ -449,6 +452,8 @@ int launch_smem_cs(const ConvArgs& c, cudaStream_t st) {
   PlanS pl;
   if (!plan_smem<kI8, BN, IbT>(c.g.RS(), c.L.n_pad, &pl))
     return fail(ICV_ERR_UNSUPPORTED, "indirection slice of this kernel size does not fit in shared memory");
+  if (c.g.N * c.g.H * c.g.W * (int64_t)c.g.C >= (int64_t(1) << 31))
+    return fail(ICV_ERR_UNSUPPORTED, "tensor-core kernel: input tensors of 2^31 or more elements are not supported");
   std::call_once(attr_once, [&] {
     attr_err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     if (attr_err == cudaSuccess && kCS > 1) {
@@ -477,10 +482,13 @@ int launch_smem_cs(const ConvArgs& c, cudaStream_t st) {
   static const char* tg = getenv("ICV_TMA_GATHER");
   a.use_tma_x = kCS == 1 && (tg && tg[0] == '1') && make_input_tmap(c, &tmap_x) == ICV_OK;
   if (!a.use_tma_x) tmap_x = tmap;   // unused placeholder
+  CUtensorMap tmap_y;
+  a.use_tma_y = make_output_tmap(c, &tmap_y) == ICV_OK;
+  if (!a.use_tma_y) tmap_y = tmap;   // unused placeholder
   const int sms = sm_count();
   if constexpr (kCS == 1) {
     const int grid = (int)(a.total_tiles < sms ? a.total_tiles : sms);
-    kernel<<<grid, kThreadsS, pl.bytes, st>>>(tmap, tmap_x, a, pl);
+    kernel<<<grid, kThreadsS, pl.bytes, st>>>(tmap, tmap_x, tmap_y, a, pl);
   } else {
     const int64_t groups = (a.total_tiles / a.n_tiles + kCS - 1) / kCS * a.n_tiles;
     int64_t clusters = sms / kCS;
@@ -498,7 +506,7 @@ int launch_smem_cs(const ConvArgs& c, cudaStream_t st) {
     cfg.stream = st;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    if (cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, tmap, tmap_x, a, pl); e != cudaSuccess)
+    if (cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, tmap, tmap_x, tmap_y, a, pl); e != cudaSuccess)
       return cuda_check(e, "igemm_smem cluster launch");
   }
   note_launch();
@@ -587,6 +595,31 @@ int make_filter_tmap(const ConvArgs& c, int block_n, int depth, CUtensorMap* tma
 // = C elements; box = one 128-byte channel block of one row; 128-byte
 // swizzle (the A tile's canonical layout).  Rows < 0 or >= N*H*W and
 // columns >= C are zero-filled by TMA.
+// 2-D view of the output (rows = output pixels of the batch, columns = K)
+// for the epilogue's TMA tile stores: box = 32 columns x 32 rows; bf16 rows
+// of the box are 64 bytes with the 64-byte swizzle, uint8 rows 32 bytes
+// unswizzled.  Needs 16-byte aligned rows (K*elem % 16 == 0).
+int make_output_tmap(const ConvArgs& c, CUtensorMap* tmap) {
+  static const char* off = getenv("ICV_TMA_STORE");
+  if (off && off[0] == '0') return ICV_ERR_UNSUPPORTED;
+  const bool i8 = c.L.family == kFamTcU8;
+  if (!i8 && c.L.family != kFamTcBf16 && c.L.family != kFamStemBf16) return ICV_ERR_UNSUPPORTED;
+  const int eb = i8 ? 1 : 2;
+  if ((c.g.K * eb) % 16 != 0 || (reinterpret_cast<uintptr_t>(c.y) & 15) != 0) return ICV_ERR_UNSUPPORTED;
+  if (c.P >= (int64_t(1) << 31)) return ICV_ERR_UNSUPPORTED;
+  auto encode = get_tensor_map_encoder();
+  if (!encode) return ICV_ERR_CUDA;
+  const cuuint64_t dims[2] = {(cuuint64_t)c.g.K, (cuuint64_t)c.P};
+  const cuuint64_t strides[1] = {(cuuint64_t)c.g.K * eb};
+  const cuuint32_t box[2] = {32, 32};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult cr = encode(tmap, i8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, c.y, dims, strides,
+                       box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                       i8 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return cr == CUDA_SUCCESS ? ICV_OK : ICV_ERR_CUDA;
+}
+
 int make_input_tmap(const ConvArgs& c, CUtensorMap* tmap) {
   if (c.L.family != kFamTcBf16 && c.L.family != kFamTcU8) return ICV_ERR_UNSUPPORTED;
   const int64_t rows = c.g.N * c.g.H * c.g.W;
@@ -609,6 +642,7 @@ int make_input_tmap(const ConvArgs& c, CUtensorMap* tmap) {
 
 void fill_tc_args(const ConvArgs& c, int block_n, TcArgs* a) {
   const bool i8 = c.L.family == kFamTcU8;
+  a->use_tma_y = 0;
   a->x = static_cast<const uint8_t*>(c.x);
   a->zero_row = static_cast<const uint8_t*>(c.zero_row);
   a->ib = c.ib;

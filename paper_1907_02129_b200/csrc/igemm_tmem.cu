@@ -50,7 +50,7 @@ struct CfgT {
   static constexpr int kBBytes = BN * 128;
   static constexpr int kOnesBytes = kI8 ? 16 * 128 : 0;
   static constexpr int kIbBytes = kMaxRST * kBM * (int)sizeof(IbT);   // one tile's index slice
-  static constexpr int kEpiBytes = kEpiWarpsT * 32 * (kI8 ? 48 : 80);
+  static constexpr int kEpiBytes = kEpiWarpsT * kEpiWarpBytes<kI8>;
   static constexpr int kBiasBytes = 4 * kMaxBias;
   static constexpr int kBarBytes = 256;
   static constexpr int kSmemBytes =

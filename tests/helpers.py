@@ -18,7 +18,7 @@ def fill_uniform(numel: int, seed: int) -> np.ndarray:
     return np.random.default_rng(seed).uniform(-1.0, 1.0, numel).astype(np.float32)
 
 
-def assert_bf16_close(got: np.ndarray, ref: np.ndarray, rel: float = REL_TOL_BF16) -> dict:
+def assert_bf16_close(got: np.ndarray, ref: np.ndarray, rel: float = REL_TOL_BF16, what: str = "") -> dict:
     """The bf16 tolerance of this repo: normwise
     max|got - ref| / max|ref| <= rel AND elementwise
     |got - ref| <= rel*|ref| + rel*rms(ref)."""
@@ -30,6 +30,6 @@ def assert_bf16_close(got: np.ndarray, ref: np.ndarray, rel: float = REL_TOL_BF1
     rms = float(np.sqrt(np.mean(ref * ref))) if ref.size else 1.0
     normwise = float(err.max() / scale) if ref.size else 0.0
     bad = err > rel * np.abs(ref) + rel * rms
-    assert normwise <= rel, f"normwise rel error {normwise:.3e} > {rel}"
-    assert not bad.any(), f"{int(bad.sum())} elements outside rtol={rel}, atol={rel}*rms"
+    assert normwise <= rel, f"{what}: normwise rel error {normwise:.3e} > {rel}"
+    assert not bad.any(), f"{what}: {int(bad.sum())} elements outside rtol={rel}, atol={rel}*rms"
     return {"normwise": normwise, "max_abs": float(err.max()) if ref.size else 0.0}
