@@ -46,9 +46,16 @@ def load_peaks() -> dict:
         with open(path) as f:
             p = json.load(f)
         p["which"] = "measured"
-        return p
     except OSError:
-        return dict(PEAKS_FALLBACK)
+        p = dict(PEAKS_FALLBACK)
+    try:   # int8 / fp32 peaks measured on a B200 of this pool (tools/measure_peaks.py)
+        with open(os.path.join(ROOT, "profiles", "peaks_extra.json")) as f:
+            extra = json.load(f)
+        p["int8_tops"] = extra.get("int8_tops")
+        p["fp32_tflops"] = extra.get("fp32_tflops")
+    except (OSError, ValueError):
+        pass
+    return p
 
 
 # ----------------------------------------------------------------- clocks
@@ -246,7 +253,8 @@ def roofline_for(w, ms: float, peaks: dict, sustained: bool = False) -> dict:
     HBM-bound ones against the measured copy bandwidth."""
     ridge_tflops = peaks["bf16_tflops_sustained" if sustained else "bf16_tflops"]
     if w.dtype == "u8":
-        ridge_tflops = 2.0 * ridge_tflops
+        # measured int8 GEMM peak (tools/measure_peaks.py -> profiles/peaks_extra.json), else 2x bf16 (nominal)
+        ridge_tflops = peaks.get("int8_tops") or 2.0 * ridge_tflops
     ai = w.flops / w.compulsory_bytes
     hbm = peaks["hbm_gbs"]
     if ai * hbm / 1e3 >= ridge_tflops and w.dtype != "f32":
@@ -368,6 +376,7 @@ def gpu_bench(args) -> None:
                             "kernel": _lib.kernel_name(ow_.params, ow_.in_shape, ox.dtype),
                             "roofline": roofline_for(ow_, oms, peaks)}
             del ox, opf, oib_, oy
+        other["cfg5"] = stack_bench(device, peaks, flush)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -419,6 +428,40 @@ def gpu_bench(args) -> None:
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def stack_bench(device, peaks: dict, flush, batch: int = 256, passes: int = 5) -> dict:
+    """cfg5: the 53-layer ResNet-50 conv stack, N=256, chained through the
+    public API (paper_1907_02129_b200/stack.py); median of `passes` passes
+    after 2 warm-up passes, L2 flushed before each (the activations are far
+    larger than L2 anyway).  Per-layer parity is tests/test_gpu_stack.py."""
+    import torch
+
+    from paper_1907_02129_b200.stack import ResNet50Stack
+
+    stack = ResNet50Stack(batch=batch, device=device)
+    for _ in range(2):
+        stack.run()
+    totals, pools, per = [], [], []
+    for _ in range(passes):
+        flush()
+        t, pool, layers = stack.timed_run()
+        totals.append(t)
+        pools.append(pool)
+        per.append(layers)
+    total = statistics.median(totals)
+    conv = sum(statistics.median(p[i] for p in per) for i in range(len(stack.layers)))
+    bf16, hbm = peaks["bf16_tflops"], peaks["hbm_gbs"]
+    roof_ms = sum(max(l.flops / (bf16 * 1e9), l.compulsory_bytes / (hbm * 1e6)) for l in stack.layers)
+    res = {"workload": f"cfg5_resnet50_conv_stack_bf16_n{batch}", "dtype": "bf16", "layers": len(stack.layers),
+           "ms_per_step": round(total, 4), "conv_ms": round(conv, 4), "maxpool_ms": round(statistics.median(pools), 4),
+           "value": round(stack.flops / (total * 1e-3) / 1e12, 2), "unit": "TFLOP/s (end to end, max pool included)",
+           "value_convs_only": round(stack.flops / (conv * 1e-3) / 1e12, 2),
+           "sum_of_layer_rooflines_ms": round(roof_ms, 4), "frac_of_sum_roofline": round(roof_ms / conv, 3),
+           "per_layer": "profiles/r01_cfg5_layers.json (tools/time_stack.py)"}
+    del stack
+    torch.cuda.empty_cache()
+    return res
 
 
 def correctness_gate(w, xh, pf, ib, y) -> dict:
