@@ -21,7 +21,10 @@ constexpr int kBM = 128;                // output pixels per tile (TMEM lanes / 
 constexpr int kABytes = kBM * 128;      // one 128-byte K block of the A tile
 constexpr int kMaxBias = 2048;          // output channels whose epilogue constants live in smem
 
-#ifdef ICV_TRACE
+#if defined(ICV_STEM_PHASES) && !defined(ICV_TRACE)
+extern __device__ unsigned long long g_icv_trace[1024][128];
+#define TRACE(slot)
+#elif defined(ICV_TRACE)
 // Debug-build timeline (tools/trace_conv.py): per CTA, globaltimer (ns) at
 // kernel entry [0], after setup [1], MMA warp's last commit of tile i [2+i],
 // epilogue's tmem-full wakeup of tile i [10+i] and release [18+i], producer
@@ -127,7 +130,7 @@ struct StridedTiles {
 template <bool kI8>
 constexpr int kEpiWarpBytes = kI8 ? 2048 : 4096;
 
-template <bool kI8, int BN, int kEpiWarps, int kAccStride, typename Sched = StridedTiles>
+template <bool kI8, int BN, int kEpiWarps, int kAccStride, typename Sched = StridedTiles, int kAccStages = 2>
 __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane, uint32_t tmem_base, uint8_t* sEpi,
                                               const uint32_t* sBias, uint64_t* tfull, uint64_t* tempty,
                                               Sched sched = Sched{0}, const CUtensorMap* tmap_y = nullptr) {
@@ -173,7 +176,12 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
       rowsum = (int32_t)rs;
     }
     const int cols_left = a.K - nt * BN - col0;
+#ifdef ICV_EXP_NOEPI   // experiment: release the accumulators without storing
+    const int nchunks = 0;
+    (void)cols_left;
+#else
     const int nchunks = cols_left > 0 ? (min(kColsPerWarp, cols_left) + 31) / 32 : 0;
+#endif
     uint32_t v[32];
     if (nchunks > 0) {
       tmem_ld_32x32b_x32(taddr + col0, v);
@@ -281,7 +289,7 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
     }
 #endif
     if (ew == 0 && lane == 0 && ti_ < 8) TRACE(18 + ti_);
-    if (++as == 2) { as = 0; aphase ^= 1; }
+    if (++as == kAccStages) { as = 0; aphase ^= 1; }
   }
   if (use_tma && lane == 0) bulk_wait_group<0>();   // output written before the CTA exits
 #ifdef ICV_TRACE

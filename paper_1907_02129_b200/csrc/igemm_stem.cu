@@ -26,7 +26,12 @@ constexpr int kProdThreads = 32 * kProdWarpsStem;
 constexpr int kEpiWarpsStem = 4;
 constexpr int kMmaWarpStem = kProdWarpsStem + kEpiWarpsStem;
 constexpr int kThreadsStem = 32 * (kMmaWarpStem + 1);
+#ifndef ICV_STEM_ACC
+#define ICV_STEM_ACC 2
+#endif
+constexpr int kAccStagesStem = ICV_STEM_ACC;       // TMEM accumulators in flight (MMA runs ahead of the epilogue)
 constexpr int kStagesStem = 2;          // A tiles in flight
+constexpr int kPrefetch = 4;            // L2 prefetch distance of input windows (tiles, image-major)
 
 // Byte offset of element offset `d` (a multiple of C) in the pixel-slot
 // window (8 bytes per pixel): d / C * 8 = d * kSlotMul (mod 2^32).
@@ -73,7 +78,7 @@ struct StemSched {
   __device__ __forceinline__ int64_t operator()(int64_t k) const { return tile(pos(k)); }
 };
 
-#ifdef ICV_TRACE
+#if defined(ICV_TRACE) || defined(ICV_STEM_PHASES)
 // debug build: per-CTA cycle accumulators of the producer / MMA phases
 // (slots 26..39 of g_icv_trace, tools/trace_stem.py), kept in registers
 #define STEM_T0(cond) long long _t = clock64(), _acc[5] = {0, 0, 0, 0, 0}; const bool _tr = (cond)
@@ -120,7 +125,7 @@ struct CfgStem {
   static constexpr int kHalfPix = kWinPix / 2;              // even pixels, then odd pixels
   static constexpr int kMiscBytes = 1024;                   // bias, reductions, window bases
   static constexpr int kSmemBytes = 1024 + kStagesStem * kABytes + kBBytes + kEpiBytes + 2 * kStageBytes +
-                                    kSlotBytes + 2 * kRelBytes + kMiscBytes + 256;
+                                    2 * kSlotBytes + 2 * kRelBytes + kMiscBytes + 256;
   static_assert(kSmemBytes <= 232448, "shared memory overflow");
   static_assert(C >= 1 && C <= 4, "channel-poor kernel handles 1..4 channels");
   static_assert(kGroups * C * 8 <= kBlocks * 64, "tap groups overflow the A row");
@@ -188,8 +193,8 @@ __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __gri
   uint8_t* sB = sA + kStagesStem * Cf::kABytes;
   uint8_t* sEpi = sB + Cf::kBBytes;
   uint8_t* sStage = sEpi + Cf::kEpiBytes;                            // [2] raw input windows
-  uint8_t* sSlot = sStage + 2 * Cf::kStageBytes;                     // pixel-slot window (+ 2 zero slots)
-  uint8_t* sRel = sSlot + Cf::kSlotBytes;                            // [2][kTaps/2][128][2] slot offsets
+  uint8_t* sSlot = sStage + 2 * Cf::kStageBytes;                     // [2] pixel-slot windows (+ 2 zero slots)
+  uint8_t* sRel = sSlot + 2 * Cf::kSlotBytes;                        // [2][kTaps/2][128][2] slot offsets
   uint8_t* sMisc = sRel + 2 * Cf::kRelBytes;
   uint32_t* sBias = reinterpret_cast<uint32_t*>(sMisc);                         // 128 x 4 B
   int32_t* sRed = reinterpret_cast<int32_t*>(sMisc + 512);                      // [2][2][8] min/max per warp
@@ -199,9 +204,10 @@ __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __gri
   uint64_t* full = reinterpret_cast<uint64_t*>(sMisc + Cf::kMiscBytes);
   uint64_t* empty = full + kStagesStem;
   uint64_t* tfull = empty + kStagesStem;
-  uint64_t* tempty = tfull + 2;
-  uint64_t* bfull = tempty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
+  uint64_t* tempty = tfull + kAccStagesStem;
+  uint64_t* bfull = tempty + kAccStagesStem;
+  uint64_t* winbar = bfull + 1;                                      // [2] raw window landed (bulk copy)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(winbar + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -211,22 +217,24 @@ __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __gri
       mbar_init(&full[s], kProdThreads);   // every producer thread (st.shared + proxy fence + arrive)
       mbar_init(&empty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < kAccStagesStem; ++s) {
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], 32 * kEpiWarpsStem);
     }
     mbar_init(bfull, 1);
+    for (int s = 0; s < 2; ++s) mbar_init(&winbar[s], 1);
     fence_mbar_init();
     tma_prefetch_desc(&tmap_b);
   }
   for (int i = threadIdx.x; i < a.n_pad; i += blockDim.x) sBias[i] = __ldg(static_cast<const uint32_t*>(a.bias) + i);
-  if (threadIdx.x < 8) {   // the two fixed slots: bound zero row, then true zeros
-    const int j = threadIdx.x;
+  if (threadIdx.x < 16) {   // the two fixed slots of each slot buffer: bound zero row, then true zeros
+    const int j = threadIdx.x & 7;
     const uint16_t* z = reinterpret_cast<const uint16_t*>(a.zero_row);
-    uint16_t* slot = reinterpret_cast<uint16_t*>(sSlot + Cf::kWinPix * 8);
+    uint16_t* slot = reinterpret_cast<uint16_t*>(sSlot + (threadIdx.x >> 3) * Cf::kSlotBytes + Cf::kWinPix * 8);
     slot[j] = (j < 4 && j < C) ? __ldg(z + j) : (uint16_t)0;
   }
-  if (warp == kMmaWarpStem) tmem_alloc<(2 * BN <= 128 ? 128 : 256)>(tmem_slot);
+  constexpr uint32_t kTmemCols = kAccStagesStem * BN <= 256 ? 256 : 512;
+  if (warp == kMmaWarpStem) tmem_alloc<kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -285,7 +293,6 @@ __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __gri
       if (k < my_tiles) {
         const int buf = (int)(k & 1);
         const int ks = p.key & 1;
-        int32_t kw_groups = 0, kw_w0 = 0;
         if (new_key(k, p)) {
           uint32_t lo = 0xFFFFFFFFu;   // ZERO_REF (-1) and padding (-2) are the largest as unsigned
           int32_t hi = -1;
@@ -313,8 +320,6 @@ __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __gri
           const int32_t w0 = hi < 0 ? 0 : (int32_t)(lo / (8 * C) * (8 * C));   // 8-pixel (16C-byte) aligned
           const int32_t groups = hi < 0 ? 0 : ((hi - w0) / C + 8) / 8;           // 8-pixel groups spanned
           if (threadIdx.x == 0) { sKeyW0[ks] = w0; sKeyGroups[ks] = groups; }
-          kw_groups = groups;
-          kw_w0 = w0;
           // pixel s of the window lives in slot (s & 1) * kHalfPix + (s >> 1); ZERO_REF -> slot Cf::kWinPix
           // (pixel 2 * Cf::kWinPix), taps past R*S -> slot Cf::kWinPix + 1
           const int32_t d = row_valid ? w0 - base : -2 * Cf::kWinPix * C;
@@ -335,23 +340,38 @@ __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __gri
             }
           }
         }
-        // (a reused pattern's window was published to smem before an earlier barrier)
-        int32_t groups = sKeyGroups[ks], w0 = sKeyW0[ks];
-        if (new_key(k, p)) { groups = kw_groups; w0 = kw_w0; }
-        w0 += p.img * (int32_t)a.img_elems;
-        const bool fits = groups * 8 <= Cf::kWinPix;
-        if (threadIdx.x == 0) sWin[buf] = fits ? groups : -1;
-        if (fits) {
-          const uint32_t dst = sStage_u32 + buf * Cf::kStageBytes;
-          const uint8_t* src = a.x + (int64_t)w0 * 2;
-          for (int32_t ch = threadIdx.x; ch < groups * C; ch += kProdThreads) {
-            int32_t valid = (x_elems - (w0 + ch * 8)) * 2;
-            valid = valid < 0 ? 0 : (valid > 16 ? 16 : valid);
-            cp_async_16(dst + (uint32_t)ch * 16, valid ? src + ch * 16 : a.x, (uint32_t)valid);
+        // One bulk copy of the window's bytes (contiguous NHWC pixels) into
+        // sStage[k & 1], tracked by winbar[k & 1] (the stage buffer is free:
+        // every producer converted tile k-2 before the last barrier).  With
+        // the image-major schedule the same pattern's window kPrefetch images
+        // later is pulled into L2 at the same time.
+        if (threadIdx.x == 0) {
+          const int32_t groups = sKeyGroups[ks];
+          const int32_t w0 = sKeyW0[ks] + p.img * (int32_t)a.img_elems;
+          const bool fits = groups * 8 <= Cf::kWinPix;
+          sWin[buf] = fits ? groups : -1;
+          if (fits && groups > 0) {
+            const int64_t end = (int64_t)w0 + groups * 8 * C;            // window end (elements)
+            const int64_t lim = end < x_elems ? end : x_elems;
+            const uint32_t bytes = (uint32_t)(((lim - w0) * 2) & ~15LL);   // whole 16-byte chunks in bounds
+            const uint32_t dst = sStage_u32 + buf * Cf::kStageBytes;
+            // a ragged tail (< 16 bytes, only the tensor's last chunk) is copied by this thread
+            for (int64_t b = bytes; b < (lim - w0) * 2; b += 2)
+              asm volatile("st.shared.u16 [%0], %1;" ::"r"(dst + (uint32_t)b),
+                           "h"(__ldg(reinterpret_cast<const uint16_t*>(a.x) + w0 + b / 2)) : "memory");
+            mbar_arrive_expect_tx(&winbar[buf], bytes);
+            if (bytes) bulk_load(dst, a.x + (int64_t)w0 * 2, bytes, &winbar[buf]);
+            if (sched.n_img > 1 && p.img + kPrefetch < sched.n_img && k + kPrefetch < my_tiles) {
+              const int64_t pw0 = (int64_t)w0 + (int64_t)kPrefetch * a.img_elems;
+              const int64_t pend = pw0 + groups * 8 * C < x_elems ? pw0 + groups * 8 * C : x_elems;
+              const uint32_t pbytes = (uint32_t)(((pend - pw0) * 2) & ~15LL);
+              if (pbytes) bulk_prefetch_l2(a.x + pw0 * 2, pbytes);
+            }
+          } else {
+            mbar_arrive(&winbar[buf]);
           }
         }
       }
-      cp_async_commit();
     };
 
     // prologue: windows of tiles 0 and 1
@@ -369,10 +389,10 @@ __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __gri
     for (int64_t k = 0; k < my_tiles; ++k) {
       load_refs(k + 2, pp);                   // lands while tile k is assembled
       const int buf = (int)(k & 1);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");   // window k (window k+1 may still fly)
-      named_bar_sync(1, kProdThreads);        // window k landed for every thread; tile k-1 assembled
+      mbar_wait(&winbar[buf], (uint32_t)(k >> 1) & 1u);   // window k landed (and sWin[buf] published)
       STEM_ACC(0);
       const int32_t groups = sWin[buf];
+      const uint32_t slots = sSlot_u32 + buf * Cf::kSlotBytes;
       if (groups > 0) {                       // raw window -> pixel slots (even pixels, then odd pixels)
         const uint32_t src = sStage_u32 + buf * Cf::kStageBytes;
         for (int g = threadIdx.x; g < groups; g += kProdThreads) {
@@ -390,18 +410,24 @@ __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __gri
           }
 #pragma unroll
           for (int par = 0; par < 2; ++par) {
-            const uint32_t dst = sSlot_u32 + (par * Cf::kHalfPix + g * 4) * 8;
+            const uint32_t dst = slots + (par * Cf::kHalfPix + g * 4) * 8;
             sts128(dst, s[2 * par], s[2 * par + 1], s[2 * par + 4], s[2 * par + 5]);
             sts128(dst + 16, s[2 * par + 8], s[2 * par + 9], s[2 * par + 12], s[2 * par + 13]);
           }
         }
       }
-      named_bar_sync(1, kProdThreads);        // slots ready; every thread has read sWin[buf]
+      // slots of tile k ready; every producer finished tile k-1 (so slot buffer
+      // buf^1 and its stage are free for tile k+1) and has read sWin[buf]
+      named_bar_sync(1, kProdThreads);
       STEM_ACC(1);
       mbar_wait(&empty[stage], phase ^ 1);
       STEM_ACC(2);
       const uint32_t tileA = sA_u32 + stage * Cf::kABytes;
+#ifdef ICV_EXP_STEM_NOBUILD
+      if (false) {
+#else
       if (groups >= 0) {
+#endif
         const uint32_t rel_base = sRel_u32 + (pb.key & 1) * Cf::kRelBytes + row * 4;
 #pragma unroll 2
         for (int g = g_begin; g < g_end; ++g) {
@@ -409,18 +435,18 @@ __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __gri
 #pragma unroll
           for (int i = 0; i < 8; i += 2) {
             const uint32_t r2 = lds32(rel_base + (g * 4 + i / 2) * kBM * 4);
-            const uint2 v0 = lds64(sSlot_u32 + (r2 & 0xFFFFu));
-            const uint2 v1 = lds64(sSlot_u32 + (r2 >> 16));
+            const uint2 v0 = lds64(slots + (r2 & 0xFFFFu));
+            const uint2 v1 = lds64(slots + (r2 >> 16));
             place_tap<C>(w, i, v0.x, v0.y);
             place_tap<C>(w, i + 1, v1.x, v1.y);
           }
           store_group<C>(w, tileA, row, g);
         }
-      } else {
+      } else if (groups < 0) {
         // window too wide: read the taps from global memory
         const RowRef rr = row_ref(a, sched.tile(pb), row);
         const IbT* ib = static_cast<const IbT*>(a.ib) + rr.ent0;
-        const uint2 zr = lds64(sSlot_u32 + Cf::kWinPix * 8);
+        const uint2 zr = lds64(slots + Cf::kWinPix * 8);
 #pragma unroll 1
         for (int g = g_begin; g < g_end; ++g) {
           uint32_t w[4 * C];
@@ -491,11 +517,12 @@ __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __gri
       }
       __syncwarp();
       if (++stage == kStagesStem) { stage = 0; phase ^= 1; }
-      if (++as == 2) { as = 0; aphase ^= 1; }
+      if (++as == kAccStagesStem) { as = 0; aphase ^= 1; }
     }
     STEM_FLUSH(26, 2);
   } else {
-    epilogue_loop<false, BN, kEpiWarpsStem, BN>(a, warp - kProdWarpsStem, lane, tmem_base, sEpi, sBias, tfull, tempty,
+    epilogue_loop<false, BN, kEpiWarpsStem, BN, StemSched, kAccStagesStem>(a, warp - kProdWarpsStem, lane, tmem_base,
+                                                                         sEpi, sBias, tfull, tempty,
                                                  sched, a.use_tma_y ? &tmap_y : nullptr);
   }
 
@@ -503,7 +530,7 @@ __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __gri
   __syncthreads();
   if (warp == kMmaWarpStem) {
     tc_fence_after();
-    tmem_dealloc<(2 * BN <= 128 ? 128 : 256)>(tmem_base);
+    tmem_dealloc<kTmemCols>(tmem_base);
   }
 }
 

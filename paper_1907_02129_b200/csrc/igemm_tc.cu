@@ -29,7 +29,7 @@
 
 namespace icv {
 
-#ifdef ICV_TRACE
+#if defined(ICV_TRACE) || defined(ICV_STEM_PHASES)
 __device__ unsigned long long g_icv_trace[1024][128];
 #endif
 
@@ -707,7 +707,7 @@ const char* tc_kernel_name(const ConvArgs& c) {
 
 }  // namespace icv
 
-#ifdef ICV_TRACE
+#if defined(ICV_TRACE) || defined(ICV_STEM_PHASES)
 extern "C" ICV_API int icv_debug_trace(unsigned long long* host, int reset) {
   if (host && cudaMemcpyFromSymbol(host, icv::g_icv_trace, sizeof(icv::g_icv_trace)) != cudaSuccess)
     return ICV_ERR_CUDA;
