@@ -60,6 +60,12 @@ typedef enum icv_dtype {
  * reference representation to the implementation). */
 #define ICV_IB_PER_IMAGE 0x100
 
+/* Flag OR-ed into icv_conv's `ib_dtype`: the buffer is exactly what
+ * icv_ib_build produced for this geometry (icv_ib_check can verify it).  It
+ * lets channel-poor stride-2 layers consume the buffer at input-row
+ * granularity (row-sliding kernel); without it they gather tap by tap. */
+#define ICV_IB_CANONICAL 0x200
+
 /* Convolution geometry; field-for-field convbench.tensors.ConvParams
  * (tensors.py:41-72). */
 typedef struct icv_conv_desc {
@@ -122,6 +128,12 @@ ICV_API int icv_ib_build(const icv_conv_desc* desc, const icv_shape4* in, int64_
 /* ---- filter packing (K7) ---------------------------------------------- */
 /* Bytes of device storage icv_pack_filter writes for `compute_dtype`
  * (weights + per-channel epilogue constants). */
+/* Count the entries of `ib` (layout flags as for icv_ib_build) that differ
+ * from the canonical buffer of this geometry; the count is written to the
+ * DEVICE int32 `mismatches` (stream-ordered, no synchronization). */
+ICV_API int icv_ib_check(const icv_conv_desc* desc, const icv_shape4* in, int64_t batch, int32_t mr, int32_t ib_dtype,
+                         const void* ib, int32_t* mismatches, void* stream);
+
 ICV_API int icv_packed_filter_bytes(const icv_conv_desc* desc, int32_t compute_dtype, int64_t* bytes);
 
 /* Repack KRSC weights (`w_dtype` ICV_F32 / ICV_BF16 / ICV_U8) into the

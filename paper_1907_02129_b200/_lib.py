@@ -22,6 +22,7 @@ LIB_PATH = os.environ.get("ICV_LIB") or os.path.join(os.path.dirname(os.path.abs
 ICV_OK, ICV_ERR_ARG, ICV_ERR_GEOMETRY, ICV_ERR_STALE, ICV_ERR_UNSUPPORTED, ICV_ERR_CUDA = 0, -1, -2, -3, -4, -5
 ICV_F32, ICV_BF16, ICV_U8, ICV_I32, ICV_I64 = 0, 1, 2, 3, 4
 ICV_IB_PER_IMAGE = 0x100
+ICV_IB_CANONICAL = 0x200   # buffer is exactly icv_ib_build's output (row-sliding kernels may use it)
 
 TORCH_TO_ICV = {torch.float32: ICV_F32, torch.bfloat16: ICV_BF16, torch.uint8: ICV_U8,
                 torch.int32: ICV_I32, torch.int64: ICV_I64}
@@ -55,6 +56,7 @@ SIGNATURES = {
     "icv_ib_entries": (ctypes.c_int, [ctypes.POINTER(Desc), ctypes.POINTER(Shape), _I64, _I32,
                                       ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
     "icv_ib_build": (ctypes.c_int, [ctypes.POINTER(Desc), ctypes.POINTER(Shape), _I64, _I32, _I64, _I32, _P, _P]),
+    "icv_ib_check": (ctypes.c_int, [ctypes.POINTER(Desc), ctypes.POINTER(Shape), _I64, _I32, _I32, _P, _P, _P]),
     "icv_packed_filter_bytes": (ctypes.c_int, [ctypes.POINTER(Desc), _I32, ctypes.POINTER(_I64)]),
     "icv_pack_filter": (ctypes.c_int, [ctypes.POINTER(Desc), _I32, _I32, _P, _P, ctypes.POINTER(Quant), _P, _P]),
     "icv_requant_params": (ctypes.c_int, [_F32, _F32, _F32, ctypes.POINTER(_I32), ctypes.POINTER(_I32)]),

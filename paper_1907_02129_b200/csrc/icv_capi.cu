@@ -106,6 +106,11 @@ int packed_layout(const icv_conv_desc* d, int32_t dtype, PackedLayout* L) {
     L->w_bytes = (int64_t)L->n_pad * L->row_bytes;
     L->bias_off = align_up(L->w_bytes, 256);
     L->bias_bytes = 4 * (int64_t)L->n_pad;
+    // plus, for stride-2 layers, the row-sliding kernel's copy: per kernel row
+    // a [n_pad][32] (kx < 8, c < 4) no-swizzle K-major block
+    if (rows_filter_eligible(d->kernel_h, d->kernel_w, d->stride_h, d->stride_w, d->dilation_h, d->dilation_w,
+                             (int)C, (int)K))
+      L->rows_off = align_up(L->bias_off + L->bias_bytes, 1024);
   } else {
     const int eb = fam == kFamF32Exact ? 4 : (fam == kFamCoreBf16 ? 2 : 1);
     L->n_pad = (int)K;
@@ -116,6 +121,7 @@ int packed_layout(const icv_conv_desc* d, int32_t dtype, PackedLayout* L) {
     L->bias_bytes = 4 * K;
   }
   L->total = align_up(L->bias_off + L->bias_bytes, 256);
+  if (L->rows_off) L->total = align_up(L->rows_off + (int64_t)d->kernel_h * L->n_pad * 64, 256);
   return ICV_OK;
 }
 
@@ -192,6 +198,19 @@ ICV_API int icv_ib_build(const icv_conv_desc* desc, const icv_shape4* in, int64_
   return launch_ib_build(g, batch, mr, first_tile, ib_dtype, ib, (cudaStream_t)stream);
 }
 
+ICV_API int icv_ib_check(const icv_conv_desc* desc, const icv_shape4* in, int64_t batch, int32_t mr, int32_t ib_dtype,
+                         const void* ib, int32_t* mismatches, void* stream) {
+  Geom g;
+  if (int s = make_geom(desc, in, &g)) return s;
+  if (mr < 1) return fail(ICV_ERR_ARG, "mr must be >= 1");
+  if (batch < 1 || batch > in->n) return fail(ICV_ERR_ARG, "batch must be within the physical input batch");
+  const bool per_image = (ib_dtype & ICV_IB_PER_IMAGE) != 0;
+  ib_dtype &= ~(ICV_IB_PER_IMAGE | ICV_IB_CANONICAL);
+  if (ib_dtype != ICV_I64 && ib_dtype != ICV_I32) return fail(ICV_ERR_ARG, "ib dtype must be int64 or int32");
+  if (!ib || !mismatches) return fail(ICV_ERR_ARG, "icv_ib_check: null pointer");
+  return launch_ib_check(g, per_image ? 1 : batch, mr, ib_dtype, ib, mismatches, (cudaStream_t)stream);
+}
+
 ICV_API int icv_packed_filter_bytes(const icv_conv_desc* desc, int32_t compute_dtype, int64_t* bytes) {
   PackedLayout L;
   if (int s = packed_layout(desc, compute_dtype, &L)) return s;
@@ -245,7 +264,8 @@ static const char* kernel_name_for(const ConvArgs& a) {
     case kFamCoreU8: return "icv_conv_core<u8>";
     case kFamTcBf16:
     case kFamTcU8: return tc_kernel_name(a);
-    case kFamStemBf16: return "icv_igemm_stem<bf16>";
+    case kFamStemBf16:
+      return (a.L.rows_off && rows_kernel_eligible(a.g)) ? "icv_igemm_rows<bf16>" : "icv_igemm_stem<bf16>";
   }
   return "?";
 }
@@ -267,7 +287,8 @@ ICV_API int icv_conv(const icv_conv_desc* desc, const icv_shape4* in, int64_t ba
   if (batch < 1 || batch > in->n) return fail(ICV_ERR_ARG, "batch must be within the physical input batch");
   if (mr < 1) return fail(ICV_ERR_ARG, "mr must be >= 1");
   a.ib_per_image = (ib_dtype & ICV_IB_PER_IMAGE) != 0;
-  ib_dtype &= ~ICV_IB_PER_IMAGE;
+  a.ib_canonical = (ib_dtype & ICV_IB_CANONICAL) != 0;
+  ib_dtype &= ~(ICV_IB_PER_IMAGE | ICV_IB_CANONICAL);
   if (ib_dtype != ICV_I64 && ib_dtype != ICV_I32) return fail(ICV_ERR_ARG, "ib dtype must be int64 or int32");
   if (!x || !zero_row || !ib || !packed || !y) return fail(ICV_ERR_ARG, "null tensor pointer");
   if (int s = packed_layout(desc, dtype, &a.L)) return s;

@@ -42,11 +42,14 @@ struct PackedLayout {
   int cblocks;        // 128-byte channel blocks per tap (tensor-core families)
   int64_t row_bytes;  // bytes per packed output channel row
   int64_t w_off, w_bytes, bias_off, bias_bytes, total;
+  int64_t rows_off;   // channel-poor family: row-sliding filter copy (0 = absent)
 };
 int packed_layout(const icv_conv_desc* d, int32_t dtype, PackedLayout* L);
 
 // ---- kernels (launchers) ---------------------------------------------------
 int launch_ib_build(const Geom& g, int64_t batch, int32_t mr, int64_t first_tile, int32_t ib_dtype, void* ib,
+                    cudaStream_t st);
+int launch_ib_check(const Geom& g, int64_t batch, int32_t mr, int32_t ib_dtype, const void* ib, int32_t* mismatches,
                     cudaStream_t st);
 int launch_pack(const Geom& g, const PackedLayout& L, int32_t w_dtype, const void* w, const void* bias,
                 const icv_quant* q, void* packed, cudaStream_t st);
@@ -60,6 +63,7 @@ struct ConvArgs {
   const void* ib;
   int32_t ib_is_i32;
   int32_t ib_per_image;  // entries are image-relative (ICV_IB_PER_IMAGE)
+  int32_t ib_canonical;  // caller guarantees the icv_ib_build layout (ICV_IB_CANONICAL)
   const uint8_t* packed;
   PackedLayout L;
   void* y;
@@ -71,5 +75,8 @@ int launch_conv_core(const ConvArgs& a, cudaStream_t st);       // bf16 / u8, an
 int launch_conv_tc(const ConvArgs& a, cudaStream_t st);         // bf16 / u8 tcgen05
 const char* tc_kernel_name(const ConvArgs& a);
 int launch_conv_stem(const ConvArgs& a, cudaStream_t st);   // channel-poor bf16 (tcgen05)
+bool rows_kernel_eligible(const Geom& g);
+bool rows_filter_eligible(int R, int S, int SY, int SX, int DY, int DX, int C, int K);
+int launch_conv_rows(const ConvArgs& a, cudaStream_t st);   // channel-poor, stride 2, row-sliding A
 
 }  // namespace icv

@@ -21,7 +21,7 @@ constexpr int kBM = 128;                // output pixels per tile (TMEM lanes / 
 constexpr int kABytes = kBM * 128;      // one 128-byte K block of the A tile
 constexpr int kMaxBias = 2048;          // output channels whose epilogue constants live in smem
 
-#if defined(ICV_STEM_PHASES) && !defined(ICV_TRACE)
+#if (defined(ICV_STEM_PHASES) || defined(ICV_ROWS_PHASES) || defined(ICV_ROWS_TIMELINE)) && !defined(ICV_TRACE)
 extern __device__ unsigned long long g_icv_trace[1024][128];
 #define TRACE(slot)
 #elif defined(ICV_TRACE)
@@ -57,6 +57,8 @@ struct TcArgs {
   int32_t use_tma_x;         // input tensor map valid (TMA gathers allowed)
   int32_t ib_per_image;      // buffer holds image 0's (image-relative) references
   int32_t use_tma_y;         // output tensor map valid: epilogue stores tiles with TMA
+  int32_t tiles_per_row;     // row-tiled kernels: tile = (output row, 128-pixel block); 3-D output map
+  int32_t ow;                // row-tiled kernels: output row width (pixels >= ow are not stored)
   int64_t ohw, img_elems;    // Ho*Wo, H*W*C
 };
 
@@ -114,6 +116,12 @@ __device__ __forceinline__ void store_partial(uint8_t* dst, uint4 val, int n) {
   }
 }
 
+#ifdef ICV_ROWS_PHASES   // debug: epilogue phase cycle accumulators (warp 0, lane 0) -> g_icv_trace[cta][42..47]
+#define EP_ACC(i) do { const long long _n = clock64(); _ep[i] += _n - _et; _et = _n; } while (0)
+#else
+#define EP_ACC(i)
+#endif
+
 // Tile schedule: local tile k of this CTA is tile_of(k), k < n_local
 // (default: tiles blockIdx.x, blockIdx.x + gridDim.x, ...).
 struct StridedTiles {
@@ -130,7 +138,8 @@ struct StridedTiles {
 template <bool kI8>
 constexpr int kEpiWarpBytes = kI8 ? 2048 : 4096;
 
-template <bool kI8, int BN, int kEpiWarps, int kAccStride, typename Sched = StridedTiles, int kAccStages = 2>
+template <bool kI8, int BN, int kEpiWarps, int kAccStride, typename Sched = StridedTiles, int kAccStages = 2,
+          bool kRowTiles = false>
 __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane, uint32_t tmem_base, uint8_t* sEpi,
                                               const uint32_t* sBias, uint64_t* tfull, uint64_t* tempty,
                                               Sched sched = Sched{0}, const CUtensorMap* tmap_y = nullptr) {
@@ -151,12 +160,17 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
 #ifdef ICV_TRACE
   long long t_prev = clock64(), t_wait = 0, t_work = 0;
 #endif
+#ifdef ICV_ROWS_PHASES
+  long long _et = clock64(), _ep[6] = {0, 0, 0, 0, 0, 0};
+#endif
   for (int64_t ti = 0; ti < n_local; ++ti) {
     const int64_t tile = sched(ti);
     const int64_t mt = tile / a.n_tiles;
     const int nt = (int)(tile - mt * a.n_tiles);
+    EP_ACC(5);
     mbar_wait(&tfull[as], aphase);
     tc_fence_after();
+    EP_ACC(0);
 #ifdef ICV_TRACE
     {   // slot 28: cycles waiting for accumulators, 29: cycles working (warp 0, lane 0)
       const long long t = clock64();
@@ -166,7 +180,14 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
 #endif
     const int ti_ = (int)ti;
     if (ew == 0 && lane == 0 && ti_ < 8) TRACE(10 + ti_);
-    const int64_t row0 = mt * kBM + slot * 32;  // first pixel of this warp's rows
+    // first pixel of this warp's rows; row-tiled: (output row, first pixel of the block)
+    int64_t row0 = mt * kBM + slot * 32;
+    int32_t rt_row = 0, rt_ox0 = 0;
+    if constexpr (kRowTiles) {
+      rt_row = (int32_t)((uint32_t)mt / (uint32_t)a.tiles_per_row);
+      rt_ox0 = ((int32_t)mt - rt_row * a.tiles_per_row) * kBM + slot * 32;
+      row0 = (int64_t)rt_row * a.ow + rt_ox0;
+    }
     const uint32_t taddr = tmem_base + ((uint32_t)(slot * 32) << 16) + as * kAccStride;
     int32_t rowsum = 0;
     if constexpr (kI8) {
@@ -187,6 +208,7 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
       tmem_ld_32x32b_x32(taddr + col0, v);
       tmem_ld_wait_regs(v);
     }
+    EP_ACC(1);
 #pragma unroll 1
     for (int ci = 0; ci < nchunks; ++ci) {
       const int c = col0 + ci * 32;
@@ -222,6 +244,7 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
           w[q] = word;
         }
       }
+      EP_ACC(2);
       if (use_tma) {
         // stage the 32 x 32 block as the TMA box (bf16: 64-byte rows with the
         // 64-byte swizzle, conflict-free row-per-lane writes; u8: dense
@@ -240,11 +263,16 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
         }
         fence_proxy_async_smem();
         __syncwarp();
+        EP_ACC(3);
         if (lane == 0) {
-          tma_store_2d(tmap_y, sb, n, (int32_t)row0);
+          if constexpr (kRowTiles)   // (channel, pixel in the output row, output row); pixels >= Wo clipped
+            tma_store_3d(tmap_y, sb, n, rt_ox0, rt_row);
+          else
+            tma_store_2d(tmap_y, sb, n, (int32_t)row0);
           bulk_commit_group();
         }
         ++chunk_seq;
+        EP_ACC(4);
         if (ci + 1 < nchunks) {
           tmem_ld_wait_regs(vn);
 #pragma unroll
@@ -264,7 +292,7 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
         const int rr = pass * kRowsPerPass + lane / kChunks;
         const int q = lane % kChunks;
         const int64_t p = row0 + rr;
-        if (p < a.P) {
+        if (kRowTiles ? rt_ox0 + rr < a.ow : p < a.P) {
           const uint4 val = *reinterpret_cast<const uint4*>(stg + rr * kStageRowBytes + q * 16);
           const int col = n + q * (16 / eb);
           uint8_t* dst = static_cast<uint8_t*>(a.y) + (p * a.K + col) * eb;
@@ -281,6 +309,9 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
     }
     tc_fence_before();
     mbar_arrive(&tempty[as]);
+#ifdef ICV_ROWS_TIMELINE
+    if (ew == 0 && lane == 0 && ti < 24) g_icv_trace[blockIdx.x][80 + ti] = ({ unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); t_; });
+#endif
 #ifdef ICV_TRACE
     {
       const long long t = clock64();
@@ -292,6 +323,10 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
     if (++as == kAccStages) { as = 0; aphase ^= 1; }
   }
   if (use_tma && lane == 0) bulk_wait_group<0>();   // output written before the CTA exits
+#ifdef ICV_ROWS_PHASES
+  if (ew == 0 && lane == 0)
+    for (int i = 0; i < 6; ++i) g_icv_trace[blockIdx.x][42 + i] = (unsigned long long)_ep[i];
+#endif
 #ifdef ICV_TRACE
   if (ew == 0 && lane == 0) {
     g_icv_trace[blockIdx.x][28] = (unsigned long long)t_wait;

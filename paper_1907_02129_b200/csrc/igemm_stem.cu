@@ -148,11 +148,6 @@ __device__ __forceinline__ uint2 lds64(uint32_t addr) {
   asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
   return v;
 }
-__device__ __forceinline__ uint4 lds128(uint32_t addr) {
-  uint4 v;
-  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
-  return v;
-}
 
 // element j (0 .. 2*N-1) of a little-endian array of N packed bf16 pairs
 template <int N>
@@ -582,6 +577,8 @@ bool stem_kernel_eligible(int C, int RS, int K) {
 }
 
 int launch_conv_stem(const ConvArgs& c, cudaStream_t st) {
+  // stride-2 layers with a canonical buffer: the row-sliding kernel (igemm_rows.cu)
+  if (c.ib_canonical && c.L.rows_off && rows_kernel_eligible(c.g)) return launch_conv_rows(c, st);
   if (c.ib_is_i32) return dispatch_stem<int32_t>(c, st);
   return dispatch_stem<int64_t>(c, st);
 }

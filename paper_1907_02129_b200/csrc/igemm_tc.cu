@@ -29,7 +29,7 @@
 
 namespace icv {
 
-#if defined(ICV_TRACE) || defined(ICV_STEM_PHASES)
+#if defined(ICV_TRACE) || defined(ICV_STEM_PHASES) || defined(ICV_ROWS_PHASES) || defined(ICV_ROWS_TIMELINE)
 __device__ unsigned long long g_icv_trace[1024][128];
 #endif
 
@@ -643,6 +643,8 @@ int make_input_tmap(const ConvArgs& c, CUtensorMap* tmap) {
 void fill_tc_args(const ConvArgs& c, int block_n, TcArgs* a) {
   const bool i8 = c.L.family == kFamTcU8;
   a->use_tma_y = 0;
+  a->tiles_per_row = 1;
+  a->ow = 0;
   a->x = static_cast<const uint8_t*>(c.x);
   a->zero_row = static_cast<const uint8_t*>(c.zero_row);
   a->ib = c.ib;
@@ -707,7 +709,7 @@ const char* tc_kernel_name(const ConvArgs& c) {
 
 }  // namespace icv
 
-#if defined(ICV_TRACE) || defined(ICV_STEM_PHASES)
+#if defined(ICV_TRACE) || defined(ICV_STEM_PHASES) || defined(ICV_ROWS_PHASES) || defined(ICV_ROWS_TIMELINE)
 extern "C" ICV_API int icv_debug_trace(unsigned long long* host, int reset) {
   if (host && cudaMemcpyFromSymbol(host, icv::g_icv_trace, sizeof(icv::g_icv_trace)) != cudaSuccess)
     return ICV_ERR_CUDA;

@@ -62,6 +62,25 @@ __global__ void pack_kpacked_bf16(const Tin* __restrict__ w, __nv_bfloat16* __re
   }
 }
 
+// row-sliding layout (igemm_rows.cu): per kernel row ky a [n_pad][32] K-major
+// no-swizzle block, k = kx*4 + c (kx < 8, c < 4), core matrices of 8 rows x
+// 8 elements: byte ((n/8)*4 + k/8)*128 + (n%8)*16 + (k%8)*2.
+template <typename Tin>
+__global__ void pack_rows_bf16(const Tin* __restrict__ w, uint8_t* __restrict__ out, int K, int R, int S, int C,
+                               int n_pad, int64_t total) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(i % 32);
+    const int64_t nk = i / 32;
+    const int n = (int)(nk % n_pad);
+    const int ky = (int)(nk / n_pad);
+    const int kx = k / 4, c = k % 4;
+    float v = 0.f;
+    if (n < K && kx < S && c < C) v = to_f32<Tin>(w[(((int64_t)n * R + ky) * S + kx) * C + c]);
+    const int64_t off = (int64_t)ky * n_pad * 64 + ((n / 8) * 4 + k / 8) * 128 + (n % 8) * 16 + (k % 8) * 2;
+    *reinterpret_cast<__nv_bfloat16*>(out + off) = __float2bfloat16_rn(v);
+  }
+}
+
 template <typename Tin, typename Tout>
 __global__ void pack_copy(const Tin* __restrict__ w, Tout* __restrict__ out, int64_t total) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -142,6 +161,17 @@ int launch_pack(const Geom& g, const PackedLayout& L, int32_t w_dtype, const voi
       pack_bias_f32<<<grid_for(L.n_pad), 256, 0, st>>>(static_cast<const float*>(bias),
                                                          reinterpret_cast<float*>(base + L.bias_off), g.K, L.n_pad);
       launches = 2;
+      if (L.rows_off) {
+        const int64_t rtotal = (int64_t)g.R * L.n_pad * 32;
+        if (w_dtype == ICV_F32)
+          pack_rows_bf16<float><<<grid_for(rtotal), 256, 0, st>>>(static_cast<const float*>(w), base + L.rows_off, g.K,
+                                                                  g.R, g.S, g.C, L.n_pad, rtotal);
+        else
+          pack_rows_bf16<__nv_bfloat16><<<grid_for(rtotal), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(w),
+                                                                          base + L.rows_off, g.K, g.R, g.S, g.C,
+                                                                          L.n_pad, rtotal);
+        ++launches;
+      }
       break;
     }
     case kFamTcU8: {

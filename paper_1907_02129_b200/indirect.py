@@ -65,6 +65,10 @@ class IndirectionBuffer:
     zero_row: torch.Tensor
     offsets: torch.Tensor      # (tiles, R*S, mr) int64 (or int32), device resident
     per_image: bool = False    # offsets cover image 0 only (image-relative form)
+    # offsets are exactly what icv_ib_build produced (always true for buffers
+    # made by this module; an initialized buffer is immutable).
+    # Lets channel-poor stride-2 layers read it at input-row granularity.
+    canonical: bool = True
 
     @property
     def pixel_count(self) -> int:
@@ -99,6 +103,21 @@ class IndirectionBuffer:
         step = self.in_shape.h * self.in_shape.w * self.in_shape.c
         rows = np.where(rows < 0, rows, rows + (n * step)[:, None])
         return rows.reshape(self.tile_count, mr, rs).transpose(0, 2, 1).copy()
+
+    def verify(self) -> int:
+        """Entries differing from the canonical buffer of this geometry
+        (device check, icv_ib_check); a nonzero count clears `canonical` so
+        the kernels gather tap by tap from whatever the buffer holds."""
+        d, s = L.desc_of(self.params), L.shape_of(self.in_shape)
+        fmt = L.TORCH_TO_ICV[self.offsets.dtype] | (L.ICV_IB_PER_IMAGE if self.per_image else 0)
+        dev = self.offsets.device
+        out = torch.zeros(1, dtype=torch.int32, device=dev)
+        with torch.cuda.device(dev):
+            L.check(L.lib().icv_ib_check(ctypes.byref(d), ctypes.byref(s), self.batch, self.mr, fmt,
+                                         L.ptr(self.offsets), L.ptr(out), L.stream_of(dev)), "icv_ib_check")
+        bad = int(out.item())
+        self.canonical = bad == 0
+        return bad
 
     def rows_for_tile(self, t: int) -> list[torch.Tensor]:
         """Dereference tile t: R*S*mr pixel-row views in kernel-element order,
@@ -246,7 +265,8 @@ def indirect_conv(input: NhwcTensor, pf: PackedFilter, ib: IndirectionBuffer, pa
     with torch.cuda.device(dev):
         L.check(L.lib().icv_conv(ctypes.byref(d), ctypes.byref(s), batch, L.TORCH_TO_ICV[input.dtype],
                                  L.ptr(input.data), L.ptr(ib.zero_row), L.ptr(ib.offsets),
-                                 L.TORCH_TO_ICV[ib.offsets.dtype] | (L.ICV_IB_PER_IMAGE if ib.per_image else 0),
+                                 L.TORCH_TO_ICV[ib.offsets.dtype] | (L.ICV_IB_PER_IMAGE if ib.per_image else 0)
+                                 | (L.ICV_IB_CANONICAL if ib.canonical else 0),
                                  ib.mr, L.ptr(pf.packed),
                                  ctypes.byref(q) if q is not None else None, L.ptr(out.data), L.stream_of(dev)),
                 "icv_conv")

@@ -125,7 +125,7 @@ def test_packed_filter_bytes_and_kernel_selection():
     assert L.kernel_name(CFG2.params, CFG2.in_shape, torch.bfloat16).startswith("icv_igemm_")
     assert L.kernel_name(CFG3B.params, CFG3B.in_shape, torch.bfloat16).startswith("icv_igemm_")
     assert L.kernel_name(CFG4.params, CFG4.in_shape, torch.uint8).startswith("icv_igemm_")
-    assert L.kernel_name(CFG3A.params, CFG3A.in_shape, torch.bfloat16) == "icv_igemm_stem<bf16>"   # C=3 stem
+    assert L.kernel_name(CFG3A.params, CFG3A.in_shape, torch.bfloat16) == "icv_igemm_rows<bf16>"   # C=3 stem
 
 
 def test_null_and_range_arguments_are_rejected():

@@ -449,9 +449,80 @@ def test_stem_per_image_schedules(geom, index_dtype):
     pf = icv.pack_filter(filt, torch.from_numpy(bias), p, tile, compute_dtype=torch.bfloat16)
     zero = icv.make_zero_row(p.in_channels, dtype=torch.bfloat16, device=DEV)
     out_shape = icv.conv_output_shape(p, shape)
-    assert L.kernel_name(p, shape, torch.bfloat16) == "icv_igemm_stem<bf16>"
+    assert L.kernel_name(p, shape, torch.bfloat16) in ("icv_igemm_stem<bf16>", "icv_igemm_rows<bf16>")
     ib = icv.init_indirection_buffer(x, zero, p, out_shape, tile, index_dtype=index_dtype, per_image=True)
     y = icv.indirect_conv(x, pf, ib, p, tile).numpy().reshape(-1, p.out_channels)
     ref = oconv.indirect_conv_f32(oconv.bf16_round(xh), np.zeros(shape.c, np.float32), ib.offsets_host(), p,
                                   oconv.bf16_round(wh), bias, n, out_shape.h, out_shape.w)
     assert_bf16_close(y, ref)
+
+
+
+# ----------------------------------------------- row-sliding stem kernel (K4b)
+def _stem_problem(g, index_dtype=torch.int64, per_image=True, seed=13):
+    g = dict(g)
+    n, h, wd = g.pop("n"), g.pop("h"), g.pop("w")
+    p = make_params(**g)
+    shape = icv.Shape4(n, h, wd, p.in_channels)
+    rng = np.random.default_rng(seed)
+    xh = rng.standard_normal(shape.numel, dtype=np.float32)
+    wh = rng.standard_normal(p.out_channels * p.kernel_elems * p.in_channels, dtype=np.float32)
+    bias = rng.standard_normal(p.out_channels, dtype=np.float32)
+    tile = icv.TileConfig(mr=128)
+    x = icv.NhwcTensor(shape, torch.from_numpy(xh).to(DEV).to(torch.bfloat16))
+    filt = icv.FilterTensor(p.out_channels, p.kernel_h, p.kernel_w, p.in_channels, torch.from_numpy(wh).to(DEV))
+    pf = icv.pack_filter(filt, torch.from_numpy(bias), p, tile, compute_dtype=torch.bfloat16)
+    zero = icv.make_zero_row(p.in_channels, dtype=torch.bfloat16, device=DEV)
+    out_shape = icv.conv_output_shape(p, shape)
+    ib = icv.init_indirection_buffer(x, zero, p, out_shape, tile, index_dtype=index_dtype, per_image=per_image)
+    return p, shape, xh, wh, bias, x, pf, ib, tile, out_shape
+
+
+@pytest.mark.parametrize("geom", [
+    dict(r=7, s=7, sy=2, sx=2, pt=3, pl=3, c=3, k=64, n=3, h=96, w=88),     # one tile per output row
+    dict(r=7, s=7, sy=2, sx=2, pt=3, pl=3, c=3, k=64, n=2, h=70, w=320),    # two tiles per row (Wo = 160)
+    dict(r=7, s=7, sy=2, sx=2, pt=3, pl=3, c=3, k=40, n=2, h=65, w=64),     # K < 64, odd H
+    dict(r=7, s=7, sy=2, sx=2, pt=3, pl=3, c=3, k=128, n=1, h=64, w=96),    # 128-wide filter
+    dict(r=3, s=3, sy=2, sx=2, pt=1, pl=1, c=3, k=64, n=2, h=80, w=72),     # 3x3/2 (one K step)
+    dict(r=7, s=7, sy=2, sx=2, pt=2, pl=4, pb=4, pr=1, c=3, k=64, n=2, h=70, w=80),   # asymmetric padding
+])
+@pytest.mark.parametrize("per_image,index_dtype", [(True, torch.int64), (False, torch.int64), (True, torch.int32)])
+def test_rows_kernel_matches_oracle(geom, per_image, index_dtype):
+    p, shape, xh, wh, bias, x, pf, ib, tile, o = _stem_problem(geom, index_dtype, per_image)
+    assert L.kernel_name(p, shape, torch.bfloat16) == "icv_igemm_rows<bf16>"
+    y = icv.indirect_conv(x, pf, ib, p, tile).numpy().reshape(-1, p.out_channels)
+    pixels = o.n * o.h * o.w
+    idx = np.unique(np.concatenate([np.arange(min(pixels, 2 * o.w)), np.arange(max(0, pixels - 2 * o.w), pixels),
+                                    np.random.default_rng(1).integers(0, pixels, 2048)]))
+    ref = oconv.indirect_conv_f32(oconv.bf16_round(xh), np.zeros(shape.c, np.float32), ib.offsets_host(), p,
+                                  oconv.bf16_round(wh), bias, o.n, o.h, o.w, pixel_index=idx)
+    assert_bf16_close(y[idx], ref)
+
+
+def test_rows_kernel_equals_tap_gather_and_respects_noncanonical_buffers():
+    """The row-sliding kernel gives the tap-by-tap gather kernel's answer; a
+    buffer that differs from the canonical one is detected by icv_ib_check
+    and then read entry by entry (the kernel follows the buffer)."""
+    g = dict(r=7, s=7, sy=2, sx=2, pt=3, pl=3, c=3, k=64, n=2, h=64, w=64)
+    p, shape, xh, wh, bias, x, pf, ib, tile, o = _stem_problem(g)
+    assert ib.verify() == 0 and ib.canonical
+    y_rows = icv.indirect_conv(x, pf, ib, p, tile).numpy()
+    ib.canonical = False
+    y_gather = icv.indirect_conv(x, pf, ib, p, tile).numpy()
+    assert_bf16_close(y_rows, y_gather)    # same sums, different fp32 accumulation order
+    # redirect one tap of pixel 5 to another input row: the gather path follows it
+    ib.offsets[0, 24, 5] = ib.offsets[0, 24, 9]
+    assert ib.verify() > 0 and not ib.canonical
+    y = icv.indirect_conv(x, pf, ib, p, tile).numpy().reshape(-1, p.out_channels)
+    ref = oconv.indirect_conv_f32(oconv.bf16_round(xh), np.zeros(shape.c, np.float32), ib.offsets_host(), p,
+                                  oconv.bf16_round(wh), bias, o.n, o.h, o.w, pixel_index=np.arange(16))
+    assert_bf16_close(y[:16], ref)
+
+
+@pytest.mark.parametrize("index_dtype", [torch.int64, torch.int32])
+@pytest.mark.parametrize("per_image", [False, True])
+def test_ib_check_accepts_built_buffers(index_dtype, per_image):
+    for g in (dict(r=3, s=3, pt=1, pl=1, c=8, k=8, n=3, h=9, w=7), dict(r=7, s=7, sy=2, sx=2, pt=3, pl=3, c=3, k=64,
+                                                                        n=2, h=40, w=48)):
+        p, shape, xh, wh, bias, x, pf, ib, tile, o = _stem_problem(g, index_dtype, per_image)
+        assert ib.verify() == 0

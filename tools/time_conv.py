@@ -21,13 +21,16 @@ def main():
     for name in names:
         w, x, xh, pf, ib, y, tile = bench.setup_problem(name, 0, CONFIGS[name].in_shape.n, dev,
                                                         per_image=os.environ.get("ICV_IB", "per-image") == "per-image")
+        if os.environ.get("ICV_NONCANONICAL"):
+            ib.canonical = False
         t = bench.time_steps(lambda: icv.indirect_conv(x, pf, ib, w.params, tile, out=y), 50, 5,
                              lambda: flush.fill_(1))
         ms = statistics.median(t)
         ok = ""
         if w.dtype == "bf16" and not os.environ.get("ICV_NO_GATE"):
             ok = bench.correctness_gate(w, xh, pf, ib, y)["normwise_rel_err"]
-        print(f"{name:6s} {ms * 1e3:8.2f} us  {w.flops / ms / 1e9:8.1f} TFLOP/s  gate={ok}")
+        kname = icv._lib.kernel_name(w.params, w.in_shape, x.dtype)
+        print(f"{name:6s} {ms * 1e3:8.2f} us  {w.flops / ms / 1e9:8.1f} TFLOP/s  gate={ok}  [{kname}]")
         del x, pf, ib, y
 
 
