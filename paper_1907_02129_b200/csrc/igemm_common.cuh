@@ -138,17 +138,21 @@ struct StridedTiles {
 template <bool kI8>
 constexpr int kEpiWarpBytes = kI8 ? 2048 : 4096;
 
+// kTileGroups > 1: the epilogue warps split into groups of 4 that take
+// alternate tiles (each warp all BN columns of its 32 rows), so several
+// tiles are in the epilogue at once; otherwise extra warps split columns.
 template <bool kI8, int BN, int kEpiWarps, int kAccStride, typename Sched = StridedTiles, int kAccStages = 2,
-          bool kRowTiles = false>
+          bool kRowTiles = false, int kTileGroups = 1>
 __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane, uint32_t tmem_base, uint8_t* sEpi,
                                               const uint32_t* sBias, uint64_t* tfull, uint64_t* tempty,
                                               Sched sched = Sched{0}, const CUtensorMap* tmap_y = nullptr) {
   constexpr int kOutRowBytes = kI8 ? 32 : 64;
   constexpr int kStageRowBytes = kI8 ? 48 : 80;  // padded: row-per-lane staging writes are conflict free
   const int slot = ew & 3;
-  constexpr int kColGroups = kEpiWarps / 4;
+  constexpr int kColGroups = kEpiWarps / 4 / kTileGroups;
   constexpr int kColsPerWarp = BN / kColGroups;
-  const int col0 = (ew / 4) * kColsPerWarp;
+  const int group = kTileGroups > 1 ? ew / 4 : 0;
+  const int col0 = kTileGroups > 1 ? 0 : (ew / 4) * kColsPerWarp;
   uint8_t* stg = sEpi + ew * kEpiWarpBytes<kI8>;
   const bool vec_ok = kI8 ? (a.K & 15) == 0 : (a.K & 7) == 0;
   const bool use_tma = tmap_y != nullptr;
@@ -163,10 +167,14 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
 #ifdef ICV_ROWS_PHASES
   long long _et = clock64(), _ep[6] = {0, 0, 0, 0, 0, 0};
 #endif
-  for (int64_t ti = 0; ti < n_local; ++ti) {
+  if constexpr (kTileGroups > 1) {   // this group's first tile
+    as = group % kAccStages;
+    aphase = (uint32_t)(group / kAccStages) & 1u;
+  }
+  for (int64_t ti = group; ti < n_local; ti += kTileGroups) {
     const int64_t tile = sched(ti);
-    const int64_t mt = tile / a.n_tiles;
-    const int nt = (int)(tile - mt * a.n_tiles);
+    const int64_t mt = a.n_tiles == 1 ? tile : tile / a.n_tiles;
+    const int nt = a.n_tiles == 1 ? 0 : (int)(tile - mt * a.n_tiles);
     EP_ACC(5);
     mbar_wait(&tfull[as], aphase);
     tc_fence_after();
@@ -308,7 +316,8 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
       }
     }
     tc_fence_before();
-    mbar_arrive(&tempty[as]);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&tempty[as]);   // one arrival per epilogue warp
 #ifdef ICV_ROWS_TIMELINE
     if (ew == 0 && lane == 0 && ti < 24) g_icv_trace[blockIdx.x][80 + ti] = ({ unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); t_; });
 #endif
@@ -320,7 +329,14 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
     }
 #endif
     if (ew == 0 && lane == 0 && ti_ < 8) TRACE(18 + ti_);
-    if (++as == kAccStages) { as = 0; aphase ^= 1; }
+    if constexpr (kTileGroups > 1) {
+      static_assert(kAccStages % kTileGroups == 0, "groups must map to fixed accumulator stages");
+      as += kTileGroups;
+      if (as >= kAccStages) { as -= kAccStages; aphase ^= 1; }
+    } else if (++as == kAccStages) {
+      as = 0;
+      aphase ^= 1;
+    }
   }
   if (use_tma && lane == 0) bulk_wait_group<0>();   // output written before the CTA exits
 #ifdef ICV_ROWS_PHASES

@@ -168,12 +168,12 @@ __global__ void __launch_bounds__(kThreadsR, 1) igemm_rows_kernel(const __grid_c
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStagesR; ++s) {
       mbar_init(&stage_full[s], 1);
-      mbar_init(&stage_free[s], kConvThreads);
+      mbar_init(&stage_free[s], kConvWarps);   // one arrival per converter warp
     }
-    for (int s = 0; s < 2; ++s) mbar_init(&rows_ready[s], kConvThreads);
+    for (int s = 0; s < 2; ++s) mbar_init(&rows_ready[s], kConvWarps);
     for (int s = 0; s < kAccR; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 32 * kEpiWarpsR);
+      mbar_init(&tempty[s], 4);   // one arrival per warp of the epilogue group that owns the tile
     }
     for (int s = 0; s < kMDone; ++s) mbar_init(&mdone[s], 1);
     mbar_init(bfull, 1);
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(kThreadsR, 1) igemm_rows_kernel(const __grid_c
       // image: anything may be) have completed
       const int64_t need = tr.fresh ? k - 1 : k - 2;
       RP_ACC(3);
-      if (need >= 0) mbar_wait(&mdone[need % kMDone], (uint32_t)(need / kMDone) & 1u);
+      if (need >= 0) mbar_wait(&tfull[need % kAccR], (uint32_t)(need / kAccR) & 1u);   // MMAs of tile `need` done
       RP_ACC(0);
       mbar_wait(&stage_full[s], (uint32_t)((k / kStagesR) & 1));
       RP_ACC(1);
@@ -276,9 +276,14 @@ __global__ void __launch_bounds__(kThreadsR, 1) igemm_rows_kernel(const __grid_c
                        "r"(e[2] | (e[3] << 16)) : "memory");
         }
       }
+#ifndef ICV_EXP_NOFENCE
       fence_proxy_async_smem();   // ring writes -> visible to the tensor core
-      mbar_arrive(&stage_free[s]);
-      mbar_arrive(&rows_ready[rs]);
+#endif
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&stage_free[s]);
+        mbar_arrive(&rows_ready[rs]);
+      }
       if (tid == 0) RTK(32, k);
       RP_ACC(2);
     }
@@ -330,8 +335,7 @@ __global__ void __launch_bounds__(kThreadsR, 1) igemm_rows_kernel(const __grid_c
 #ifdef ICV_ROWS_PHASES
         { const long long _n = clock64(); _ra[2] += _n - _rt; _rt = _n; }
 #endif
-        tc_commit(&mdone[k % kMDone]);
-        tc_commit(&tfull[as]);
+        tc_commit(&tfull[as]);   // accumulator ready (epilogue) and the tile's ring rows free (converters)
         RTK(56, k);
       }
       __syncwarp();
@@ -340,7 +344,7 @@ __global__ void __launch_bounds__(kThreadsR, 1) igemm_rows_kernel(const __grid_c
     }
     RP_FLUSH(38, lane == 0);
   } else {
-    epilogue_loop<false, BN, kEpiWarpsR, BN, RowTiles, kAccR, true>(a.t, warp - kConvWarps, lane, tmem_base, sEpi, sBias,
+    epilogue_loop<false, BN, kEpiWarpsR, BN, RowTiles, kAccR, true, kEpiWarpsR / 4>(a.t, warp - kConvWarps, lane, tmem_base, sEpi, sBias,
                                                                  tfull, tempty, sched,
                                                                  a.t.use_tma_y ? &tmap_y : nullptr);
   }

@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __gri
     }
     for (int s = 0; s < kAccStagesStem; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 32 * kEpiWarpsStem);
+      mbar_init(&tempty[s], kEpiWarpsStem);   // one arrival per epilogue warp
     }
     mbar_init(bfull, 1);
     for (int s = 0; s < 2; ++s) mbar_init(&winbar[s], 1);

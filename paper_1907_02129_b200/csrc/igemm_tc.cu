@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_c
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);                   // tcgen05.commit after the last K block
-      mbar_init(&tempty[s], 32 * kEpiWarpsS);    // every epilogue thread
+      mbar_init(&tempty[s], kEpiWarpsS);   // one arrival per epilogue warp
     }
     fence_mbar_init();
     tma_prefetch_desc(&tmap_b);

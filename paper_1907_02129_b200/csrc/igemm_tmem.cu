@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(kThreadsT, 1) igemm_tmem_kernel(const __grid_c
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 32 * kEpiWarpsT);
+      mbar_init(&tempty[s], kEpiWarpsT);   // one arrival per epilogue warp
     }
     fence_mbar_init();
     tma_prefetch_desc(&tmap_b);
