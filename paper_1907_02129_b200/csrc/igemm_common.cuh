@@ -145,7 +145,8 @@ template <bool kI8, int BN, int kEpiWarps, int kAccStride, typename Sched = Stri
           bool kRowTiles = false, int kTileGroups = 1>
 __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane, uint32_t tmem_base, uint8_t* sEpi,
                                               const uint32_t* sBias, uint64_t* tfull, uint64_t* tempty,
-                                              Sched sched = Sched{0}, const CUtensorMap* tmap_y = nullptr) {
+                                              Sched sched = Sched{0}, const CUtensorMap* tmap_y = nullptr,
+                                              uint32_t tempty_remote = 0) {
   constexpr int kOutRowBytes = kI8 ? 32 : 64;
   constexpr int kStageRowBytes = kI8 ? 48 : 80;  // padded: row-per-lane staging writes are conflict free
   const int slot = ew & 3;
@@ -317,7 +318,10 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
     }
     tc_fence_before();
     __syncwarp();
-    if (lane == 0) mbar_arrive(&tempty[as]);   // one arrival per epilogue warp
+    if (lane == 0) {   // one arrival per epilogue warp (at the pair leader for a pair peer)
+      if (tempty_remote) mbar_arrive_remote(tempty_remote + as * 8);
+      else mbar_arrive(&tempty[as]);
+    }
 #ifdef ICV_ROWS_TIMELINE
     if (ew == 0 && lane == 0 && ti < 24) g_icv_trace[blockIdx.x][80 + ti] = ({ unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); t_; });
 #endif

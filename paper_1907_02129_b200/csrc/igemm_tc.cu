@@ -39,9 +39,10 @@ constexpr int kEpiWarpsS = 4;
 constexpr int kMmaWarpS = 4 + kEpiWarpsS;
 constexpr int kThreadsS = 32 * (kMmaWarpS + 1);
 
-template <bool kI8, int BN>
+template <bool kI8, int BN, int kPair = 1>
 struct CfgS {
-  static constexpr int kBBytes = BN * 128;
+  // B bytes per K block held by this CTA (a CTA pair splits the BN rows)
+  static constexpr int kBBytes = BN * 128 / kPair;
   // One smem slot = one 128-byte K block of A (128 rows) and of B (BN rows).
   // A stage groups kKB slots behind one full/empty barrier pair so the MMA
   // warp pays one barrier round trip per kKB*4 MMAs.
@@ -67,9 +68,9 @@ struct PlanS {
   int off_b, off_ones, off_epi, off_bias, off_ib, off_bar, bytes;
 };
 
-template <bool kI8, int BN, typename IbT>
+template <bool kI8, int BN, typename IbT, int kPair = 1>
 bool plan_smem(int rs, int n_pad, PlanS* p) {
-  using C = CfgS<kI8, BN>;
+  using C = CfgS<kI8, BN, kPair>;
   const int bias = (n_pad * 4 + 15) / 16 * 16;
   const int ib = 2 * rs * kBM * 4 + 2 * kBM * 4;   // int32 index slices + per-row bases
   const int fixed = 1024 + C::kOnesBytes + C::kEpiBytes + bias + ib + C::kBarBytes;
@@ -117,8 +118,12 @@ __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_c
                                                                   const __grid_constant__ CUtensorMap tmap_x,
                                                                   const __grid_constant__ CUtensorMap tmap_y,
                                                                   const TcArgs a, const PlanS pl) {
-  using C = CfgS<kI8, BN>;
-  static_assert(kCS == 1 || C::kKB == kCS, "a cluster splits each stage's K blocks across its CTAs");
+  // kCS == 2: CTA pair -- the leader (rank 0) issues cta_group::2 MMAs with
+  // M = 256 (its 128 rows + the peer's 128 rows); each CTA gathers its own A
+  // rows and TMA-loads its half of the filter rows, so each SM receives half
+  // the filter bytes of the single-CTA kernel.
+  using C = CfgS<kI8, BN, kCS>;
+  static_assert(kCS == 1 || kCS == 2, "single CTA or CTA pair");
   constexpr uint16_t kMask = (uint16_t)((1u << kCS) - 1);
   const ClusterTiles<kCS> sched{a.total_tiles / a.n_tiles, a.n_tiles};
   const uint32_t crank = kCS > 1 ? cluster_ctarank() : 0;
@@ -159,12 +164,14 @@ __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_c
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       // TMA path: 1 expect_tx arrival; cp.async path: 128 producer arrivals + 1
-      mbar_init(&full[s], tma_gather ? 1 : 128 + 1);
-      mbar_init(&empty[s], kCS);     // tcgen05.commit of every CTA whose filter blocks land here
+      // cp.async path: 128 producer arrivals + 1 expect_tx (+ 1 forwarded from the peer, pair leader)
+      mbar_init(&full[s], tma_gather ? 1 : 128 + 1 + (kCS == 2 && crank == 0 ? 1 : 0));
+      mbar_init(&empty[s], 1);       // tcgen05.commit (multicast to both CTAs of a pair)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);                   // tcgen05.commit after the last K block
-      mbar_init(&tempty[s], kEpiWarpsS);   // one arrival per epilogue warp
+      // one arrival per epilogue warp (of both CTAs at the pair leader)
+      mbar_init(&tempty[s], (kCS == 2 && crank == 0) ? 2 * kEpiWarpsS : kEpiWarpsS);
     }
     fence_mbar_init();
     tma_prefetch_desc(&tmap_b);
@@ -178,9 +185,12 @@ __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_c
     }
   }
   for (int i = threadIdx.x; i < a.n_pad; i += blockDim.x) sBias[i] = __ldg(static_cast<const uint32_t*>(a.bias) + i);
-  if (warp == kMmaWarpS) tmem_alloc<C::kTmemCols>(tmem_slot);
+  if (warp == kMmaWarpS) {
+    if constexpr (kCS == 2) tmem_alloc2<C::kTmemCols>(tmem_slot);
+    else tmem_alloc<C::kTmemCols>(tmem_slot);
+  }
   tc_fence_before();
-  if constexpr (kCS > 1) cluster_sync_all();   // peers' barriers initialised before any multicast
+  if constexpr (kCS > 1) cluster_sync_all();   // peers' barriers initialised before any remote arrival
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
@@ -309,11 +319,9 @@ __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_c
                 // issued by the producer warps in turn
                 if (lane == 0 && warp == (stage_seq & 3)) {
                   mbar_arrive_expect_tx(&full[stage], C::kKB * C::kBBytes);
-                  if constexpr (kCS == 1)
-                    tma_load_3d(sB_u32 + stage * C::kKB * C::kBBytes, &tmap_b, &full[stage], 0, nt * BN, kb);
-                  else   // this CTA's K block of the stage, to every CTA of the cluster
-                    tma_load_3d_mc(sB_u32 + (stage * C::kKB + crank) * C::kBBytes, &tmap_b, &full[stage], 0,
-                                   nt * BN, kb + (int)crank, kMask);
+                  // (a pair member loads its half of the BN filter rows)
+                  tma_load_3d(sB_u32 + stage * C::kKB * C::kBBytes, &tmap_b, &full[stage], 0,
+                              nt * BN + (int)crank * (BN / kCS), kb);
                 }
                 ++stage_seq;
               }
@@ -360,10 +368,25 @@ __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_c
       g_icv_trace[blockIdx.x][38] = (unsigned long long)p_wait;
     }
 #endif
+  } else if (warp == kMmaWarpS && kCS == 2 && crank != 0) {
+    // ------------------------------------------------------------ pair peer: forwarder
+    // The leader's MMAs read this CTA's stages too: once a stage is full here
+    // (own gathers + own filter half), tell the leader's full barrier.
+    const int stages_per_tile = (num_kb + C::kKB - 1) / C::kKB;
+    const int64_t n_local = sched.count();
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t t = 0; t < n_local; ++t)
+      for (int si = 0; si < stages_per_tile; ++si) {
+        mbar_wait(&full[stage], phase);
+        if (lane == 0) mbar_arrive_remote(mapa_rank(smem_u32(&full[stage]), 0));
+        __syncwarp();
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
+      }
   } else if (warp == kMmaWarpS) {
     // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc = make_idesc<kI8>(kBM, BN);
-    constexpr uint32_t idesc_ones = make_idesc<kI8>(kBM, 16);
+    constexpr uint32_t idesc = make_idesc<kI8>(kBM * kCS, BN);
+    constexpr uint32_t idesc_ones = make_idesc<kI8>(kBM * kCS, 16);
     const uint64_t ones_desc = sw128_kmajor_desc(smem_u32(sOnes));
     const int stages_per_tile = (num_kb + C::kKB - 1) / C::kKB;
     int stage = 0;
@@ -403,15 +426,24 @@ __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_c
 #pragma unroll
             for (int k = 0; k < 4; ++k) {  // 4 x 32-byte K steps per 128-byte block
               const uint32_t acc = (si | j | k) != 0;
+              if constexpr (kCS == 1) {
 #ifndef ICV_EXP_NOMMA   // experiment: fills only
-              tc_mma<kI8>(d, adesc + 2 * k, bdesc + 2 * k, idesc, acc);
+                tc_mma<kI8>(d, adesc + 2 * k, bdesc + 2 * k, idesc, acc);
 #endif
-              if constexpr (kI8) tc_mma<true>(d + BN, adesc + 2 * k, ones_desc + 2 * k, idesc_ones, acc);
+                if constexpr (kI8) tc_mma<true>(d + BN, adesc + 2 * k, ones_desc + 2 * k, idesc_ones, acc);
+              } else {
+                tc_mma2<kI8>(d, adesc + 2 * k, bdesc + 2 * k, idesc, acc);
+                if constexpr (kI8) tc_mma2<true>(d + BN, adesc + 2 * k, ones_desc + 2 * k, idesc_ones, acc);
+              }
             }
           }
-          if constexpr (kCS == 1) tc_commit(&empty[stage]);
-          else tc_commit_mc(&empty[stage], kMask);   // the stage is free in every CTA that fills it
-          if (si == stages_per_tile - 1) tc_commit(&tfull[as]);
+          if constexpr (kCS == 1) {
+            tc_commit(&empty[stage]);
+            if (si == stages_per_tile - 1) tc_commit(&tfull[as]);
+          } else {   // the stage is free, and the accumulator ready, in both CTAs
+            tc_commit2_mc(&empty[stage], kMask);
+            if (si == stages_per_tile - 1) tc_commit2_mc(&tfull[as], kMask);
+          }
         }
         __syncwarp();
         if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -430,17 +462,20 @@ __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_c
     }
 #endif
   } else {
+    // a pair peer releases accumulators at the leader (which issues the next MMAs)
+    const uint32_t tempty_remote = (kCS == 2 && crank != 0) ? mapa_rank(smem_u32(tempty), 0) : 0u;
     epilogue_loop<kI8, BN, kEpiWarpsS, C::kAccStride>(a, warp - 4, lane, tmem_base, sEpi, sBias, tfull, tempty,
-                                                      sched, a.use_tma_y ? &tmap_y : nullptr);
+                                                      sched, a.use_tma_y ? &tmap_y : nullptr, tempty_remote);
   }
 
   tc_fence_before();
   __syncthreads();
+  if constexpr (kCS > 1) cluster_sync_all();   // both CTAs done: no peer still signals, writes or reads TMEM
   if (warp == kMmaWarpS) {
     tc_fence_after();
-    tmem_dealloc<C::kTmemCols>(tmem_base);
+    if constexpr (kCS == 2) tmem_dealloc2<C::kTmemCols>(tmem_base);
+    else tmem_dealloc<C::kTmemCols>(tmem_base);
   }
-  if constexpr (kCS > 1) cluster_sync_all();   // no peer still signals or writes into this CTA
 }
 
 template <bool kI8, int BN, typename IbT, int kCS>
@@ -450,7 +485,7 @@ int launch_smem_cs(const ConvArgs& c, cudaStream_t st) {
   static cudaError_t attr_err = cudaSuccess;
   static int max_clusters = 0;
   PlanS pl;
-  if (!plan_smem<kI8, BN, IbT>(c.g.RS(), c.L.n_pad, &pl))
+  if (!plan_smem<kI8, BN, IbT, kCS>(c.g.RS(), c.L.n_pad, &pl))
     return fail(ICV_ERR_UNSUPPORTED, "indirection slice of this kernel size does not fit in shared memory");
   if (c.g.N * c.g.H * c.g.W * (int64_t)c.g.C >= (int64_t(1) << 31))
     return fail(ICV_ERR_UNSUPPORTED, "tensor-core kernel: input tensors of 2^31 or more elements are not supported");
@@ -474,7 +509,7 @@ int launch_smem_cs(const ConvArgs& c, cudaStream_t st) {
   });
   if (attr_err != cudaSuccess) return cuda_check(attr_err, "kernel attributes (smem / clusters)");
   CUtensorMap tmap, tmap_x;
-  if (int s = make_filter_tmap(c, BN, kCS > 1 ? 1 : CfgS<kI8, BN>::kKB, &tmap)) return s;
+  if (int s = make_filter_tmap(c, BN / kCS, CfgS<kI8, BN>::kKB, &tmap)) return s;
   TcArgs a;
   fill_tc_args(c, BN, &a);
   // TMA tile::gather4 for A is correct but ~2.5x slower than the cp.async
@@ -513,11 +548,7 @@ int launch_smem_cs(const ConvArgs& c, cudaStream_t st) {
   return cuda_check(cudaGetLastError(), "igemm_smem launch");
 }
 
-// Filter-sharing clusters of 2 CTAs for BLOCK_N <= 128 (each CTA TMA-loads
-// half of a stage's filter blocks and multicasts them).  Correct, but on
-// B200 it measured slower than independent CTAs (the mainloop is bound by
-// L2->SM delivery into each SM, which multicast does not reduce), so it is
-// opt-in: ICV_CLUSTER=2.
+// CTA pairs (cta_group::2, M = 256): ICV_CLUSTER=2 (see the kernel).
 bool use_clusters() {
   static const char* v = getenv("ICV_CLUSTER");
   return v && v[0] == '2';
@@ -525,9 +556,7 @@ bool use_clusters() {
 
 template <bool kI8, int BN, typename IbT>
 int launch_smem(const ConvArgs& c, cudaStream_t st) {
-  if constexpr (CfgS<kI8, BN>::kKB == 2) {
-    if (use_clusters()) return launch_smem_cs<kI8, BN, IbT, 2>(c, st);
-  }
+  if (use_clusters()) return launch_smem_cs<kI8, BN, IbT, 2>(c, st);
   return launch_smem_cs<kI8, BN, IbT, 1>(c, st);
 }
 
