@@ -35,9 +35,14 @@ __device__ unsigned long long g_icv_trace[1024][128];
 
 namespace {
 
-constexpr int kEpiWarpsS = 4;
-constexpr int kMmaWarpS = 4 + kEpiWarpsS;
-constexpr int kThreadsS = 32 * (kMmaWarpS + 1);
+// Epilogue warps: 8 for uint8 (the q31 requantization is the heavier
+// epilogue; measured 47 -> 41 us on cfg4), 4 for bf16 (8 measured slower).
+template <bool kI8>
+constexpr int kEpiWarpsS = kI8 ? 8 : 4;
+template <bool kI8>
+constexpr int kMmaWarpS = 4 + kEpiWarpsS<kI8>;
+template <bool kI8>
+constexpr int kThreadsS = 32 * (kMmaWarpS<kI8> + 1);
 
 template <bool kI8, int BN, int kPair = 1>
 struct CfgS {
@@ -56,7 +61,7 @@ struct CfgS {
   static constexpr int kAccStride = kI8 ? 2 * BN : BN;  // TMEM columns per accumulator stage
   static constexpr int kTmemNeed = 2 * kAccStride;
   static constexpr uint32_t kTmemCols = kTmemNeed <= 64 ? 64 : kTmemNeed <= 128 ? 128 : kTmemNeed <= 256 ? 256 : 512;
-  static constexpr int kEpiBytes = kEpiWarpsS * kEpiWarpBytes<kI8>;
+  static constexpr int kEpiBytes = kEpiWarpsS<kI8> * kEpiWarpBytes<kI8>;
   static constexpr int kBarBytes = 256;
   static_assert(kTmemNeed <= 512, "TMEM overflow");
 };
@@ -114,7 +119,7 @@ struct ClusterTiles {
 };
 
 template <bool kI8, int BN, typename IbT, int kCS>
-__global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_constant__ CUtensorMap tmap_b,
+__global__ void __launch_bounds__(kThreadsS<kI8>, 1) igemm_smem_kernel(const __grid_constant__ CUtensorMap tmap_b,
                                                                   const __grid_constant__ CUtensorMap tmap_x,
                                                                   const __grid_constant__ CUtensorMap tmap_y,
                                                                   const TcArgs a, const PlanS pl) {
@@ -171,7 +176,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_c
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);                   // tcgen05.commit after the last K block
       // one arrival per epilogue warp (of both CTAs at the pair leader)
-      mbar_init(&tempty[s], (kCS == 2 && crank == 0) ? 2 * kEpiWarpsS : kEpiWarpsS);
+      mbar_init(&tempty[s], (kCS == 2 && crank == 0) ? 2 * kEpiWarpsS<kI8> : kEpiWarpsS<kI8>);
     }
     fence_mbar_init();
     tma_prefetch_desc(&tmap_b);
@@ -185,7 +190,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_c
     }
   }
   for (int i = threadIdx.x; i < a.n_pad; i += blockDim.x) sBias[i] = __ldg(static_cast<const uint32_t*>(a.bias) + i);
-  if (warp == kMmaWarpS) {
+  if (warp == kMmaWarpS<kI8>) {
     if constexpr (kCS == 2) tmem_alloc2<C::kTmemCols>(tmem_slot);
     else tmem_alloc<C::kTmemCols>(tmem_slot);
   }
@@ -368,7 +373,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_c
       g_icv_trace[blockIdx.x][38] = (unsigned long long)p_wait;
     }
 #endif
-  } else if (warp == kMmaWarpS && kCS == 2 && crank != 0) {
+  } else if (warp == kMmaWarpS<kI8> && kCS == 2 && crank != 0) {
     // ------------------------------------------------------------ pair peer: forwarder
     // The leader's MMAs read this CTA's stages too: once a stage is full here
     // (own gathers + own filter half), tell the leader's full barrier.
@@ -383,7 +388,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_c
         __syncwarp();
         if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
-  } else if (warp == kMmaWarpS) {
+  } else if (warp == kMmaWarpS<kI8>) {
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t idesc = make_idesc<kI8>(kBM * kCS, BN);
     constexpr uint32_t idesc_ones = make_idesc<kI8>(kBM * kCS, 16);
@@ -464,14 +469,14 @@ __global__ void __launch_bounds__(kThreadsS, 1) igemm_smem_kernel(const __grid_c
   } else {
     // a pair peer releases accumulators at the leader (which issues the next MMAs)
     const uint32_t tempty_remote = (kCS == 2 && crank != 0) ? mapa_rank(smem_u32(tempty), 0) : 0u;
-    epilogue_loop<kI8, BN, kEpiWarpsS, C::kAccStride>(a, warp - 4, lane, tmem_base, sEpi, sBias, tfull, tempty,
+    epilogue_loop<kI8, BN, kEpiWarpsS<kI8>, C::kAccStride>(a, warp - 4, lane, tmem_base, sEpi, sBias, tfull, tempty,
                                                       sched, a.use_tma_y ? &tmap_y : nullptr, tempty_remote);
   }
 
   tc_fence_before();
   __syncthreads();
   if constexpr (kCS > 1) cluster_sync_all();   // both CTAs done: no peer still signals, writes or reads TMEM
-  if (warp == kMmaWarpS) {
+  if (warp == kMmaWarpS<kI8>) {
     tc_fence_after();
     if constexpr (kCS == 2) tmem_dealloc2<C::kTmemCols>(tmem_base);
     else tmem_dealloc<C::kTmemCols>(tmem_base);
@@ -500,7 +505,7 @@ int launch_smem_cs(const ConvArgs& c, cudaStream_t st) {
       at[0].val.clusterDim.y = 1;
       at[0].val.clusterDim.z = 1;
       q.gridDim = dim3(kCS * 74);
-      q.blockDim = dim3(kThreadsS);
+      q.blockDim = dim3(kThreadsS<kI8>);
       q.dynamicSmemBytes = pl.bytes;
       q.attrs = at;
       q.numAttrs = 1;
@@ -523,7 +528,7 @@ int launch_smem_cs(const ConvArgs& c, cudaStream_t st) {
   const int sms = sm_count();
   if constexpr (kCS == 1) {
     const int grid = (int)(a.total_tiles < sms ? a.total_tiles : sms);
-    kernel<<<grid, kThreadsS, pl.bytes, st>>>(tmap, tmap_x, tmap_y, a, pl);
+    kernel<<<grid, kThreadsS<kI8>, pl.bytes, st>>>(tmap, tmap_x, tmap_y, a, pl);
   } else {
     const int64_t groups = (a.total_tiles / a.n_tiles + kCS - 1) / kCS * a.n_tiles;
     int64_t clusters = sms / kCS;
@@ -536,7 +541,7 @@ int launch_smem_cs(const ConvArgs& c, cudaStream_t st) {
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     cfg.gridDim = dim3((unsigned)(clusters * kCS));
-    cfg.blockDim = dim3(kThreadsS);
+    cfg.blockDim = dim3(kThreadsS<kI8>);
     cfg.dynamicSmemBytes = pl.bytes;
     cfg.stream = st;
     cfg.attrs = at;
