@@ -39,8 +39,14 @@ namespace {
 // epilogue; measured 47 -> 41 us on cfg4), 4 for bf16 (8 measured slower).
 template <bool kI8>
 constexpr int kEpiWarpsS = kI8 ? 8 : 4;
+// Gather (producer) warps: each covers 128 / kProdWarpsS A rows.
+#ifndef ICV_PROD_WARPS_BF16
+#define ICV_PROD_WARPS_BF16 4   // 8 measured equal on cfg2 / cfg3b (the fill is L2->SM bound, not issue bound)
+#endif
 template <bool kI8>
-constexpr int kMmaWarpS = 4 + kEpiWarpsS<kI8>;
+constexpr int kProdWarpsS = kI8 ? 4 : ICV_PROD_WARPS_BF16;
+template <bool kI8>
+constexpr int kMmaWarpS = kProdWarpsS<kI8> + kEpiWarpsS<kI8>;
 template <bool kI8>
 constexpr int kThreadsS = 32 * (kMmaWarpS<kI8> + 1);
 
@@ -170,7 +176,7 @@ __global__ void __launch_bounds__(kThreadsS<kI8>, 1) igemm_smem_kernel(const __g
     for (int s = 0; s < kStages; ++s) {
       // TMA path: 1 expect_tx arrival; cp.async path: 128 producer arrivals + 1
       // cp.async path: 128 producer arrivals + 1 expect_tx (+ 1 forwarded from the peer, pair leader)
-      mbar_init(&full[s], tma_gather ? 1 : 128 + 1 + (kCS == 2 && crank == 0 ? 1 : 0));
+      mbar_init(&full[s], tma_gather ? 1 : 32 * kProdWarpsS<kI8> + 1 + (kCS == 2 && crank == 0 ? 1 : 0));
       mbar_init(&empty[s], 1);       // tcgen05.commit (multicast to both CTAs of a pair)
     }
     for (int s = 0; s < 2; ++s) {
@@ -204,15 +210,17 @@ __global__ void __launch_bounds__(kThreadsS<kI8>, 1) igemm_smem_kernel(const __g
   const uint32_t sA_u32 = smem_u32(sA);
   const uint32_t sB_u32 = smem_u32(sB);
 
-  if (warp < 4) {
+  if (warp < kProdWarpsS<kI8>) {
     // ------------------------------------------------------------ producers
+    constexpr int kPW = kProdWarpsS<kI8>;
+    constexpr int kRowsW = kBM / kPW;          // A rows per producer warp (32 or 16)
     const int chunk = lane & 7;
     const int sub = lane >> 3;
     const int slice_elems = a.RS * kBM;
     const int64_t my_tiles = sched.count();
     // cp.async the (R*S taps x 128 pixels) index slice of local tile k into buffer k&1
     auto stage_index_slice = [&](int64_t k) {
-      if (k < my_tiles) {
+      if (k < my_tiles && threadIdx.x < kBM) {
         const int64_t mt = sched(k) / a.n_tiles;
         const uint32_t base = smem_u32(sIB + (k & 1) * slice_elems) + threadIdx.x * 4;
         const RowRef rr = row_ref(a, mt, threadIdx.x);                        // row = threadIdx.x
@@ -225,7 +233,7 @@ __global__ void __launch_bounds__(kThreadsS<kI8>, 1) igemm_smem_kernel(const __g
     };
     stage_index_slice(0);
     cp_async_wait_committed();
-    named_bar_sync(1, 128);
+    named_bar_sync(1, 32 * kProdWarpsS<kI8>);
     int stage = 0;
     uint32_t phase = 0;
 #ifdef ICV_TRACE
@@ -287,12 +295,12 @@ __global__ void __launch_bounds__(kThreadsS<kI8>, 1) igemm_smem_kernel(const __g
         // destinations are two registers plus immediates, and with the
         // channel-block count known at compile time the source offsets are
         // immediates too.
-        const int myrow = warp * 32 + lane;
+        const int myrow = warp * kRowsW + (lane & (kRowsW - 1));
         const int64_t mybase = rbase[myrow];
         const bool c_full = (a.c_bytes & 127) == 0;
         uint32_t dofs[2];
 #pragma unroll
-        for (int b = 0; b < 2; ++b) dofs[b] = (warp * 32 + 4 * b + sub) * 128 + ((chunk ^ (4 * b + sub)) << 4);
+        for (int b = 0; b < 2; ++b) dofs[b] = (warp * kRowsW + 4 * b + sub) * 128 + ((chunk ^ (4 * b + sub)) << 4);
         auto gather_tile = [&](auto cbc) {
           constexpr int kCBc = decltype(cbc)::value;   // 0: runtime channel-block count
           const int cblocks = kCBc ? kCBc : a.cblocks;
@@ -301,9 +309,9 @@ __global__ void __launch_bounds__(kThreadsS<kI8>, 1) igemm_smem_kernel(const __g
           for (int e = 0; e < a.RS; ++e) {
             const int64_t off = resolve_ref((int64_t)slice[e * kBM + myrow], mybase);
             const uint8_t* mine = off < 0 ? a.zero_row : a.x + off * a.elem_bytes;   // ZERO_REF -> zero row
-            const uint8_t* src[8];
+            const uint8_t* src[kRowsW / 4];
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
+            for (int i = 0; i < kRowsW / 4; ++i)
               src[i] = reinterpret_cast<const uint8_t*>(
                            __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(mine), 4 * i + sub)) +
                        chunk * 16;
@@ -322,7 +330,7 @@ __global__ void __launch_bounds__(kThreadsS<kI8>, 1) igemm_smem_kernel(const __g
                 // the stage's filter blocks: one 3-D box (kKB K blocks; a tail
                 // block past the filter is zero-filled and never multiplied),
                 // issued by the producer warps in turn
-                if (lane == 0 && warp == (stage_seq & 3)) {
+                if (lane == 0 && warp == (stage_seq % kPW)) {
                   mbar_arrive_expect_tx(&full[stage], C::kKB * C::kBBytes);
                   // (a pair member loads its half of the BN filter rows)
                   tma_load_3d(sB_u32 + stage * C::kKB * C::kBBytes, &tmap_b, &full[stage], 0,
@@ -335,13 +343,13 @@ __global__ void __launch_bounds__(kThreadsS<kI8>, 1) igemm_smem_kernel(const __g
 #ifndef ICV_EXP_NOA   // experiment: no A gathers
               if (c_full || cb + 1 < cblocks) {
 #pragma unroll
-                for (int i = 0; i < 8; ++i)
+                for (int i = 0; i < kRowsW / 4; ++i)
                   cp_async_16_full((i & 1 ? d1 : d0) + (i >> 1) * 1024, src[i] + cb * 128);
               } else {   // partial last channel block: zero-fill past C
                 int valid = a.c_bytes - (cb * 128 + chunk * 16);
                 valid = valid < 0 ? 0 : (valid > 16 ? 16 : valid);
 #pragma unroll
-                for (int i = 0; i < 8; ++i)
+                for (int i = 0; i < kRowsW / 4; ++i)
                   cp_async_16((i & 1 ? d1 : d0) + (i >> 1) * 1024, valid ? src[i] + cb * 128 : a.x, (uint32_t)valid);
               }
 #endif
@@ -365,7 +373,7 @@ __global__ void __launch_bounds__(kThreadsS<kI8>, 1) igemm_smem_kernel(const __g
       // and every producer is done reading slice k
       cp_async_wait_committed();
       if (threadIdx.x == 0 && k < 8) TRACE(48 + k);   // producer: next slice landed
-      named_bar_sync(1, 128);
+      named_bar_sync(1, 32 * kProdWarpsS<kI8>);
     }
 #ifdef ICV_TRACE
     if (threadIdx.x == 0) {
@@ -469,7 +477,7 @@ __global__ void __launch_bounds__(kThreadsS<kI8>, 1) igemm_smem_kernel(const __g
   } else {
     // a pair peer releases accumulators at the leader (which issues the next MMAs)
     const uint32_t tempty_remote = (kCS == 2 && crank != 0) ? mapa_rank(smem_u32(tempty), 0) : 0u;
-    epilogue_loop<kI8, BN, kEpiWarpsS<kI8>, C::kAccStride>(a, warp - 4, lane, tmem_base, sEpi, sBias, tfull, tempty,
+    epilogue_loop<kI8, BN, kEpiWarpsS<kI8>, C::kAccStride>(a, warp - kProdWarpsS<kI8>, lane, tmem_base, sEpi, sBias, tfull, tempty,
                                                       sched, a.use_tma_y ? &tmap_y : nullptr, tempty_remote);
   }
 
