@@ -59,7 +59,10 @@ constexpr int kLoadWarpR = kMmaWarpR + 1;
 constexpr int kThreadsR = 32 * (kLoadWarpR + 1);
 constexpr int kMDone = 4;                 // MMA-done barriers (tile k -> k % 4)
 constexpr int kStagesR = 6;               // raw-row stages in flight (the loader runs this many tiles ahead)
-constexpr int kAccR = 4;                  // TMEM accumulators (the MMA may run kAccR tiles ahead of the epilogue)
+constexpr int kRowsReady = 8;             // converted-tile barriers (converters run up to kLag + 1 tiles ahead of the MMA)
+// TMEM accumulators (the MMA may run kAccR tiles ahead of the epilogue)
+template <int BN>
+constexpr int kAccRFor = BN <= 64 ? 8 : 4;
 
 struct RowsArgs {
   TcArgs t;                     // epilogue fields (y, K, bias, n_tiles = 1, tiles_per_row, P)
@@ -138,6 +141,16 @@ struct TileWalk {
 template <int BN, int kR, int kKS, int kC>
 __global__ void __launch_bounds__(kThreadsR, 1) igemm_rows_kernel(const __grid_constant__ CUtensorMap tmap_y,
                                                                   const RowsArgs a, const RowsPlan pl) {
+  constexpr int kAccR = kAccRFor<BN>;
+  // Ring-slot reuse: the 2 rows tile k adds evict rows last read by tile
+  // k - (kRing + 1 - kR) / 2 or earlier, so within an image the converters
+  // only wait for the MMAs of tile k - kLag (bounded by the accumulator ring
+  // so the tfull phase they wait on is unambiguous); a new image may evict
+  // anything, so its first tile waits for all earlier MMAs.
+  constexpr int kLagRing = (kRing + 1 - kR) / 2;
+  constexpr int kLagCap = kAccR - 1 < kRowsReady - 2 ? kAccR - 1 : kRowsReady - 2;
+  constexpr int kLag = kLagRing < kLagCap ? kLagRing : kLagCap;
+  static_assert(kLag + 2 <= kRowsReady, "rows_ready phases must stay unambiguous");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sB = smem + pl.off_b;
@@ -148,8 +161,8 @@ __global__ void __launch_bounds__(kThreadsR, 1) igemm_rows_kernel(const __grid_c
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + pl.off_bar);
   uint64_t* stage_full = bars;                    // [kStagesR] raw rows landed (bulk copy)
   uint64_t* stage_free = stage_full + kStagesR;   // [kStagesR] converters done with the raw rows
-  uint64_t* rows_ready = stage_free + kStagesR;   // [2] tile's rows converted
-  uint64_t* mdone = rows_ready + 2;               // [4] MMAs of tile k complete
+  uint64_t* rows_ready = stage_free + kStagesR;   // [kRowsReady] tile's rows converted
+  uint64_t* mdone = rows_ready + kRowsReady;      // [4] (unused)
   uint64_t* tfull = mdone + kMDone;               // [kAccR]
   uint64_t* tempty = tfull + kAccR;               // [kAccR]
   uint64_t* bfull = tempty + kAccR;
@@ -170,7 +183,7 @@ __global__ void __launch_bounds__(kThreadsR, 1) igemm_rows_kernel(const __grid_c
       mbar_init(&stage_full[s], 1);
       mbar_init(&stage_free[s], kConvWarps);   // one arrival per converter warp
     }
-    for (int s = 0; s < 2; ++s) mbar_init(&rows_ready[s], kConvWarps);
+    for (int s = 0; s < kRowsReady; ++s) mbar_init(&rows_ready[s], kConvWarps);
     for (int s = 0; s < kAccR; ++s) {
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], 4);   // one arrival per warp of the epilogue group that owns the tile
@@ -233,12 +246,11 @@ __global__ void __launch_bounds__(kThreadsR, 1) igemm_rows_kernel(const __grid_c
     const uint32_t stage_u32 = smem_u32(sStage);
     for (int64_t k = 0; k < my_tiles; ++k) {
       const int s = (int)(k % kStagesR);
-      const int rs = (int)(k & 1);
+      const int rs = (int)(k % kRowsReady);
       const TileRows tr = walk.next(a);
-      // the ring rows this tile overwrites are free once the MMAs of tile k-2
-      // (same image: no row of tile k-1 is evicted) or of tile k-1 (a new
-      // image: anything may be) have completed
-      const int64_t need = tr.fresh ? k - 1 : k - 2;
+      // the ring rows this tile overwrites are free once the MMAs of tile
+      // k - kLag (same image) or of tile k-1 (a new image) have completed
+      const int64_t need = tr.fresh ? k - 1 : k - kLag;
       RP_ACC(3);
       if (need >= 0) mbar_wait(&tfull[need % kAccR], (uint32_t)(need / kAccR) & 1u);   // MMAs of tile `need` done
       RP_ACC(0);
@@ -301,12 +313,11 @@ __global__ void __launch_bounds__(kThreadsR, 1) igemm_rows_kernel(const __grid_c
     // descriptor constant parts (address field = bits 0..13, smem < 256 KB)
     const uint64_t adesc0 = desc_noswz(0, 16, 128), bdesc0 = desc_noswz(sB_u32, 128, 512);
     for (int64_t k = 0; k < my_tiles; ++k) {
-      const int s = (int)(k & 1);
       const TileRows tr = walk.next(a);
       RP_ACC(3);
       mbar_wait(&tempty[as], aphase ^ 1);
       RP_ACC(0);
-      mbar_wait(&rows_ready[s], (uint32_t)(k >> 1) & 1u);
+      mbar_wait(&rows_ready[k % kRowsReady], (uint32_t)(k / kRowsReady) & 1u);
       RP_ACC(1);
       tc_fence_after();
       RP_ACC(3);
@@ -366,6 +377,7 @@ bool plan_rows(const ConvArgs& c, int BN, int tpr, RowsPlan* p, int* ring_row_by
   const int ring = (kRing + 1) * *ring_row_bytes;
   const int stage = (c.g.R * (int)c.g.W * c.g.C * 2 + 15) / 16 * 16;
   const int epi = kEpiWarpsR * kEpiWarpBytes<false>;
+  (void)BN;
   int off = 0;
   p->off_epi = off;  off += epi;                       // 1024-aligned (TMA-store staging)
   p->off_b = off;    off += (b + 1023) / 1024 * 1024;
