@@ -223,6 +223,23 @@ def setup_problem(name: str, n_lo: int, n_hi: int, device, pf_bcast=None, mr: in
     return w, x, xh, pf, ib, y, tile
 
 
+def make_l2_flush(device):
+    """L2 flush between timed steps: write a 256 MiB buffer (evicts every line
+    of the step's inputs from the 126 MB L2), then read another 256 MiB, so
+    the write's dirty lines are written back HERE rather than inside the next
+    timed step.  Both outside the CUDA events."""
+    import torch
+
+    wbuf = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=device)
+    rbuf = torch.ones(32 * 1024 * 1024, dtype=torch.int64, device=device)
+
+    def flush():
+        wbuf.fill_(1)
+        torch.sum(rbuf)
+
+    return flush
+
+
 def time_steps(fn, steps: int, warmup: int, flush=None, on_timed=None):
     """Per-step CUDA-event times (ms) of fn() on the current stream, with an
     optional L2 flush before every step (outside the events)."""
@@ -310,10 +327,7 @@ def gpu_bench(args) -> None:
     wl.CONFIGS["_bench"] = big
     w, x, xh, pf, ib, y, tile = setup_problem("_bench", rank * per_rank, (rank + 1) * per_rank, device, bcast,
                                               mr=args.mr, per_image=args.ib == "per-image")
-    flush_buf = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=device)
-
-    def flush():
-        flush_buf.fill_(1)
+    flush = make_l2_flush(device)
 
     def step():
         icv.indirect_conv(x, pf, ib, w.params, tile, out=y)
@@ -464,7 +478,7 @@ def gpu_bench(args) -> None:
                    "H": w0.in_shape.h, "W": w0.in_shape.w, "C": w0.in_shape.c, "K": w0.params.out_channels,
                    "kernel": f"{w0.params.kernel_h}x{w0.params.kernel_w}", "parallelism": f"dp{world} (batch-sharded)",
                    "mr": args.mr, "index_dtype": "int64", "ib_layout": args.ib,
-                   "l2": "flushed between steps (256 MiB device write, outside the timed events)",
+                   "l2": "flushed between steps (256 MiB device write + 256 MiB read, outside the timed events)",
                    "conv_kernel": _lib.kernel_name(w0.params, w0.in_shape, x.dtype)},
         "roofline": roof,
         "e2e": {"value": round(w0.flops * world * e2e_n / (e2e_total * 1e-3) / 1e12, 4), "unit": "TFLOP/s",

@@ -66,6 +66,12 @@ typedef enum icv_dtype {
  * granularity (row-sliding kernel); without it they gather tap by tap. */
 #define ICV_IB_CANONICAL 0x200
 
+/* Flag OR-ed into icv_conv's `ib_dtype`: the bound zero row is all zero
+ * bytes (and, per the reference's contract, read-only: indirect.py:42).
+ * Stride-1 layers may then realize padding as out-of-bounds zero fill of
+ * their TMA windows instead of reading the zero row. */
+#define ICV_ZERO_ROW_ZEROS 0x400
+
 /* Convolution geometry; field-for-field convbench.tensors.ConvParams
  * (tensors.py:41-72). */
 typedef struct icv_conv_desc {
@@ -167,8 +173,10 @@ ICV_API int icv_conv(const icv_conv_desc* desc, const icv_shape4* in, int64_t ba
              const void* zero_row, const void* ib, int32_t ib_dtype, int32_t mr, const void* packed,
              const icv_quant* quant, void* y, void* stream);
 
-/* Which kernel icv_conv would launch for this problem (for tests/benches):
- * writes a static NUL-terminated name into *name. */
+/* Which kernel icv_conv would launch for this problem (for tests/benches)
+ * with a canonical buffer (ICV_IB_CANONICAL, as init_indirection_buffer
+ * builds) and a 16-byte aligned input: writes a static NUL-terminated name
+ * into *name. */
 ICV_API int icv_conv_kernel_name(const icv_conv_desc* desc, const icv_shape4* in, int32_t dtype, const char** name);
 
 /* Launch counter: number of kernels this library has launched in this

@@ -275,6 +275,9 @@ ICV_API int icv_conv_kernel_name(const icv_conv_desc* desc, const icv_shape4* in
   if (int s = make_geom(desc, in, &a.g)) return s;
   if (int s = packed_layout(desc, dtype, &a.L)) return s;
   a.P = in->n * a.g.OH * a.g.OW;
+  a.ib_canonical = 1;   // as for every buffer init_indirection_buffer builds
+  a.zero_known = 1;     // (a float zero row from make_zero_row)
+  a.x = reinterpret_cast<const void*>(uintptr_t(256));   // (16-byte aligned input assumed)
   if (name) *name = kernel_name_for(a);
   return ICV_OK;
 }
@@ -288,7 +291,8 @@ ICV_API int icv_conv(const icv_conv_desc* desc, const icv_shape4* in, int64_t ba
   if (mr < 1) return fail(ICV_ERR_ARG, "mr must be >= 1");
   a.ib_per_image = (ib_dtype & ICV_IB_PER_IMAGE) != 0;
   a.ib_canonical = (ib_dtype & ICV_IB_CANONICAL) != 0;
-  ib_dtype &= ~(ICV_IB_PER_IMAGE | ICV_IB_CANONICAL);
+  a.zero_known = (ib_dtype & ICV_ZERO_ROW_ZEROS) != 0;
+  ib_dtype &= ~(ICV_IB_PER_IMAGE | ICV_IB_CANONICAL | ICV_ZERO_ROW_ZEROS);
   if (ib_dtype != ICV_I64 && ib_dtype != ICV_I32) return fail(ICV_ERR_ARG, "ib dtype must be int64 or int32");
   if (!x || !zero_row || !ib || !packed || !y) return fail(ICV_ERR_ARG, "null tensor pointer");
   if (int s = packed_layout(desc, dtype, &a.L)) return s;

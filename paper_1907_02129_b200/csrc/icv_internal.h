@@ -64,6 +64,7 @@ struct ConvArgs {
   int32_t ib_is_i32;
   int32_t ib_per_image;  // entries are image-relative (ICV_IB_PER_IMAGE)
   int32_t ib_canonical;  // caller guarantees the icv_ib_build layout (ICV_IB_CANONICAL)
+  int32_t zero_known;    // caller guarantees the zero row is all zero bytes (ICV_ZERO_ROW_ZEROS)
   const uint8_t* packed;
   PackedLayout L;
   void* y;
@@ -73,6 +74,8 @@ struct ConvArgs {
 int launch_conv_f32_exact(const ConvArgs& a, cudaStream_t st);
 int launch_conv_core(const ConvArgs& a, cudaStream_t st);       // bf16 / u8, any C (CUDA cores)
 int launch_conv_tc(const ConvArgs& a, cudaStream_t st);         // bf16 / u8 tcgen05
+bool win_kernel_eligible(const ConvArgs& a);                   // stride-1 window kernel applies
+int launch_conv_win(const ConvArgs& a, cudaStream_t st);        // bf16 / u8 tcgen05, sliding window A
 const char* tc_kernel_name(const ConvArgs& a);
 int launch_conv_stem(const ConvArgs& a, cudaStream_t st);   // channel-poor bf16 (tcgen05)
 bool rows_kernel_eligible(const Geom& g);

@@ -738,6 +738,7 @@ bool tc_kernel_available(const ConvArgs& c) {
 
 int launch_conv_tc(const ConvArgs& c, cudaStream_t st) {
   if (c.L.n_pad > kMaxBias) return fail(ICV_ERR_UNSUPPORTED, "more than 2048 output channels");
+  if (win_kernel_eligible(c)) return launch_conv_win(c, st);
   if (use_tmem_kernel() && tmem_kernel_eligible(c)) return launch_conv_tmem(c, st);
   if (c.ib_is_i32) return dispatch_smem<int32_t>(c, st);
   return dispatch_smem<int64_t>(c, st);
@@ -745,6 +746,7 @@ int launch_conv_tc(const ConvArgs& c, cudaStream_t st) {
 
 const char* tc_kernel_name(const ConvArgs& c) {
   const bool i8 = c.L.family == kFamTcU8;
+  if (win_kernel_eligible(c)) return i8 ? "icv_igemm_win<u8>" : "icv_igemm_win<bf16>";
   if (use_tmem_kernel() && tmem_kernel_eligible(c)) return i8 ? "icv_igemm_tmem<u8>" : "icv_igemm_tmem<bf16>";
   return i8 ? "icv_igemm_smem<u8>" : "icv_igemm_smem<bf16>";
 }

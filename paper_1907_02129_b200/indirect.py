@@ -69,6 +69,10 @@ class IndirectionBuffer:
     # made by this module; an initialized buffer is immutable).
     # Lets channel-poor stride-2 layers read it at input-row granularity.
     canonical: bool = True
+    # the zero row was all zero bytes when the buffer was initialized (it is
+    # read-only by contract, indirect.py:42): stride-1 layers may then take
+    # padding from TMA out-of-bounds zero fill (ICV_ZERO_ROW_ZEROS)
+    zero_is_zero: bool = False
 
     @property
     def pixel_count(self) -> int:
@@ -171,8 +175,9 @@ def init_indirection_buffer(input: NhwcTensor, zero_row: torch.Tensor, params: C
     tiles = _tile_count(pixels, tile.mr)
     offsets = torch.empty((tiles, params.kernel_elems, tile.mr), dtype=index_dtype, device=input.data.device)
     _build(input.shape, params, batch, tile.mr, offsets, 0, per_image)
+    zero_is_zero = not bool(zero_row.view(torch.uint8).any().item())
     return IndirectionBuffer(tile.mr, batch, out_shape.h, out_shape.w, params, input.shape, input.data,
-                             zero_row, offsets, per_image)
+                             zero_row, offsets, per_image, zero_is_zero=zero_is_zero)
 
 
 def update_for_batch_growth(ib: IndirectionBuffer, new_batch: int) -> IndirectionBuffer:
@@ -266,7 +271,8 @@ def indirect_conv(input: NhwcTensor, pf: PackedFilter, ib: IndirectionBuffer, pa
         L.check(L.lib().icv_conv(ctypes.byref(d), ctypes.byref(s), batch, L.TORCH_TO_ICV[input.dtype],
                                  L.ptr(input.data), L.ptr(ib.zero_row), L.ptr(ib.offsets),
                                  L.TORCH_TO_ICV[ib.offsets.dtype] | (L.ICV_IB_PER_IMAGE if ib.per_image else 0)
-                                 | (L.ICV_IB_CANONICAL if ib.canonical else 0),
+                                 | (L.ICV_IB_CANONICAL if ib.canonical else 0)
+                                 | (L.ICV_ZERO_ROW_ZEROS if ib.zero_is_zero else 0),
                                  ib.mr, L.ptr(pf.packed),
                                  ctypes.byref(q) if q is not None else None, L.ptr(out.data), L.stream_of(dev)),
                 "icv_conv")

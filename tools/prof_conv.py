@@ -25,9 +25,9 @@ def main():
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(0)
     w, x, xh, pf, ib, y, tile = bench.setup_problem(args.config, 0, CONFIGS[args.config].in_shape.n, dev, mr=args.mr)
-    flush_buf = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    flush_l2 = bench.make_l2_flush(dev)
     for _ in range(args.iters):
-        flush_buf.fill_(1)
+        flush_l2()
         icv.indirect_conv(x, pf, ib, w.params, tile, out=y)
     torch.cuda.synchronize()
     print("done", args.config)

@@ -34,13 +34,13 @@ def main():
                                                     mr=args.mr)
     fn = L.lib().icv_debug_stats
     fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush_l2 = bench.make_l2_flush(dev)
     for _ in range(3):
         icv.indirect_conv(x, pf, ib, w.params, tile, out=y)
     torch.cuda.synchronize()
     buf = np.zeros((1024, 8), np.uint64)
     fn(None, 1)
-    flush.fill_(1)
+    flush_l2()
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()

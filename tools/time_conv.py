@@ -17,14 +17,14 @@ def main():
 
     names = sys.argv[1:] or ["cfg2", "cfg3b", "cfg4"]
     dev = torch.device("cuda", 0)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush_l2 = bench.make_l2_flush(dev)
     for name in names:
         w, x, xh, pf, ib, y, tile = bench.setup_problem(name, 0, CONFIGS[name].in_shape.n, dev,
                                                         per_image=os.environ.get("ICV_IB", "per-image") == "per-image")
         if os.environ.get("ICV_NONCANONICAL"):
             ib.canonical = False
         t = bench.time_steps(lambda: icv.indirect_conv(x, pf, ib, w.params, tile, out=y), 50, 5,
-                             lambda: flush.fill_(1))
+                             flush_l2)
         ms = statistics.median(t)
         ok = ""
         if w.dtype == "bf16" and not os.environ.get("ICV_NO_GATE"):

@@ -22,11 +22,11 @@ def main():
     w, x, xh, pf, ib, y, tile = bench.setup_problem(name, 0, CONFIGS[name].in_shape.n, dev)
     fn = L.lib().icv_debug_trace
     fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush_l2 = bench.make_l2_flush(dev)
     for _ in range(3):
         icv.indirect_conv(x, pf, ib, w.params, tile, out=y)
     fn(None, 1)
-    flush.fill_(1)
+    flush_l2()
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
@@ -75,11 +75,11 @@ def stages(name="cfg2"):
     w, x, xh, pf, ib, y, tile = bench.setup_problem(name, 0, CONFIGS[name].in_shape.n, dev)
     fn = L.lib().icv_debug_trace
     fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush_l2 = bench.make_l2_flush(dev)
     for _ in range(3):
         icv.indirect_conv(x, pf, ib, w.params, tile, out=y)
     fn(None, 1)
-    flush.fill_(1)
+    flush_l2()
     icv.indirect_conv(x, pf, ib, w.params, tile, out=y)
     torch.cuda.synchronize()
     buf = np.zeros((1024, 128), np.uint64)
