@@ -79,6 +79,7 @@ struct WinArgs {
   int32_t cbe;           // elements per 128-byte channel block
   int32_t win_lead;      // bytes from a slot's start to the window's first row (1024-aligned)
   int32_t zero_known;    // host certifies the zero row is all zeros (no in-kernel check)
+  int32_t win_split;     // TMA windows: rows split over this many issuing threads (lane 0 of warps 0..)
 };
 
 struct PlanW {
@@ -199,6 +200,46 @@ __device__ __forceinline__ UnitTiles unit_tiles(const WinArgs& a, int32_t u, uin
   return r;
 }
 
+#ifdef ICV_WEXP_PREFETCH   // experiment: L2 prefetch of the next window (measured slower: cfg2 25.5 -> 27.5 us)
+constexpr bool kNoPrefetch = false;
+#else
+constexpr bool kNoPrefetch = true;
+#endif
+
+#ifdef ICV_WEXP_FILTER1   // experiment: thread 0 alone loads the resident filter
+constexpr bool kFilter1 = true;
+#else
+constexpr bool kFilter1 = false;
+#endif
+
+// Prefetch into L2 the input rows a unit's window covers (every channel: the
+// rows of one image are contiguous), one bulk prefetch per image touched.
+__device__ __forceinline__ void prefetch_window(const WinArgs& a, const UnitTiles& ut) {
+  if (ut.stand_in) return;
+  const WinTile tw = win_tile(a, ut.first);
+  int32_t g = tw.g0;
+  const int32_t gend = g + (ut.cnt == 2 ? a.WR2 : a.WR);
+  const int64_t row_b = (int64_t)a.W * a.t.c_bytes;
+  while (g < gend) {
+    const int32_t n = g / a.Hz;
+    if (n >= a.batch) break;
+    const int32_t r = g - n * a.Hz;
+    const int32_t h = min(gend - g, a.Hz - r);
+    const int32_t iy0 = max(r - a.Zr, 0), iy1 = min(r + h - a.Zr, a.H);
+    if (iy1 > iy0) {
+      int64_t bytes = (int64_t)(iy1 - iy0) * row_b;
+      const uint8_t* src = a.t.x + ((int64_t)n * a.H + iy0) * row_b;
+      while (bytes > 0) {   // (bulk prefetch sizes are 32-bit; 16-byte multiples)
+        const uint32_t b = (uint32_t)(bytes < (1 << 20) ? bytes : (1 << 20));
+        bulk_prefetch_l2(src, b & ~15u);
+        src += b;
+        bytes -= b;
+      }
+    }
+    g += h;
+  }
+}
+
 template <bool kI8, int BN, int kMT, int kCS>
 __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_constant__ CUtensorMap tmap_b,
                                                             const __grid_constant__ WinMaps maps,
@@ -237,6 +278,9 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) TRACE(0);
+#ifdef ICV_TRACE
+  if (threadIdx.x == 0) g_icv_trace[blockIdx.x][62] = (unsigned long long)clock64();
+#endif
   // TMA windows realize padding as out-of-bounds (zero-filled) pixels: only
   // valid when the bound zero row is all zeros.  The host certifies that
   // (zero_known) or the CTA checks it; otherwise the producers gather the
@@ -265,6 +309,9 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
     fence_mbar_init();
     tma_prefetch_desc(&tmap_b);
   }
+#ifndef ICV_WEXP_NODESCPF
+  if (warp == 1 && lane < kMaxWR && lane < (a.WR2 > a.WR ? a.WR2 : a.WR)) tma_prefetch_desc(&maps.m[lane]);
+#endif
   if constexpr (kI8) {
     if (threadIdx.x < 128) {   // all-ones B tile (16 rows x 128 bytes): per-pixel input sums
       reinterpret_cast<uint4*>(sOnes)[threadIdx.x] = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
@@ -291,11 +338,31 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
   const uint32_t sB_u32 = smem_u32(sB);
   const int32_t row_bytes = a.Wp * 128;   // one plane row of one channel block
 
+  // resident filter: K-block slot `slot` = (channel block cb, tap e) of this CTA's rows
+  auto load_filter_slot = [&](int slot) {
+    const int cb = slot / RS, e = slot - cb * RS;
+    if (crank == 0) mbar_arrive_expect_tx(&bfull[slot], kCS * C::kBBytes);
+    if constexpr (kCS == 2)
+      tma_load_3d_cg2(sB_u32 + slot * C::kBBytes, &tmap_b, mapa_rank(smem_u32(&bfull[slot]), 0), 0,
+                      (int)crank * (BN / kCS), e * cblocks + cb);
+    else
+      tma_load_3d(sB_u32 + slot * C::kBBytes, &tmap_b, &bfull[slot], 0, 0, e * cblocks + cb);
+  };
   if (warp < kProdWarpsW) {
     // ------------------------------------------------------------ producers
     // (TMA windows: thread 0 alone -- an idle thread must not trail the
     // barrier phases it waits on)
-    if (tma_win && threadIdx.x != 0) goto done;
+    // A resident filter is loaded by all four producer warps (lane 0 of warp
+    // w: K-block slots w, w + 4, ...): one thread's TMA loads complete about
+    // one per 450 cycles whatever their size (tools/micro/tma_rate.cu), so a
+    // single issuer would stretch the first unit by RS * cblocks * 450 cycles.
+    if (tma_win && pl.resident && lane == 0 && cid < a.units && !kFilter1) {
+      if (warp != 0)   // (warp 0 issues its slots after each window, below)
+        for (int slot = warp; slot < cblocks * RS; slot += kProdWarpsW) load_filter_slot(slot);
+    }
+    // TMA windows: lane 0 of warps 0 .. win_split-1 each load a share of the
+    // window's rows (one thread's TMA loads are served one after another)
+    if (tma_win && !(lane == 0 && warp < a.win_split)) goto done;
     {
       int ws = 0, bs = 0;
       uint32_t wph = 0, bph = 0;
@@ -308,17 +375,22 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
         const int32_t rows = ut.cnt == 2 ? a.WR2 : a.WR;   // window of this CTA's tiles
         // pair: shift the window so this CTA's first tile starts at the leader's column
         const int32_t shift = kCS > 1 ? (win_tile(a, ut.lead).rel0 - tw.rel0) * 128 : 0;
+        // L2 prefetch of the NEXT unit's window (all channel blocks): its TMA
+        // loads then hit L2 instead of waiting on HBM behind this unit's MMAs
+        if (threadIdx.x == 0 && u + ncl < a.units && !kNoPrefetch) prefetch_window(a, unit_tiles<kCS>(a, u + ncl, crank));
         for (int cb = 0; cb < cblocks; ++cb) {
           mbar_wait(&wempty[ws], wph ^ 1);
+          if (threadIdx.x == 0 && uk < 4 && cb < 2) TRACE(64 + uk * 2 + cb);
           const uint32_t wbase = sWin_u32 + ws * pl.win_stage + a.win_lead;
           if (tma_win) {
             // completion of both CTAs' windows is counted at the leader
-            if (crank == 0) mbar_arrive_expect_tx(&wfull[ws], kCS * rows * row_bytes);
+            if (crank == 0 && threadIdx.x == 0) mbar_arrive_expect_tx(&wfull[ws], kCS * rows * row_bytes);
             const uint32_t bar = kCS > 1 ? mapa_rank(smem_u32(&wfull[ws]), 0) : smem_u32(&wfull[ws]);
-            // one box per image block the window rows [g0, g0 + rows) touch
-            int32_t g = tw.g0;
-            const int32_t gend = g + rows;
-            uint32_t dst = wbase + shift;
+            // this thread's share of the rows; one box per image block it touches
+            const int32_t r0 = rows * warp / a.win_split, r1 = rows * (warp + 1) / a.win_split;
+            int32_t g = tw.g0 + r0;
+            const int32_t gend = tw.g0 + r1;
+            uint32_t dst = wbase + shift + r0 * row_bytes;
             while (g < gend) {
               const int32_t n = g / a.Hz;
               const int32_t r = g - n * a.Hz;          // row inside the image block
@@ -359,12 +431,7 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
             if (uk == 0)
               for (int e = 0; e < RS; ++e) {
                 const int slot = cb * RS + e;
-                if (crank == 0) mbar_arrive_expect_tx(&bfull[slot], kCS * C::kBBytes);
-                if constexpr (kCS == 2)
-                  tma_load_3d_cg2(sB_u32 + slot * C::kBBytes, &tmap_b, mapa_rank(smem_u32(&bfull[slot]), 0), 0,
-                                  (int)crank * (BN / kCS), e * cblocks + cb);
-                else
-                  tma_load_3d(sB_u32 + slot * C::kBBytes, &tmap_b, &bfull[slot], 0, 0, e * cblocks + cb);
+                if (!tma_win || kFilter1 || slot % kProdWarpsW == 0) load_filter_slot(slot);
               }
           } else if (threadIdx.x == 0) {
             for (int e = 0; e < RS; ++e) {
@@ -408,6 +475,7 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
       const uint32_t d = tmem_base + as * C::kAccStage;
       for (int cb = 0; cb < cblocks; ++cb) {
         mbar_wait(&wfull[ws], wph);
+        if (lane == 0 && uk < 4 && cb < 2) TRACE(72 + uk * 2 + cb);
         tc_fence_after();
         // tile i of the unit: 128 window rows after tile i - 1
         uint64_t adesc[kMT];
@@ -463,6 +531,7 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
           __syncwarp();
           if (++bs == pl.bslots) { bs = 0; bph ^= 1; }
         }
+        if (lane == 0 && uk < 4 && cb < 2) TRACE(80 + uk * 2 + cb);
         if (++ws == pl.wstages) { ws = 0; wph ^= 1; }
       }
       if (lane == 0 && uk < 8) TRACE(2 + uk);
@@ -633,6 +702,9 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
 done:
   tc_fence_before();
   __syncthreads();
+#ifdef ICV_TRACE
+  if (threadIdx.x == 0) { g_icv_trace[blockIdx.x][60] = (unsigned long long)clock64(); TRACE(61); }
+#endif
   if constexpr (kCS > 1) cluster_sync_all();   // no peer still signals, writes or reads TMEM
   if (warp == kMmaWarpW) {
     tc_fence_after();
@@ -783,6 +855,10 @@ int launch_win(const ConvArgs& c, const WinGeom& w, cudaStream_t st, bool reside
     std::memset(&maps, 0, sizeof(maps));   // unused (cp.async windows)
   }
   a.zero_known = c.zero_known;
+  a.win_split = env_int("ICV_WIN_SPLIT", 2);
+  if (a.win_split < 1) a.win_split = 1;
+  if (a.win_split > kProdWarpsW) a.win_split = kProdWarpsW;
+  if (a.win_split > w.WR) a.win_split = w.WR;
   a.H = (int32_t)c.g.H; a.W = (int32_t)c.g.W; a.OH = (int32_t)c.g.OH; a.OW = (int32_t)c.g.OW;
   a.S = c.g.S; a.DY = c.g.DY; a.DX = c.g.DX; a.PT = c.g.PT; a.PL = c.g.PL;
   a.Zc = w.Zc; a.Zr = w.Zr; a.Hz = w.Hz; a.Wp = w.Wp; a.WR = w.WR; a.WR2 = w.WR2;
@@ -899,6 +975,9 @@ bool win_kernel_eligible(const ConvArgs& c) {
   if (c.L.n_pad > kMaxBias) return false;
   if (c.P >= (int64_t(1) << 31)) return false;
   if ((reinterpret_cast<uintptr_t>(c.x) & 15) != 0) return false;
+  // 1x1 layers have no tap re-reads for the window to save; measured slower
+  // than the gather kernel on every ResNet-50 1x1 (profiles/r01d_cfg5_layers.json)
+  if (c.g.R * c.g.S == 1 && !(env && env[0] == '1')) return false;
   WinGeom w;
   if (!win_geom(c, &w)) return false;
   const char* mu = getenv("ICV_WIN_MIN_USEFUL");

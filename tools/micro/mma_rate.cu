@@ -7,11 +7,6 @@
 #include "../../paper_1907_02129_b200/csrc/sm100_ptx.cuh"
 using namespace icv;
 
-__device__ __forceinline__ bool elect_one() {
-  uint32_t pred = 0;
-  asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(pred));
-  return pred != 0;
-}
 
 template <bool kI8, int N, int kVar>
 __global__ void __launch_bounds__(128, 1) mma_rate(int iters, unsigned long long* out) {

@@ -39,11 +39,6 @@ __global__ void tma_kernel(const __grid_constant__ CUtensorMap tm_shared, const 
   cyc[blockIdx.x] = t1 - t0;
 }
 
-__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
-      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2) : "memory");
-}
 
 // 3D boxes {64 elems, rows, depth}: depth consecutive 128-byte K blocks per load.
 // issuers: number of warps issuing (each warp lane 0 owns stages w, w+issuers, ...)
