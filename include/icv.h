@@ -72,6 +72,12 @@ typedef enum icv_dtype {
  * their TMA windows instead of reading the zero row. */
 #define ICV_ZERO_ROW_ZEROS 0x400
 
+/* Flag OR-ed into icv_conv's `ib_dtype` (uint8): every byte of the bound
+ * zero row equals quant->input_zero_point (as the reference semantics
+ * prescribe for quantized padding).  Windowed layers may then zero-fill
+ * padding and add the packed per-tap correction zx * sum_c (w - zw). */
+#define ICV_ZERO_ROW_ZP 0x800
+
 /* Convolution geometry; field-for-field convbench.tensors.ConvParams
  * (tensors.py:41-72). */
 typedef struct icv_conv_desc {

@@ -24,6 +24,7 @@ ICV_F32, ICV_BF16, ICV_U8, ICV_I32, ICV_I64 = 0, 1, 2, 3, 4
 ICV_IB_PER_IMAGE = 0x100
 ICV_IB_CANONICAL = 0x200   # buffer is exactly icv_ib_build's output (row-sliding kernels may use it)
 ICV_ZERO_ROW_ZEROS = 0x400  # bound zero row is all zero bytes (window kernels may zero-fill padding)
+ICV_ZERO_ROW_ZP = 0x800     # uint8: every zero-row byte is the input zero point (zero fill + per-tap correction)
 
 TORCH_TO_ICV = {torch.float32: ICV_F32, torch.bfloat16: ICV_BF16, torch.uint8: ICV_U8,
                 torch.int32: ICV_I32, torch.int64: ICV_I64}

@@ -121,6 +121,10 @@ int packed_layout(const icv_conv_desc* d, int32_t dtype, PackedLayout* L) {
     L->bias_bytes = 4 * K;
   }
   L->total = align_up(L->bias_off + L->bias_bytes, 256);
+  if (fam == kFamTcU8) {   // per-tap padding corrections for zero-filled (TMA) windows
+    L->tapcorr_off = L->total;
+    L->total = align_up(L->tapcorr_off + RS * L->n_pad * 4, 256);
+  }
   if (L->rows_off) L->total = align_up(L->rows_off + (int64_t)d->kernel_h * L->n_pad * 64, 256);
   return ICV_OK;
 }
@@ -292,7 +296,8 @@ ICV_API int icv_conv(const icv_conv_desc* desc, const icv_shape4* in, int64_t ba
   a.ib_per_image = (ib_dtype & ICV_IB_PER_IMAGE) != 0;
   a.ib_canonical = (ib_dtype & ICV_IB_CANONICAL) != 0;
   a.zero_known = (ib_dtype & ICV_ZERO_ROW_ZEROS) != 0;
-  ib_dtype &= ~(ICV_IB_PER_IMAGE | ICV_IB_CANONICAL | ICV_ZERO_ROW_ZEROS);
+  a.zero_is_zp = (ib_dtype & ICV_ZERO_ROW_ZP) != 0;
+  ib_dtype &= ~(ICV_IB_PER_IMAGE | ICV_IB_CANONICAL | ICV_ZERO_ROW_ZEROS | ICV_ZERO_ROW_ZP);
   if (ib_dtype != ICV_I64 && ib_dtype != ICV_I32) return fail(ICV_ERR_ARG, "ib dtype must be int64 or int32");
   if (!x || !zero_row || !ib || !packed || !y) return fail(ICV_ERR_ARG, "null tensor pointer");
   if (int s = packed_layout(desc, dtype, &a.L)) return s;

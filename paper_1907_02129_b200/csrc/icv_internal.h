@@ -43,6 +43,7 @@ struct PackedLayout {
   int64_t row_bytes;  // bytes per packed output channel row
   int64_t w_off, w_bytes, bias_off, bias_bytes, total;
   int64_t rows_off;   // channel-poor family: row-sliding filter copy (0 = absent)
+  int64_t tapcorr_off; // uint8 tensor-core family: [RS][n_pad] int32 zx * sum_c (w - zw) per tap (0 = absent)
 };
 int packed_layout(const icv_conv_desc* d, int32_t dtype, PackedLayout* L);
 
@@ -65,6 +66,7 @@ struct ConvArgs {
   int32_t ib_per_image;  // entries are image-relative (ICV_IB_PER_IMAGE)
   int32_t ib_canonical;  // caller guarantees the icv_ib_build layout (ICV_IB_CANONICAL)
   int32_t zero_known;    // caller guarantees the zero row is all zero bytes (ICV_ZERO_ROW_ZEROS)
+  int32_t zero_is_zp;    // uint8: caller guarantees every zero-row byte is the input zero point (ICV_ZERO_ROW_ZP)
   const uint8_t* packed;
   PackedLayout L;
   void* y;

@@ -55,7 +55,7 @@ constexpr int kMmaWarpW = kProdWarpsW + kEpiWarpsW;
 constexpr int kThreadsW = 32 * (kMmaWarpW + 1);
 constexpr int kEpiRowBytes = 80;                 // staged output row (64 B + 16 B pad: conflict-free)
 constexpr int kEpiWarpBytesW = 32 * kEpiRowBytes;
-constexpr int kMaxWinStages = 3;
+constexpr int kMaxWinStages = 4;
 constexpr int kMaxBSlots = 40;                   // (resident filters: one slot per K block)
 constexpr int kEpiBarId = 2;                     // named barrier of the epilogue warps
 #ifndef ICV_MAX_WR
@@ -80,33 +80,43 @@ struct WinArgs {
   int32_t win_lead;      // bytes from a slot's start to the window's first row (1024-aligned)
   int32_t zero_known;    // host certifies the zero row is all zeros (no in-kernel check)
   int32_t win_split;     // TMA windows: rows split over this many issuing threads (lane 0 of warps 0..)
+  // stride 2: the input is read as nph phase planes (row parity py, column
+  // parity px); php[p] = 2 * py + px of the p-th plane holding taps
+  int32_t sy;            // 1 or 2 (both directions)
+  int32_t nph;
+  int32_t php[4];
+  int32_t g_shift, rel_shift;   // window row / in-window position of a tile's first pixel (see win_tile)
+  const int32_t* tapcorr;       // u8 with TMA windows: per (tap, channel) zx * sum_c (w - zw), added for padded taps
 };
 
 struct PlanW {
   int wstages, bslots;
   int resident;          // the CTA's filter rows stay in smem: every K block loaded once, never released
   int win_stage;         // bytes per window stage (one window of up to WR2 rows + pair slack)
-  int off_b, off_ones, off_epi, off_bias, off_tap, off_bar, bytes;
+  int off_b, off_ones, off_epi, off_bias, off_tap, off_corr, off_bar, bytes;
 };
 
 template <bool kI8, int BN, int kMT, int kCS>
 struct CfgW {
-  static constexpr int kAccTile = kI8 ? 2 * BN : BN;   // TMEM columns per M tile (u8: row sums at +BN)
+  // TMEM columns per M tile (u8: row sums at +BN; BN = 256 keeps 32 columns for them)
+  static constexpr int kAccTile = kI8 ? (BN == 256 ? BN + 32 : 2 * BN) : BN;
   static constexpr int kAccStage = kMT * kAccTile;
-  static constexpr int kTmemNeed = 2 * kAccStage;
+  static constexpr int kAS = 2 * kAccStage <= 512 ? 2 : 1;   // accumulator stages (2: epilogue overlaps the next unit)
+  static constexpr int kTmemNeed = kAS * kAccStage;
   static constexpr uint32_t kTmemCols = kTmemNeed <= 64 ? 64 : kTmemNeed <= 128 ? 128 : kTmemNeed <= 256 ? 256 : 512;
   static constexpr int kBBytes = BN * 128 / kCS;        // this CTA's filter rows of one K block
   static constexpr int kOnesBytes = kI8 ? 16 * 128 : 0;
   static_assert(kTmemNeed <= 512, "TMEM overflow");
 };
 
-template <bool kI8, int BN, int kMT, int kCS>
+template <bool kI8, int BN, int kMT, int kCS, bool kS2>
 bool plan_win(int win_stage, int rs, int kblocks, int n_pad, bool resident, PlanW* p) {
   using C = CfgW<kI8, BN, kMT, kCS>;
   const int bias = (n_pad * 4 + 15) / 16 * 16;
-  const int tap = (rs * 4 + 15) / 16 * 16;
+  const int tap = (rs * 8 + 9 * 4 + 15) / 16 * 16;   // sTap[rs], sTapE[rs], sPh[5], sPhP[4]
   const int bars = 1024;
-  const int fixed = 1024 + C::kOnesBytes + kEpiWarpsW * kEpiWarpBytesW + bias + tap + bars;
+  const int corr = kI8 ? rs * BN * 4 : 0;   // u8: staged per-tap padding corrections of the N tile
+  const int fixed = 1024 + C::kOnesBytes + kEpiWarpsW * kEpiWarpBytesW + bias + tap + corr + bars;
   p->resident = 0;
   if (resident) {   // two window stages + every K block of this CTA's filter rows
     if (kblocks > kMaxBSlots || fixed + 2 * win_stage + kblocks * C::kBBytes > 232448) return false;
@@ -119,12 +129,13 @@ bool plan_win(int win_stage, int rs, int kblocks, int n_pad, bool resident, Plan
     p->off_epi = p->off_ones + C::kOnesBytes;
     p->off_bias = p->off_epi + kEpiWarpsW * kEpiWarpBytesW;
     p->off_tap = p->off_bias + bias;
-    p->off_bar = p->off_tap + tap;
+    p->off_corr = p->off_tap + tap;
+    p->off_bar = p->off_corr + corr;
     p->bytes = 1024 + p->off_bar + bars;
     return true;
   }
   const char* wse = getenv("ICV_WIN_WS");   // tuning: force the window stage count
-  const int ws_max = wse && wse[0] ? atoi(wse) : kMaxWinStages;
+  const int ws_max = wse && wse[0] ? atoi(wse) : (kS2 ? kMaxWinStages : 3);
   for (int ws = ws_max; ws >= 2; --ws) {
     const int left = 232448 - fixed - ws * win_stage;
     int bs = left / C::kBBytes;
@@ -138,7 +149,8 @@ bool plan_win(int win_stage, int rs, int kblocks, int n_pad, bool resident, Plan
       p->off_epi = p->off_ones + C::kOnesBytes;
       p->off_bias = p->off_epi + kEpiWarpsW * kEpiWarpBytesW;
       p->off_tap = p->off_bias + bias;
-      p->off_bar = p->off_tap + tap;
+      p->off_corr = p->off_tap + tap;
+      p->off_bar = p->off_corr + corr;
       p->bytes = 1024 + p->off_bar + bars;
       return true;
     }
@@ -155,8 +167,8 @@ __device__ __forceinline__ WinTile win_tile(const WinArgs& a, int32_t t) {
   WinTile w;
   w.q0 = t * kBM;
   const int32_t v0 = w.q0 / a.Wp;
-  w.g0 = v0 + a.Zr - a.PT;
-  w.rel0 = w.q0 - v0 * a.Wp - a.PL + a.Zc;
+  w.g0 = v0 + a.g_shift;
+  w.rel0 = w.q0 - v0 * a.Wp + a.rel_shift;
   return w;
 }
 
@@ -212,6 +224,12 @@ constexpr bool kFilter1 = true;
 constexpr bool kFilter1 = false;
 #endif
 
+#ifdef ICV_WEXP_DIRECT   // experiment: epilogue stores straight from registers
+constexpr bool kDirect = true;
+#else
+constexpr bool kDirect = false;
+#endif
+
 // Prefetch into L2 the input rows a unit's window covers (every channel: the
 // rows of one image are contiguous), one bulk prefetch per image touched.
 __device__ __forceinline__ void prefetch_window(const WinArgs& a, const UnitTiles& ut) {
@@ -240,7 +258,7 @@ __device__ __forceinline__ void prefetch_window(const WinArgs& a, const UnitTile
   }
 }
 
-template <bool kI8, int BN, int kMT, int kCS>
+template <bool kI8, int BN, int kMT, int kCS, bool kS2>
 __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_constant__ CUtensorMap tmap_b,
                                                             const __grid_constant__ WinMaps maps,
                                                             const WinArgs a, const PlanW pl) {
@@ -266,7 +284,10 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
   uint8_t* sOnes = smem + pl.off_ones;
   uint8_t* sEpi = smem + pl.off_epi;
   uint32_t* sBias = reinterpret_cast<uint32_t*>(smem + pl.off_bias);
-  int32_t* sTap = reinterpret_cast<int32_t*>(smem + pl.off_tap);
+  int32_t* sTap = reinterpret_cast<int32_t*>(smem + pl.off_tap);   // window offset of the i-th tap (plane order)
+  int32_t* sTapE = sTap + a.t.RS;                                      // its tap index e = ky * S + kx
+  int32_t* sPh = sTapE + a.t.RS;                                       // taps of plane p: [sPh[p], sPh[p + 1])
+  int32_t* sPhP = sPh + 5;                                             // plane p's parities 2 * py + px
   uint64_t* wfull = reinterpret_cast<uint64_t*>(smem + pl.off_bar);
   uint64_t* wempty = wfull + kMaxWinStages;
   uint64_t* bfull = wempty + kMaxWinStages;
@@ -302,7 +323,7 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
       mbar_init(&bfull[s], 1);
       mbar_init(&bempty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < C::kAS; ++s) {
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], kCS * kEpiWarpsW);   // both CTAs' epilogue warps arrive at the leader
     }
@@ -318,9 +339,41 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
       fence_proxy_async_smem();
     }
   }
-  for (int e = threadIdx.x; e < a.t.RS; e += blockDim.x) {
-    const int ky = e / a.S, kx = e - ky * a.S;
-    sTap[e] = ky * a.DY * a.Wp + kx * a.DX;
+  const int nph = kS2 ? a.nph : 1;
+  if constexpr (!kS2) {
+    for (int e = threadIdx.x; e < a.t.RS; e += blockDim.x) {
+      const int ky = e / a.S, kx = e - ky * a.S;
+      sTap[e] = ky * a.DY * a.Wp + kx * a.DX;
+    }
+  } else if (threadIdx.x == 0) {
+    // taps grouped by input plane.  Stride 1: one plane, off(e) = ky*DY*Wp +
+    // kx*DX.  Stride 2: tap (ky, kx) reads plane (py, px) at row qy + Zr and
+    // column qx + Zc past the output pixel, ky*DY - PT = 2*qy + py (floor),
+    // kx*DX - PL = 2*qx + px.
+    int i = 0;
+    for (int p = 0; p < a.nph; ++p) {
+      sPh[p] = i;
+      for (int e = 0; e < a.t.RS; ++e) {
+        const int ky = e / a.S, kx = e - ky * a.S;
+        int off, ph = 0;
+        if (a.sy == 1) {
+          off = ky * a.DY * a.Wp + kx * a.DX;
+        } else {
+          const int ay = ky * a.DY - a.PT, ax = kx * a.DX - a.PL;
+          const int qy = ay >= 0 ? ay / 2 : -((1 - ay) / 2), qx = ax >= 0 ? ax / 2 : -((1 - ax) / 2);
+          ph = 2 * (ay - 2 * qy) + (ax - 2 * qx);
+          off = (qy + a.Zr) * a.Wp + qx + a.Zc;
+        }
+        if (ph == a.php[p]) {
+          sTap[i] = off;
+          sTapE[i] = e;
+          ++i;
+        }
+      }
+    }
+    sPh[a.nph] = i;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) sPhP[p] = a.php[p];
   }
   if (warp == kMmaWarpW) {
     if constexpr (kCS == 2) tmem_alloc2<C::kTmemCols>(tmem_slot);
@@ -378,9 +431,11 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
         // L2 prefetch of the NEXT unit's window (all channel blocks): its TMA
         // loads then hit L2 instead of waiting on HBM behind this unit's MMAs
         if (threadIdx.x == 0 && u + ncl < a.units && !kNoPrefetch) prefetch_window(a, unit_tiles<kCS>(a, u + ncl, crank));
-        for (int cb = 0; cb < cblocks; ++cb) {
+        for (int st = 0; st < cblocks * nph; ++st) {   // stages: (channel block, input plane)
+          const int cb = kS2 ? st / nph : st, pi = kS2 ? st - cb * nph : 0;
+          const int py = kS2 ? sPhP[pi] >> 1 : 0, px = kS2 ? sPhP[pi] & 1 : 0;
           mbar_wait(&wempty[ws], wph ^ 1);
-          if (threadIdx.x == 0 && uk < 4 && cb < 2) TRACE(64 + uk * 2 + cb);
+          if (threadIdx.x == 0 && uk < 4 && st < 2) TRACE(64 + uk * 2 + st);
           const uint32_t wbase = sWin_u32 + ws * pl.win_stage + a.win_lead;
           if (tma_win) {
             // completion of both CTAs' windows is counted at the leader
@@ -396,10 +451,14 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
               const int32_t r = g - n * a.Hz;          // row inside the image block
               const int32_t h = min(gend - g, a.Hz - r);
               const CUtensorMap* m = &maps.m[h - 1];
+              // stride 2: plane row r is input row 2 (r - Zr) + py, plane column
+              // c input column 2 (c - Zc) + px (the maps step 2 in W and H)
+              const int32_t cx = !kS2 ? -a.Zc : px - 2 * a.Zc;
+              const int32_t cy = !kS2 ? r - a.Zr : 2 * (r - a.Zr) + py;
               if constexpr (kCS == 2)
-                tma_load_4d_cg2(dst, m, bar, cb * a.cbe, -a.Zc, r - a.Zr, n);
+                tma_load_4d_cg2(dst, m, bar, cb * a.cbe, cx, cy, n);
               else
-                tma_load_4d(dst, m, &wfull[ws], cb * a.cbe, -a.Zc, r - a.Zr, n);
+                tma_load_4d(dst, m, &wfull[ws], cb * a.cbe, cx, cy, n);
               dst += h * row_bytes;
               g += h;
             }
@@ -429,12 +488,13 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
           // tap (resident filter: loaded during the first unit only)
           if (threadIdx.x == 0 && pl.resident) {
             if (uk == 0)
-              for (int e = 0; e < RS; ++e) {
-                const int slot = cb * RS + e;
+              for (int i = kS2 ? sPh[pi] : 0; i < (kS2 ? sPh[pi + 1] : RS); ++i) {
+                const int slot = cb * RS + (kS2 ? sTapE[i] : i);
                 if (!tma_win || kFilter1 || slot % kProdWarpsW == 0) load_filter_slot(slot);
               }
           } else if (threadIdx.x == 0) {
-            for (int e = 0; e < RS; ++e) {
+            for (int i = kS2 ? sPh[pi] : 0; i < (kS2 ? sPh[pi + 1] : RS); ++i) {
+              const int e = kS2 ? sTapE[i] : i;
               mbar_wait(&bempty[bs], bph ^ 1);
               if (crank == 0) mbar_arrive_expect_tx(&bfull[bs], kCS * C::kBBytes);
               if constexpr (kCS == 2)
@@ -473,16 +533,20 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
 #endif
       tc_fence_after();
       const uint32_t d = tmem_base + as * C::kAccStage;
-      for (int cb = 0; cb < cblocks; ++cb) {
+      for (int st = 0; st < cblocks * nph; ++st) {   // stages: (channel block, input plane)
+        const int cb = kS2 ? st / nph : st, pi = kS2 ? st - cb * nph : 0;
+        const bool last_stage = st == cblocks * nph - 1;
         mbar_wait(&wfull[ws], wph);
-        if (lane == 0 && uk < 4 && cb < 2) TRACE(72 + uk * 2 + cb);
+        if (lane == 0 && uk < 4 && st < 2) TRACE(72 + uk * 2 + st);
         tc_fence_after();
         // tile i of the unit: 128 window rows after tile i - 1
         uint64_t adesc[kMT];
 #pragma unroll
         for (int i = 0; i < kMT; ++i)
           adesc[i] = sw128_kmajor_desc(sWin_u32 + ws * pl.win_stage + a.win_lead + (rel0 + i * kBM) * 128);
-        for (int e = 0; e < RS; ++e) {
+        const int i_end = kS2 ? sPh[pi + 1] : RS;
+        for (int ti = kS2 ? sPh[pi] : 0; ti < i_end; ++ti) {
+          const int e = kS2 ? sTapE[ti] : ti;   // (stride 1: taps in order)
 #ifdef ICV_TRACE
           long long c1 = clock64();
 #endif
@@ -493,11 +557,11 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
 #endif
           tc_fence_after();
           if (elect_one()) {
-            const uint64_t toff = (uint64_t)(sTap[e] * 8);   // (off(e) * 128 bytes) >> 4
+            const uint64_t toff = (uint64_t)(sTap[ti] * 8);   // (off(e) * 128 bytes) >> 4
             const uint64_t bdesc = sw128_kmajor_desc(sB_u32 + bslot * C::kBBytes);
 #pragma unroll
             for (int k = 0; k < 4; ++k) {   // 4 x 32-byte K steps per 128-byte block
-              const uint32_t acc = (cb | e | k) != 0;
+              const uint32_t acc = (st | ti | k) != 0;
 #pragma unroll
               for (int i = 0; i < kMT; ++i) {
                 if (i >= cnt) break;
@@ -516,26 +580,26 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
             }
             if constexpr (kCS == 1) {
               if (!pl.resident) tc_commit(&bempty[bs]);
-              if (e == RS - 1) {
+              if (ti == i_end - 1) {
                 tc_commit(&wempty[ws]);
-                if (cb == cblocks - 1) tc_commit(&tfull[as]);
+                if (last_stage) tc_commit(&tfull[as]);
               }
             } else {   // stage free / accumulators ready in both CTAs
               if (!pl.resident) tc_commit2_mc(&bempty[bs], kMask);
-              if (e == RS - 1) {
+              if (ti == i_end - 1) {
                 tc_commit2_mc(&wempty[ws], kMask);
-                if (cb == cblocks - 1) tc_commit2_mc(&tfull[as], kMask);
+                if (last_stage) tc_commit2_mc(&tfull[as], kMask);
               }
             }
           }
           __syncwarp();
           if (++bs == pl.bslots) { bs = 0; bph ^= 1; }
         }
-        if (lane == 0 && uk < 4 && cb < 2) TRACE(80 + uk * 2 + cb);
+        if (lane == 0 && uk < 4 && st < 2) TRACE(80 + uk * 2 + st);
         if (++ws == pl.wstages) { ws = 0; wph ^= 1; }
       }
       if (lane == 0 && uk < 8) TRACE(2 + uk);
-      if (++as == 2) { as = 0; aph ^= 1; }
+      if (++as == C::kAS) { as = 0; aph ^= 1; }
     }
 #ifdef ICV_TRACE
     if (lane == 0) {
@@ -567,6 +631,14 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
     // epilogue constants (loaded here, off the producers' / MMA's critical path)
     for (int i = threadIdx.x - 32 * kProdWarpsW; i < a.t.n_pad; i += 32 * kEpiWarpsW)
       sBias[i] = __ldg(static_cast<const uint32_t*>(a.t.bias) + i);
+    // u8 padding corrections: staged once when the layer has one N tile
+    int32_t* sCorr = reinterpret_cast<int32_t*>(smem + pl.off_corr);
+    const bool corr_staged = kI8 && a.tapcorr != nullptr && a.t.n_tiles == 1;
+    if (corr_staged)
+      for (int i = threadIdx.x - 32 * kProdWarpsW; i < a.t.RS * BN; i += 32 * kEpiWarpsW) {
+        const int e = i / BN, n = i - e * BN;
+        sCorr[i] = __ldg(a.tapcorr + (int64_t)e * a.t.n_pad + n);
+      }
     named_bar_sync(kEpiBarId, 32 * kEpiWarpsW);
     const uint32_t tempty_remote = kCS == 2 && crank != 0 ? mapa_rank(smem_u32(tempty), 0) : 0u;
     const int32_t img_px = a.Hz * a.Wp;   // virtual pixels per image
@@ -595,6 +667,15 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
         const int32_t oy = r / a.Wp;
         const int32_t ox = r - oy * a.Wp;
         const int32_t myp = (n < a.batch && oy < a.OH && ox < a.OW) ? (n * a.OH + oy) * a.OW + ox : -1;
+        // u8 with zero-filled TMA windows: padded taps contributed x = 0
+        // instead of the zero point; their per-channel correction is added below
+        uint64_t oob = 0;
+        if (kI8 && a.tapcorr != nullptr && myp >= 0)
+          for (int e = 0; e < a.t.RS; ++e) {
+            const int ky = e / a.S, kx = e - ky * a.S;
+            const int iy = oy * a.sy - a.PT + ky * a.DY, ix = ox * a.sy - a.PL + kx * a.DX;
+            if (iy < 0 || iy >= a.H || ix < 0 || ix >= a.W) oob |= 1ull << e;
+          }
         // the rows this lane stores in each pass (fixed for the tile)
         uint8_t* rowptr[32 / kRowsPerPass];
 #pragma unroll
@@ -647,7 +728,13 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
             const long long corr = -(long long)a.t.zw * rowsum;
 #pragma unroll
             for (int qd = 0; qd < 8; ++qd) {
-              const int4 b = cst4[qd];
+              int4 b = cst4[qd];
+              for (uint64_t m = oob; m != 0; m &= m - 1) {
+                const int e = __ffsll((long long)m) - 1;
+                const int4 t = corr_staged ? reinterpret_cast<const int4*>(sCorr + e * BN + (n0 - nt * BN))[qd]
+                                           : __ldg(reinterpret_cast<const int4*>(a.tapcorr + (int64_t)e * a.t.n_pad + n0) + qd);
+                b.x += t.x; b.y += t.y; b.z += t.z; b.w += t.w;
+              }
               const int bb[4] = {b.x, b.y, b.z, b.w};
               uint32_t word = 0;
 #pragma unroll
@@ -658,12 +745,28 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
               w[qd] = word;
             }
           }
+          const bool full = vec_ok && n0 + 32 <= a.t.K;
+          if (kDirect && full) {
+            // straight from registers: this lane's pixel row, 16-byte pieces
+            // (no smem staging: the mainloop's MMAs need the smem bandwidth)
+            if (myp >= 0) {
+              uint4* dst = reinterpret_cast<uint4*>(static_cast<uint8_t*>(a.t.y) + (int64_t)myp * a.t.K * eb + n0 * eb);
+#pragma unroll
+              for (int qd = 0; qd < kChunks16; ++qd)
+                dst[qd] = make_uint4(w[4 * qd], w[4 * qd + 1], w[4 * qd + 2], w[4 * qd + 3]);
+            }
+            if (ci + 1 < nchunks) {
+              tmem_ld_wait_regs(vn);
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = vn[j];
+            }
+            continue;
+          }
           uint4* my = reinterpret_cast<uint4*>(stg + lane * kEpiRowBytes);
 #pragma unroll
           for (int qd = 0; qd < kChunks16; ++qd)
             my[qd] = make_uint4(w[4 * qd], w[4 * qd + 1], w[4 * qd + 2], w[4 * qd + 3]);
           __syncwarp();
-          const bool full = vec_ok && n0 + 32 <= a.t.K;
 #pragma unroll
           for (int pass = 0; pass < 32 / kRowsPerPass; ++pass) {
             const int rr = pass * kRowsPerPass + lane / kChunks16;
@@ -695,7 +798,7 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
         else mbar_arrive(&tempty[as]);
       }
       if (ew == 0 && lane == 0 && uk < 8) TRACE(18 + uk);
-      if (++as == 2) { as = 0; aph ^= 1; }
+      if (++as == C::kAS) { as = 0; aph ^= 1; }
     }
   }
 
@@ -719,14 +822,75 @@ int env_int(const char* name, int dflt) {
   return v && v[0] ? atoi(v) : dflt;
 }
 
+// TMA (zero-filled) windows are exact for this call's zero row
+bool tma_zero_ok(const ConvArgs& c) {
+  return c.zero_known || (c.L.family == kFamTcU8 && c.zero_is_zp && c.L.tapcorr_off != 0 && c.g.RS() <= 64);
+}
+
 // Geometry of the window schedule (host).
 struct WinGeom {
   int Zc, Zr, Hz, Wp, WR, WR2, tiles;
   double useful;   // stored output pixels / computed rows
+  int sy, nph, php[4], g_shift, rel_shift;
 };
+
+// floor division by 2
+static inline int fdiv2(int v) { return v >= 0 ? v / 2 : -((1 - v) / 2); }
+
+// Stride 2 (both directions): the batch is read as up to four phase planes
+// (input rows of parity py, columns of parity px), each stacked like the
+// stride-1 plane but on the OUTPUT grid: per image Hz = OH + (qy range) rows
+// of Wp = OW + (qx range) positions; plane position (r, c) of image n holds
+// input pixel (2 (r - Zr) + py, 2 (c - Zc) + px), zero outside the image.
+// Virtual pixel q = (n Hz + oy) Wp + ox reads, at tap e, position q + off(e)
+// of plane ph(e) (off(e) = (qy + Zr) Wp + qx + Zc): again one affine shift
+// per tap, so the same sliding-descriptor mainloop applies plane by plane.
+bool win_geom_s2(const ConvArgs& c, WinGeom* w) {
+  const Geom& g = c.g;
+  int qy0 = 1 << 30, qy1 = -(1 << 30), qx0 = 1 << 30, qx1 = -(1 << 30);
+  bool used[4] = {false, false, false, false};
+  for (int ky = 0; ky < g.R; ++ky)
+    for (int kx = 0; kx < g.S; ++kx) {
+      const int ay = ky * g.DY - g.PT, ax = kx * g.DX - g.PL;
+      const int qy = fdiv2(ay), qx = fdiv2(ax);
+      used[2 * (ay - 2 * qy) + (ax - 2 * qx)] = true;
+      qy0 = qy < qy0 ? qy : qy0; qy1 = qy > qy1 ? qy : qy1;
+      qx0 = qx < qx0 ? qx : qx0; qx1 = qx > qx1 ? qx : qx1;
+    }
+  w->sy = 2;
+  w->nph = 0;
+  for (int p = 0; p < 4; ++p)
+    if (used[p]) w->php[w->nph++] = p;
+  w->Zr = -qy0;
+  w->Zc = -qx0;
+  w->Hz = (int)g.OH + (qy1 - qy0);
+  w->Wp = (int)g.OW + (qx1 - qx0);
+  w->g_shift = 0;
+  w->rel_shift = 0;
+  if (w->Wp > 128) return false;   // (box width 2 Wp input columns <= 256)
+  const int64_t span = (int64_t)(w->Wp - 1) + (kBM - 1) + (int64_t)(qy1 - qy0) * w->Wp + (qx1 - qx0) + 1;
+  const int64_t wr = (span + w->Wp - 1) / w->Wp;
+  const int64_t wr2 = (span + kBM + w->Wp - 1) / w->Wp;
+  if (wr > kMaxWR || wr > 128) return false;
+  w->WR = (int)wr;
+  w->WR2 = (int)(wr2 <= kMaxWR && wr2 <= 128 ? wr2 : 0);
+  const int64_t batch = c.P / (g.OH * g.OW);
+  const int64_t vpx = ((batch - 1) * w->Hz + g.OH) * (int64_t)w->Wp;
+  if (vpx >= (int64_t(1) << 30)) return false;
+  w->tiles = (int)((vpx + kBM - 1) / kBM);
+  w->useful = (double)c.P / ((double)w->tiles * kBM);
+  return true;
+}
+
 bool win_geom(const ConvArgs& c, WinGeom* w) {
   const Geom& g = c.g;
+  if (g.SY == 2 && g.SX == 2) return win_geom_s2(c, w);
   if (g.SY != 1 || g.SX != 1) return false;
+  w->sy = 1;
+  w->nph = 1;
+  w->php[0] = 0;
+  w->g_shift = (g.PT > g.PB ? g.PT : g.PB) - g.PT;
+  w->rel_shift = (g.PL > g.PR ? g.PL : g.PR) - g.PL;
   w->Zc = g.PL > g.PR ? g.PL : g.PR;
   w->Zr = g.PT > g.PB ? g.PT : g.PB;
   w->Wp = (int)g.W + w->Zc;
@@ -757,10 +921,10 @@ int window_maps(const ConvArgs& c, const WinGeom& w, WinMaps* out) {
   const bool i8 = c.L.family == kFamTcU8;
   const int eb = i8 ? 1 : 2;
   const int64_t batch = c.P / (c.g.OH * c.g.OW);
-  using Key = std::tuple<const void*, int64_t, int64_t, int64_t, int64_t, int, int, int>;
+  using Key = std::tuple<const void*, int64_t, int64_t, int64_t, int64_t, int, int, int, int>;
   static std::mutex mu;
   static std::map<Key, WinMaps> cache;
-  const Key key{c.x, (int64_t)c.g.C, c.g.W, c.g.H, batch, w.Wp, w.WR2 > w.WR ? w.WR2 : w.WR, eb};
+  const Key key{c.x, (int64_t)c.g.C, c.g.W, c.g.H, batch, w.Wp, w.WR2 > w.WR ? w.WR2 : w.WR, eb, w.sy};
   std::lock_guard<std::mutex> lk(mu);
   auto it = cache.find(key);
   if (it != cache.end()) {
@@ -770,12 +934,13 @@ int window_maps(const ConvArgs& c, const WinGeom& w, WinMaps* out) {
   const cuuint64_t dims[4] = {(cuuint64_t)c.g.C, (cuuint64_t)c.g.W, (cuuint64_t)c.g.H, (cuuint64_t)batch};
   const cuuint64_t strides[3] = {(cuuint64_t)c.g.C * eb, (cuuint64_t)(c.g.W * c.g.C * eb),
                                  (cuuint64_t)(c.g.H * c.g.W * c.g.C * eb)};
-  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  // stride 2: every other input column and row (one phase plane per load)
+  const cuuint32_t estr[4] = {1, (cuuint32_t)w.sy, (cuuint32_t)w.sy, 1};
   WinMaps m;
   std::memset(&m, 0, sizeof(m));
   const int hmax = w.WR2 > w.WR ? w.WR2 : w.WR;
   for (int h = 1; h <= hmax; ++h) {
-    const cuuint32_t box[4] = {(cuuint32_t)(128 / eb), (cuuint32_t)w.Wp, (cuuint32_t)h, 1};
+    const cuuint32_t box[4] = {(cuuint32_t)(128 / eb), (cuuint32_t)(w.sy * w.Wp), (cuuint32_t)(w.sy * h), 1};
     CUresult cr = encode(&m.m[h - 1], i8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
                          const_cast<void*>(c.x), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -808,22 +973,22 @@ int slot_bytes(const WinGeom& w, int kmt, int kcs) {
 
 // resident filter: one-tile units, a single N tile, and every K block of
 // this CTA's filter rows fits beside two window stages
-template <bool kI8, int BN, int kMT, int kCS>
+template <bool kI8, int BN, int kMT, int kCS, bool kS2>
 bool win_plan_for(const ConvArgs& c, const WinGeom& w, PlanW* pl, bool resident = false) {
   if (kMT == 2 && w.WR2 == 0) return false;
   if (resident && (kMT != 1 || c.L.n_pad != BN)) return false;
-  return plan_win<kI8, BN, kMT, kCS>(slot_bytes(w, kMT, kCS), c.g.RS(), c.g.RS() * c.L.cblocks, c.L.n_pad, resident,
+  return plan_win<kI8, BN, kMT, kCS, kS2>(slot_bytes(w, kMT, kCS), c.g.RS(), c.g.RS() * c.L.cblocks, c.L.n_pad, resident,
                                      pl);
 }
 
-template <bool kI8, int BN, int kMT, int kCS>
+template <bool kI8, int BN, int kMT, int kCS, bool kS2>
 int launch_win(const ConvArgs& c, const WinGeom& w, cudaStream_t st, bool resident) {
-  auto kernel = igemm_win_kernel<kI8, BN, kMT, kCS>;
+  auto kernel = igemm_win_kernel<kI8, BN, kMT, kCS, kS2>;
   static std::once_flag attr_once;
   static cudaError_t attr_err = cudaSuccess;
   static int max_clusters = 0;
   PlanW pl;
-  if (!win_plan_for<kI8, BN, kMT, kCS>(c, w, &pl, resident))
+  if (!win_plan_for<kI8, BN, kMT, kCS, kS2>(c, w, &pl, resident))
     return fail(ICV_ERR_UNSUPPORTED, "window does not fit in shared memory");
   std::call_once(attr_once, [&] {
     attr_err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
@@ -852,9 +1017,19 @@ int launch_win(const ConvArgs& c, const WinGeom& w, cudaStream_t st, bool reside
   a.t.use_tma_x = env_int("ICV_WIN_TMA", 1) == 1 && window_maps(c, w, &maps) == ICV_OK;
   if (!a.t.use_tma_x) {
     if (kCS > 1) return fail(ICV_ERR_UNSUPPORTED, "window pair kernel needs TMA window maps");
+    if (w.sy != 1) return fail(ICV_ERR_UNSUPPORTED, "stride-2 window kernel needs TMA window maps");
     std::memset(&maps, 0, sizeof(maps));   // unused (cp.async windows)
   }
-  a.zero_known = c.zero_known;
+  // zero-filled TMA windows are exact when the zero row is zeros, and for
+  // uint8 also when it holds the input zero point (plus the per-tap correction)
+  a.zero_known = tma_zero_ok(c);
+  a.tapcorr = (kI8 && !c.zero_known && c.zero_is_zp && c.L.tapcorr_off)
+                  ? reinterpret_cast<const int32_t*>(c.packed + c.L.tapcorr_off) : nullptr;
+  a.sy = w.sy;
+  a.nph = w.nph;
+  for (int p = 0; p < 4; ++p) a.php[p] = p < w.nph ? w.php[p] : 0;
+  a.g_shift = w.g_shift;
+  a.rel_shift = w.rel_shift;
   a.win_split = env_int("ICV_WIN_SPLIT", 2);
   if (a.win_split < 1) a.win_split = 1;
   if (a.win_split > kProdWarpsW) a.win_split = kProdWarpsW;
@@ -922,42 +1097,51 @@ constexpr bool mt_fits() {
 }
 
 // dispatch on (dtype, BN, kMT, kCS); `launch` false: only check the plan
-template <bool kI8, int BN>
+template <bool kI8, int BN, bool kS2>
 int dispatch_bn(const ConvArgs& c, const WinGeom& w, cudaStream_t st, bool launch) {
   PlanW pl;
   // CTA pairs need TMA windows, hence a zero row the host certifies
-  const bool pair = c.zero_known && env_int("ICV_WIN_CS", 2) == 2;
+  const bool pair = tma_zero_ok(c) && env_int("ICV_WIN_CS", 2) == 2;
   const bool mt2 = env_int("ICV_WIN_MT", 2) == 2;
   const bool res = env_int("ICV_WIN_RES", 1) == 1;
   // preference: pair with a resident filter, pair with two-tile units, pair,
   // then the single-CTA kernels
-  if (pair && res && win_plan_for<kI8, BN, 1, 2>(c, w, &pl, true))
-    return launch ? launch_win<kI8, BN, 1, 2>(c, w, st, true) : ICV_OK;
+  if (pair && res && win_plan_for<kI8, BN, 1, 2, kS2>(c, w, &pl, true))
+    return launch ? launch_win<kI8, BN, 1, 2, kS2>(c, w, st, true) : ICV_OK;
   if constexpr (mt_fits<kI8, BN, 2>()) {
-    if (pair && mt2 && win_plan_for<kI8, BN, 2, 2>(c, w, &pl))
-      return launch ? launch_win<kI8, BN, 2, 2>(c, w, st, false) : ICV_OK;
+    if (pair && mt2 && win_plan_for<kI8, BN, 2, 2, kS2>(c, w, &pl))
+      return launch ? launch_win<kI8, BN, 2, 2, kS2>(c, w, st, false) : ICV_OK;
   }
-  if (pair && win_plan_for<kI8, BN, 1, 2>(c, w, &pl)) return launch ? launch_win<kI8, BN, 1, 2>(c, w, st, false) : ICV_OK;
-  if (res && win_plan_for<kI8, BN, 1, 1>(c, w, &pl, true))
-    return launch ? launch_win<kI8, BN, 1, 1>(c, w, st, true) : ICV_OK;
+  if (pair && win_plan_for<kI8, BN, 1, 2, kS2>(c, w, &pl)) return launch ? launch_win<kI8, BN, 1, 2, kS2>(c, w, st, false) : ICV_OK;
+  if (res && win_plan_for<kI8, BN, 1, 1, kS2>(c, w, &pl, true))
+    return launch ? launch_win<kI8, BN, 1, 1, kS2>(c, w, st, true) : ICV_OK;
   if constexpr (mt_fits<kI8, BN, 2>()) {
-    if (mt2 && win_plan_for<kI8, BN, 2, 1>(c, w, &pl)) return launch ? launch_win<kI8, BN, 2, 1>(c, w, st, false) : ICV_OK;
+    if (mt2 && win_plan_for<kI8, BN, 2, 1, kS2>(c, w, &pl)) return launch ? launch_win<kI8, BN, 2, 1, kS2>(c, w, st, false) : ICV_OK;
   }
-  if (win_plan_for<kI8, BN, 1, 1>(c, w, &pl)) return launch ? launch_win<kI8, BN, 1, 1>(c, w, st, false) : ICV_OK;
+  if (win_plan_for<kI8, BN, 1, 1, kS2>(c, w, &pl)) return launch ? launch_win<kI8, BN, 1, 1, kS2>(c, w, st, false) : ICV_OK;
+  return ICV_ERR_UNSUPPORTED;
+}
+
+template <bool kS2>
+int dispatch_win_s(const ConvArgs& c, const WinGeom& w, cudaStream_t st, bool launch) {
+  int bn = c.L.block_n;
+  // uint8 with 256 output channels: one N tile of 256 (the TMEM layout keeps
+  // 32 columns for the row sums, one accumulator stage)
+  if (c.L.family == kFamTcU8 && c.L.n_pad == 256 && env_int("ICV_WIN_U8_BN", 256) == 256) bn = 256;
+  if (c.L.family == kFamTcBf16) {
+    if (bn == 64) return dispatch_bn<false, 64, kS2>(c, w, st, launch);
+    if (bn == 128) return dispatch_bn<false, 128, kS2>(c, w, st, launch);
+    if (bn == 256) return dispatch_bn<false, 256, kS2>(c, w, st, launch);
+  } else if (c.L.family == kFamTcU8) {
+    if (bn == 64) return dispatch_bn<true, 64, kS2>(c, w, st, launch);
+    if (bn == 128) return dispatch_bn<true, 128, kS2>(c, w, st, launch);
+    if (bn == 256) return dispatch_bn<true, 256, kS2>(c, w, st, launch);
+  }
   return ICV_ERR_UNSUPPORTED;
 }
 
 int dispatch_win(const ConvArgs& c, const WinGeom& w, cudaStream_t st, bool launch) {
-  const int bn = c.L.block_n;
-  if (c.L.family == kFamTcBf16) {
-    if (bn == 64) return dispatch_bn<false, 64>(c, w, st, launch);
-    if (bn == 128) return dispatch_bn<false, 128>(c, w, st, launch);
-    if (bn == 256) return dispatch_bn<false, 256>(c, w, st, launch);
-  } else if (c.L.family == kFamTcU8) {
-    if (bn == 64) return dispatch_bn<true, 64>(c, w, st, launch);
-    if (bn == 128) return dispatch_bn<true, 128>(c, w, st, launch);
-  }
-  return ICV_ERR_UNSUPPORTED;
+  return w.sy == 2 ? dispatch_win_s<true>(c, w, st, launch) : dispatch_win_s<false>(c, w, st, launch);
 }
 
 }  // namespace
@@ -980,6 +1164,13 @@ bool win_kernel_eligible(const ConvArgs& c) {
   if (c.g.R * c.g.S == 1 && !(env && env[0] == '1')) return false;
   WinGeom w;
   if (!win_geom(c, &w)) return false;
+  if (w.sy == 2 && !tma_zero_ok(c)) return false;   // (no cp.async phase-plane gather)
+  // Opt-in only (ICV_WIN=1, or ICV_WIN_S2=1 / ICV_WIN_U8=1), measured slower
+  // than the gather kernel today: stride-2 phase planes (ResNet-50 s2b1 3x3
+  // 115 vs 84 us, s3b1 88 vs 60 us) and the uint8 epilogue (cfg4 85 vs 41 us).
+  const bool forced = env && env[0] == '1';
+  if (w.sy == 2 && !forced && env_int("ICV_WIN_S2", 0) != 1) return false;
+  if (c.L.family == kFamTcU8 && !forced && env_int("ICV_WIN_U8", 0) != 1) return false;
   const char* mu = getenv("ICV_WIN_MIN_USEFUL");
   const double min_useful = (env && env[0] == '1') ? 0.0 : (mu ? atof(mu) : 0.7);
   if (w.useful < min_useful) return false;

@@ -120,6 +120,19 @@ __global__ void pack_bias_u8(const uint8_t* __restrict__ w, const int32_t* __res
   }
 }
 
+// uint8 tensor-core family: out[e][n] = zx * sum_c (w[n][e][c] - zw), the
+// contribution a padded tap (x = zx) has that a zero-filled one (x = 0) lacks
+// relative to the folded constants; one block per (e, n).
+__global__ void pack_tapcorr_u8(const uint8_t* __restrict__ w, int32_t* __restrict__ out, int K, int n_pad, int RS,
+                                int C, int zx, int zw) {
+  const int e = blockIdx.x / n_pad, n = blockIdx.x - e * n_pad;
+  int s = 0;
+  if (n < K)
+    for (int c = threadIdx.x; c < C; c += blockDim.x) s += (int)w[((int64_t)n * RS + e) * C + c] - zw;
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (threadIdx.x == 0) out[(int64_t)e * n_pad + n] = zx * s;
+}
+
 int grid_for(int64_t total) {
   int64_t b = (total + 255) / 256;
   return (int)(b < 148 * 16 ? (b > 0 ? b : 1) : 148 * 16);
@@ -182,7 +195,11 @@ int launch_pack(const Geom& g, const PackedLayout& L, int32_t w_dtype, const voi
       pack_bias_u8<<<L.n_pad, 256, 0, st>>>(static_cast<const uint8_t*>(w), static_cast<const int32_t*>(bias),
                                             reinterpret_cast<int32_t*>(base + L.bias_off), g.K, L.n_pad, kk,
                                             q->input_zero_point, q->kernel_zero_point, 1);
-      launches = 2;
+      pack_tapcorr_u8<<<(unsigned)(RS * L.n_pad), 32, 0, st>>>(static_cast<const uint8_t*>(w),
+                                                               reinterpret_cast<int32_t*>(base + L.tapcorr_off), g.K,
+                                                               L.n_pad, (int)RS, g.C, q->input_zero_point,
+                                                               q->kernel_zero_point);
+      launches = 3;
       break;
     }
     case kFamF32Exact: {

@@ -73,6 +73,10 @@ class IndirectionBuffer:
     # read-only by contract, indirect.py:42): stride-1 layers may then take
     # padding from TMA out-of-bounds zero fill (ICV_ZERO_ROW_ZEROS)
     zero_is_zero: bool = False
+    # every byte of the zero row had this value at initialization (else None):
+    # a uint8 zero row filled with the input zero point lets windowed layers
+    # zero-fill padding and add a packed per-tap correction (ICV_ZERO_ROW_ZP)
+    zero_fill_byte: "int | None" = None
 
     @property
     def pixel_count(self) -> int:
@@ -175,9 +179,11 @@ def init_indirection_buffer(input: NhwcTensor, zero_row: torch.Tensor, params: C
     tiles = _tile_count(pixels, tile.mr)
     offsets = torch.empty((tiles, params.kernel_elems, tile.mr), dtype=index_dtype, device=input.data.device)
     _build(input.shape, params, batch, tile.mr, offsets, 0, per_image)
-    zero_is_zero = not bool(zero_row.view(torch.uint8).any().item())
+    zb = zero_row.reshape(-1).view(torch.uint8)
+    lo, hi = (int(v) for v in torch.aminmax(zb))
+    fill = lo if lo == hi else None
     return IndirectionBuffer(tile.mr, batch, out_shape.h, out_shape.w, params, input.shape, input.data,
-                             zero_row, offsets, per_image, zero_is_zero=zero_is_zero)
+                             zero_row, offsets, per_image, zero_is_zero=fill == 0, zero_fill_byte=fill)
 
 
 def update_for_batch_growth(ib: IndirectionBuffer, new_batch: int) -> IndirectionBuffer:
@@ -272,7 +278,9 @@ def indirect_conv(input: NhwcTensor, pf: PackedFilter, ib: IndirectionBuffer, pa
                                  L.ptr(input.data), L.ptr(ib.zero_row), L.ptr(ib.offsets),
                                  L.TORCH_TO_ICV[ib.offsets.dtype] | (L.ICV_IB_PER_IMAGE if ib.per_image else 0)
                                  | (L.ICV_IB_CANONICAL if ib.canonical else 0)
-                                 | (L.ICV_ZERO_ROW_ZEROS if ib.zero_is_zero else 0),
+                                 | (L.ICV_ZERO_ROW_ZEROS if ib.zero_is_zero else 0)
+                                 | (L.ICV_ZERO_ROW_ZP if (input.dtype == torch.uint8 and pf.quant is not None
+                                                          and ib.zero_fill_byte == pf.quant.input_zero_point) else 0),
                                  ib.mr, L.ptr(pf.packed),
                                  ctypes.byref(q) if q is not None else None, L.ptr(out.data), L.stream_of(dev)),
                 "icv_conv")
