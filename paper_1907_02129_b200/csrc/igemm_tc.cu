@@ -64,8 +64,11 @@ struct CfgS {
 #endif
   static constexpr int kMaxSlots = ICV_MAX_SLOTS;
   static constexpr int kOnesBytes = kI8 ? 16 * 128 : 0;
-  static constexpr int kAccStride = kI8 ? 2 * BN : BN;  // TMEM columns per accumulator stage
-  static constexpr int kTmemNeed = 2 * kAccStride;
+  // TMEM columns per accumulator stage (uint8: row sums at +BN; BN = 256
+  // keeps 32 columns for them and runs one accumulator stage)
+  static constexpr int kAccStride = kI8 ? (BN == 256 ? BN + 32 : 2 * BN) : BN;
+  static constexpr int kAccStages = 2 * kAccStride <= 512 ? 2 : 1;
+  static constexpr int kTmemNeed = kAccStages * kAccStride;
   static constexpr uint32_t kTmemCols = kTmemNeed <= 64 ? 64 : kTmemNeed <= 128 ? 128 : kTmemNeed <= 256 ? 256 : 512;
   static constexpr int kEpiBytes = kEpiWarpsS<kI8> * kEpiWarpBytes<kI8>;
   static constexpr int kBarBytes = 256;
@@ -465,7 +468,7 @@ __global__ void __launch_bounds__(kThreadsS<kI8>, 1) igemm_smem_kernel(const __g
         const int ti = (int)ti_local;
         if (ti < 8) TRACE(2 + ti);
       }
-      if (++as == 2) { as = 0; aphase ^= 1; }
+      if (++as == C::kAccStages) { as = 0; aphase ^= 1; }
     }
 #ifdef ICV_TRACE
     if (lane == 0) {
@@ -477,8 +480,9 @@ __global__ void __launch_bounds__(kThreadsS<kI8>, 1) igemm_smem_kernel(const __g
   } else {
     // a pair peer releases accumulators at the leader (which issues the next MMAs)
     const uint32_t tempty_remote = (kCS == 2 && crank != 0) ? mapa_rank(smem_u32(tempty), 0) : 0u;
-    epilogue_loop<kI8, BN, kEpiWarpsS<kI8>, C::kAccStride>(a, warp - kProdWarpsS<kI8>, lane, tmem_base, sEpi, sBias, tfull, tempty,
-                                                      sched, a.use_tma_y ? &tmap_y : nullptr, tempty_remote);
+    epilogue_loop<kI8, BN, kEpiWarpsS<kI8>, C::kAccStride, std::remove_const_t<decltype(sched)>, C::kAccStages>(
+        a, warp - kProdWarpsS<kI8>, lane, tmem_base, sEpi, sBias, tfull, tempty, sched, a.use_tma_y ? &tmap_y : nullptr,
+        tempty_remote);
   }
 
   tc_fence_before();
@@ -573,9 +577,21 @@ int launch_smem(const ConvArgs& c, cudaStream_t st) {
   return launch_smem_cs<kI8, BN, IbT, 1>(c, st);
 }
 
+// ICV_U8_BN=256: uint8 layers with a multiple of 256 output channels run
+// BLOCK_N 256 (half the A gathers per output, one accumulator stage); correct
+// but measured slower on cfg4 (51 vs 40 us: 1.3 waves of tiles, no epilogue
+// overlap), so BLOCK_N 128 stays the default
+template <bool kI8, int BN>
+bool smem_plan_ok(const ConvArgs& c);
+int smem_block_n(const ConvArgs& c) {
+  const char* v = getenv("ICV_U8_BN");   // (read per call: tests switch it)
+  if (c.L.family == kFamTcU8 && c.L.n_pad % 256 == 0 && v && atoi(v) == 256 && smem_plan_ok<true, 256>(c)) return 256;
+  return c.L.block_n;
+}
+
 template <typename IbT>
 int dispatch_smem(const ConvArgs& c, cudaStream_t st) {
-  const int bn = c.L.block_n;
+  const int bn = smem_block_n(c);
   if (c.L.family == kFamTcBf16) {
     if (bn == 64) return launch_smem<false, 64, IbT>(c, st);
     if (bn == 128) return launch_smem<false, 128, IbT>(c, st);
@@ -583,6 +599,7 @@ int dispatch_smem(const ConvArgs& c, cudaStream_t st) {
   } else if (c.L.family == kFamTcU8) {
     if (bn == 64) return launch_smem<true, 64, IbT>(c, st);
     if (bn == 128) return launch_smem<true, 128, IbT>(c, st);
+    if (bn == 256) return launch_smem<true, 256, IbT>(c, st);
   }
   return fail(ICV_ERR_UNSUPPORTED, "no tensor-core kernel for this tile width");
 }

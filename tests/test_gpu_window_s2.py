@@ -155,3 +155,17 @@ def test_stride1_window_u8_zero_point_row_pairs(monkeypatch):
     p = make_params(r=3, s=3, pt=1, pl=1, c=128, k=256)
     y, ref = _u8_run(p, icv.Shape4(3, 14, 14, 128), 128, 127, zero_fill=128)
     assert np.array_equal(y, ref), int((y != ref).sum())
+
+
+@pytest.mark.parametrize("geom,zx,zw", [
+    (dict(r=3, s=3, pt=1, pl=1, c=256, k=256, n=3, h=28, w=28), 128, 127),   # cfg4 geometry
+    (dict(r=3, s=3, pt=1, pl=0, pb=0, pr=1, c=64, k=512, n=2, h=9, w=11), 7, 200),
+])
+def test_u8_gather_kernel_block_n_256(geom, zx, zw, monkeypatch):
+    """Opt-in BLOCK_N 256 of the uint8 gather kernel (one accumulator stage,
+    32 TMEM columns for the row sums): bit-exact."""
+    monkeypatch.setenv("ICV_WIN", "0")
+    monkeypatch.setenv("ICV_U8_BN", "256")
+    p, shape = _params(geom)
+    y, ref = _u8_run(p, shape, zx, zw, zero_fill=zx)
+    assert np.array_equal(y, ref), int((y != ref).sum())
