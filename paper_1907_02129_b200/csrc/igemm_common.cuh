@@ -319,7 +319,7 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
     tc_fence_before();
     __syncwarp();
     if (lane == 0) {   // one arrival per epilogue warp (at the pair leader for a pair peer)
-      if (tempty_remote) mbar_arrive_remote(tempty_remote + as * 8);
+      if (tempty_remote) mbar_arrive_remote_relaxed(tempty_remote + as * 8);
       else mbar_arrive(&tempty[as]);
     }
 #ifdef ICV_ROWS_TIMELINE

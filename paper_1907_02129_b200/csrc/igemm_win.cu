@@ -39,6 +39,7 @@
 // Roles: warps 0-3 producers (thread 0 issues the window and filter TMA
 // loads; all 128 threads gather in cp.async mode), 8 epilogue warps, one MMA
 // warp (one elected lane; the pair leader's only).
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -118,13 +119,17 @@ bool plan_win(int win_stage, int rs, int kblocks, int n_pad, bool resident, Plan
   const int corr = kI8 ? rs * BN * 4 : 0;   // u8: staged per-tap padding corrections of the N tile
   const int fixed = 1024 + C::kOnesBytes + kEpiWarpsW * kEpiWarpBytesW + bias + tap + corr + bars;
   p->resident = 0;
-  if (resident) {   // two window stages + every K block of this CTA's filter rows
+  if (resident) {   // every K block of this CTA's filter rows + as many window stages (2..4) as fit
     if (kblocks > kMaxBSlots || fixed + 2 * win_stage + kblocks * C::kBBytes > 232448) return false;
+    const char* wse = getenv("ICV_WIN_WS");
+    int ws = wse && wse[0] ? atoi(wse) : kMaxWinStages;
+    ws = ws > kMaxWinStages ? kMaxWinStages : (ws < 2 ? 2 : ws);
+    while (ws > 2 && fixed + ws * win_stage + kblocks * C::kBBytes > 232448) --ws;
     p->resident = 1;
-    p->wstages = 2;
+    p->wstages = ws;
     p->bslots = kblocks;
     p->win_stage = win_stage;
-    p->off_b = 2 * win_stage;
+    p->off_b = ws * win_stage;
     p->off_ones = p->off_b + kblocks * C::kBBytes;
     p->off_epi = p->off_ones + C::kOnesBytes;
     p->off_bias = p->off_epi + kEpiWarpsW * kEpiWarpBytesW;
@@ -544,19 +549,29 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
 #pragma unroll
         for (int i = 0; i < kMT; ++i)
           adesc[i] = sw128_kmajor_desc(sWin_u32 + ws * pl.win_stage + a.win_lead + (rel0 + i * kBM) * 128);
+        const int i_beg = kS2 ? sPh[pi] : 0;
         const int i_end = kS2 ? sPh[pi + 1] : RS;
-        for (int ti = kS2 ? sPh[pi] : 0; ti < i_end; ++ti) {
-          const int e = kS2 ? sTapE[ti] : ti;   // (stride 1: taps in order)
+        // One elected lane issues the whole stage: per tap only the filter
+        // slot's barrier (skipped for a resident filter after the first
+        // unit: its slots are never reloaded), the descriptors and the MMAs
+        // -- no per-tap warp reconvergence (the issue loop has to keep up
+        // with 4 MMAs of N/2 cycles each per tap).
+        if (elect_one()) {
+          int bsl = bs;
+          uint32_t bphl = bph;
+          for (int ti = i_beg; ti < i_end; ++ti) {
+            const int e = kS2 ? sTapE[ti] : ti;   // (stride 1: taps in order)
+            const int bslot = pl.resident ? cb * RS + e : bsl;
+            if (!pl.resident || uk == 0) {
 #ifdef ICV_TRACE
-          long long c1 = clock64();
+              long long c1 = clock64();
 #endif
-          const int bslot = pl.resident ? cb * RS + e : bs;
-          mbar_wait(&bfull[bslot], pl.resident ? 0u : bph);
+              mbar_wait(&bfull[bslot], pl.resident ? 0u : bphl);
 #ifdef ICV_TRACE
-          c_wait_full += clock64() - c1;
+              c_wait_full += clock64() - c1;
 #endif
-          tc_fence_after();
-          if (elect_one()) {
+              tc_fence_after();
+            }
             const uint64_t toff = (uint64_t)(sTap[ti] * 8);   // (off(e) * 128 bytes) >> 4
             const uint64_t bdesc = sw128_kmajor_desc(sB_u32 + bslot * C::kBBytes);
 #pragma unroll
@@ -579,22 +594,24 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
               }
             }
             if constexpr (kCS == 1) {
-              if (!pl.resident) tc_commit(&bempty[bs]);
+              if (!pl.resident) tc_commit(&bempty[bsl]);
               if (ti == i_end - 1) {
                 tc_commit(&wempty[ws]);
                 if (last_stage) tc_commit(&tfull[as]);
               }
             } else {   // stage free / accumulators ready in both CTAs
-              if (!pl.resident) tc_commit2_mc(&bempty[bs], kMask);
+              if (!pl.resident) tc_commit2_mc(&bempty[bsl], kMask);
               if (ti == i_end - 1) {
                 tc_commit2_mc(&wempty[ws], kMask);
                 if (last_stage) tc_commit2_mc(&tfull[as], kMask);
               }
             }
+            if (++bsl == pl.bslots) { bsl = 0; bphl ^= 1; }
           }
-          __syncwarp();
-          if (++bs == pl.bslots) { bs = 0; bph ^= 1; }
         }
+        __syncwarp();
+        for (int ti = i_beg; ti < i_end; ++ti)   // (every lane keeps the slot counters)
+          if (++bs == pl.bslots) { bs = 0; bph ^= 1; }
         if (lane == 0 && uk < 4 && st < 2) TRACE(80 + uk * 2 + st);
         if (++ws == pl.wstages) { ws = 0; wph ^= 1; }
       }
@@ -794,7 +811,7 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {   // one arrival per epilogue warp, at the pair leader
-        if (tempty_remote) mbar_arrive_remote(tempty_remote + as * 8);
+        if (tempty_remote) mbar_arrive_remote_relaxed(tempty_remote + as * 8);
         else mbar_arrive(&tempty[as]);
       }
       if (ew == 0 && lane == 0 && uk < 8) TRACE(18 + uk);
@@ -1068,6 +1085,11 @@ int launch_win(const ConvArgs& c, const WinGeom& w, cudaStream_t st, bool reside
   a.cbe = 128 / a.t.elem_bytes;
   a.win_lead = slot_lead(w, kMT, kCS);
   if (clusters > a.units) clusters = a.units;
+  if (env_int("ICV_WIN_DEBUG", 0))
+    fprintf(stderr, "igemm_win: BN %d MT %d CS %d S2 %d resident %d wstages %d bslots %d win_stage %d smem %d | "
+                    "Wp %d Hz %d WR %d WR2 %d tiles %d units %d (two %d) clusters %lld split %d\n",
+            BN, kMT, kCS, (int)kS2, pl.resident, pl.wstages, pl.bslots, pl.win_stage, pl.bytes, w.Wp, w.Hz, w.WR, w.WR2,
+            w.tiles, a.units, a.two_units, (long long)clusters, a.win_split);
   if constexpr (kCS == 1) {
     kernel<<<(unsigned)clusters, kThreadsW, pl.bytes, st>>>(tmap_b, maps, a, pl);
   } else {

@@ -23,7 +23,12 @@ __device__ __forceinline__ bool mbar_try_cl(uint64_t* bar, uint32_t parity) {
                "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
   return ok != 0;
 }
+
+__device__ __forceinline__ void arrive_remote_relaxed(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
 __device__ int g_wait_mode;
+__device__ int g_relaxed;
 __device__ __forceinline__ void wait_mode(uint64_t* bar, uint32_t parity) {
   if (g_wait_mode == 1) { while (!mbar_test(bar, parity)) {} }
   else if (g_wait_mode == 2) { while (!mbar_try_cl(bar, parity)) {} }
@@ -115,7 +120,7 @@ __global__ void __cluster_dims__(2, 1, 1) win_pair_kernel(const __grid_constant_
       const int s = it % stages;
       wait_mode(&full[s], (it / stages) & 1);
       mbar_arrive(&empty[s]);
-      mbar_arrive_remote(mapa_rank(smem_u32(&empty[s]), 1));
+      (g_relaxed ? arrive_remote_relaxed : mbar_arrive_remote)(mapa_rank(smem_u32(&empty[s]), 1));
     }
   }
   __syncthreads();
@@ -155,14 +160,14 @@ __global__ void __cluster_dims__(2, 1, 1) win_fwd_kernel(const __grid_constant__
     for (int it = 0; it < iters; ++it) {
       const int s = it % stages;
       wait_mode(&local[s], (it / stages) & 1);
-      mbar_arrive_remote(mapa_rank(smem_u32(&full[s]), 0));
+      (g_relaxed ? arrive_remote_relaxed : mbar_arrive_remote)(mapa_rank(smem_u32(&full[s]), 0));
     }
   } else if (threadIdx.x == 64 && rank == 0) {
     for (int it = 0; it < iters; ++it) {
       const int s = it % stages;
       wait_mode(&full[s], (it / stages) & 1);
       mbar_arrive(&empty[s]);
-      mbar_arrive_remote(mapa_rank(smem_u32(&empty[s]), 1));
+      (g_relaxed ? arrive_remote_relaxed : mbar_arrive_remote)(mapa_rank(smem_u32(&empty[s]), 1));
     }
   }
   __syncthreads();
@@ -221,8 +226,10 @@ int main() {
       mx = 0;
       for (auto x : c) mx = x > mx ? x : mx;
       printf("%-36s (%5d B) stages=%d CLUSTER-LOCAL: %5.0f cycles/load\n", v.what, box_bytes, stages, mx / iters);
-      for (int mode = 0; mode < 3; ++mode) {
-      cudaMemcpyToSymbol(g_wait_mode, &mode, 4);
+      for (int mode = 0; mode < 4; ++mode) {
+      const int wm = mode == 3 ? 0 : mode, rel = mode == 3;
+      cudaMemcpyToSymbol(g_wait_mode, &wm, 4);
+      cudaMemcpyToSymbol(g_relaxed, &rel, 4);
       win_pair_kernel<<<nsm, 64, stages * ((box_bytes + 1023) / 1024 * 1024) + 1024>>>(tm, box_bytes, stages, iters,
                                                                                        v.x0, C / 64, dcyc);
       e = cudaDeviceSynchronize();
@@ -231,8 +238,9 @@ int main() {
       mx = 0;
       for (auto x : c) mx = x > mx ? x : mx;
       printf("%-36s (%5d B) stages=%d PAIR wait=%s: %5.0f cycles/load, %5.1f B/cycle/SM\n", v.what, box_bytes, stages,
-             mode == 0 ? "try_sleep" : mode == 1 ? "test_spin" : "try_cluster", mx / iters, box_bytes * (double)iters / mx);
+             mode == 0 ? "try_sleep" : mode == 1 ? "test_spin" : mode == 2 ? "try_cluster" : "try_sleep+relaxed_remote", mx / iters, box_bytes * (double)iters / mx);
       }
+      { const int one = 1; cudaMemcpyToSymbol(g_relaxed, &one, 4); }
       win_fwd_kernel<<<nsm, 96, stages * ((box_bytes + 1023) / 1024 * 1024) + 1024>>>(tm, box_bytes, stages, iters,
                                                                                       v.x0, C / 64, dcyc);
       e = cudaDeviceSynchronize();
@@ -240,7 +248,7 @@ int main() {
       cudaMemcpy(c.data(), dcyc, nsm * 8, cudaMemcpyDeviceToHost);
       mx = 0;
       for (auto x : c) mx = x > mx ? x : mx;
-      printf("%-36s (%5d B) stages=%d FWD:  %5.0f cycles/load, %5.1f B/cycle/SM\n", v.what, box_bytes, stages,
+      printf("%-36s (%5d B) stages=%d FWD(relaxed):  %5.0f cycles/load, %5.1f B/cycle/SM\n", v.what, box_bytes, stages,
              mx / iters, box_bytes * (double)iters / mx);
     }
   }

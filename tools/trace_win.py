@@ -14,6 +14,11 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 import paper_1907_02129_b200 as icv  # noqa: E402
 from paper_1907_02129_b200 import _lib as L  # noqa: E402
+from paper_1907_02129_b200 import workloads as wl  # noqa: E402
+
+# ResNet-50 layers by name (not BASELINE configs): trace_win.py r50:s1b1_3x3
+for _name, _shape, _params in wl.resnet50_layers(256):
+    wl.CONFIGS["r50:" + _name] = wl.ConvWorkload("r50_" + _name, "bf16", _shape, _params)
 
 
 def main():
