@@ -223,11 +223,6 @@ constexpr bool kNoPrefetch = false;
 constexpr bool kNoPrefetch = true;
 #endif
 
-#ifdef ICV_WEXP_FILTER1   // experiment: thread 0 alone loads the resident filter
-constexpr bool kFilter1 = true;
-#else
-constexpr bool kFilter1 = false;
-#endif
 
 #ifdef ICV_WEXP_DIRECT   // experiment: epilogue stores straight from registers
 constexpr bool kDirect = true;
@@ -408,19 +403,17 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
   };
   if (warp < kProdWarpsW) {
     // ------------------------------------------------------------ producers
-    // (TMA windows: thread 0 alone -- an idle thread must not trail the
-    // barrier phases it waits on)
-    // A resident filter is loaded by all four producer warps (lane 0 of warp
-    // w: K-block slots w, w + 4, ...): one thread's TMA loads complete about
-    // one per 450 cycles whatever their size (tools/micro/tma_rate.cu), so a
-    // single issuer would stretch the first unit by RS * cblocks * 450 cycles.
-    if (tma_win && pl.resident && lane == 0 && cid < a.units && !kFilter1) {
-      if (warp != 0)   // (warp 0 issues its slots after each window, below)
-        for (int slot = warp; slot < cblocks * RS; slot += kProdWarpsW) load_filter_slot(slot);
-    }
-    // TMA windows: lane 0 of warps 0 .. win_split-1 each load a share of the
-    // window's rows (one thread's TMA loads are served one after another)
-    if (tma_win && !(lane == 0 && warp < a.win_split)) goto done;
+    // TMA windows: lane 0 of warps 0 .. win_split-1 each load a share of
+    // the window's rows, and lane 0 of the last producer warp loads the
+    // filter blocks -- separate threads, because one thread's TMA loads are
+    // served one after another (~450 cycles each, tools/micro/tma_rate.cu)
+    // and a window must not queue behind filter loads waiting for free slots
+    // (nor the reverse).  cp.async windows: all producer threads gather,
+    // thread 0 loads the filter.  (An idle thread must not trail the barrier
+    // phases it waits on, hence the exits.)
+    const bool win_thread = !tma_win || (lane == 0 && warp < a.win_split);
+    const bool filt_thread = tma_win ? (lane == 0 && warp == kProdWarpsW - 1) : threadIdx.x == 0;
+    if (!win_thread && !filt_thread) goto done;
     {
       int ws = 0, bs = 0;
       uint32_t wph = 0, bph = 0;
@@ -439,6 +432,9 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
         for (int st = 0; st < cblocks * nph; ++st) {   // stages: (channel block, input plane)
           const int cb = kS2 ? st / nph : st, pi = kS2 ? st - cb * nph : 0;
           const int py = kS2 ? sPhP[pi] >> 1 : 0, px = kS2 ? sPhP[pi] & 1 : 0;
+          if (!win_thread) {
+            // (filter thread only)
+          } else {
           mbar_wait(&wempty[ws], wph ^ 1);
           if (threadIdx.x == 0 && uk < 4 && st < 2) TRACE(64 + uk * 2 + st);
           const uint32_t wbase = sWin_u32 + ws * pl.win_stage + a.win_lead;
@@ -489,15 +485,14 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
             cp_async_mbar_arrive_noinc(&wfull[ws]);
           }
           if (++ws == pl.wstages) { ws = 0; wph ^= 1; }
-          // this CTA's rows of the filter blocks of this channel block, one per
-          // tap (resident filter: loaded during the first unit only)
-          if (threadIdx.x == 0 && pl.resident) {
+          }
+          // this CTA's rows of the filter blocks of this stage, one per tap
+          // (resident filter: loaded during the first unit only)
+          if (filt_thread && pl.resident) {
             if (uk == 0)
-              for (int i = kS2 ? sPh[pi] : 0; i < (kS2 ? sPh[pi + 1] : RS); ++i) {
-                const int slot = cb * RS + (kS2 ? sTapE[i] : i);
-                if (!tma_win || kFilter1 || slot % kProdWarpsW == 0) load_filter_slot(slot);
-              }
-          } else if (threadIdx.x == 0) {
+              for (int i = kS2 ? sPh[pi] : 0; i < (kS2 ? sPh[pi + 1] : RS); ++i)
+                load_filter_slot(cb * RS + (kS2 ? sTapE[i] : i));
+          } else if (filt_thread) {
             for (int i = kS2 ? sPh[pi] : 0; i < (kS2 ? sPh[pi + 1] : RS); ++i) {
               const int e = kS2 ? sTapE[i] : i;
               mbar_wait(&bempty[bs], bph ^ 1);
@@ -1126,20 +1121,22 @@ int dispatch_bn(const ConvArgs& c, const WinGeom& w, cudaStream_t st, bool launc
   const bool pair = tma_zero_ok(c) && env_int("ICV_WIN_CS", 2) == 2;
   const bool mt2 = env_int("ICV_WIN_MT", 2) == 2;
   const bool res = env_int("ICV_WIN_RES", 1) == 1;
-  // preference: pair with a resident filter, pair with two-tile units, pair,
-  // then the single-CTA kernels
-  if (pair && res && win_plan_for<kI8, BN, 1, 2, kS2>(c, w, &pl, true))
-    return launch ? launch_win<kI8, BN, 1, 2, kS2>(c, w, st, true) : ICV_OK;
+  // preference: pair with two-tile units (measured fastest on every stride-1
+  // layer: cfg2 25.5 vs 27.5 us resident, ResNet-50 s1 3x3 85 vs 121 us --
+  // two tiles share each filter block and one window of WR2 rows), pair
+  // with a resident filter, pair, then the single-CTA kernels
   if constexpr (mt_fits<kI8, BN, 2>()) {
     if (pair && mt2 && win_plan_for<kI8, BN, 2, 2, kS2>(c, w, &pl))
       return launch ? launch_win<kI8, BN, 2, 2, kS2>(c, w, st, false) : ICV_OK;
   }
+  if (pair && res && win_plan_for<kI8, BN, 1, 2, kS2>(c, w, &pl, true))
+    return launch ? launch_win<kI8, BN, 1, 2, kS2>(c, w, st, true) : ICV_OK;
   if (pair && win_plan_for<kI8, BN, 1, 2, kS2>(c, w, &pl)) return launch ? launch_win<kI8, BN, 1, 2, kS2>(c, w, st, false) : ICV_OK;
-  if (res && win_plan_for<kI8, BN, 1, 1, kS2>(c, w, &pl, true))
-    return launch ? launch_win<kI8, BN, 1, 1, kS2>(c, w, st, true) : ICV_OK;
   if constexpr (mt_fits<kI8, BN, 2>()) {
     if (mt2 && win_plan_for<kI8, BN, 2, 1, kS2>(c, w, &pl)) return launch ? launch_win<kI8, BN, 2, 1, kS2>(c, w, st, false) : ICV_OK;
   }
+  if (res && win_plan_for<kI8, BN, 1, 1, kS2>(c, w, &pl, true))
+    return launch ? launch_win<kI8, BN, 1, 1, kS2>(c, w, st, true) : ICV_OK;
   if (win_plan_for<kI8, BN, 1, 1, kS2>(c, w, &pl)) return launch ? launch_win<kI8, BN, 1, 1, kS2>(c, w, st, false) : ICV_OK;
   return ICV_ERR_UNSUPPORTED;
 }

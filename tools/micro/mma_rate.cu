@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(128, 1) mma_rate(int iters, unsigned long long
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tslot;
-  if (kVar >= 7 && threadIdx.x < 32) {
+  if (kVar == 7 && threadIdx.x < 32) {
     // whole warp runs the loop; one elected lane issues (uniform operands)
     constexpr uint32_t idesc = make_idesc<kI8>(128, N);
     const uint64_t ad = sw128_kmajor_desc(smem_u32(sA));
@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(128, 1) mma_rate(int iters, unsigned long long
     mbar_wait(&bar, 0);
     long long t1 = clock64();
     if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = (unsigned long long)(t1 - t0);
-  } else if (kVar < 7 && threadIdx.x == 0) {
+  } else if ((kVar < 7 || kVar == 8) && threadIdx.x == 0) {
     constexpr uint32_t idesc = make_idesc<kI8>(128, N);
     const uint64_t ad = sw128_kmajor_desc(smem_u32(sA));
     const uint64_t bd = sw128_kmajor_desc(smem_u32(sB));
@@ -77,10 +77,15 @@ __global__ void __launch_bounds__(128, 1) mma_rate(int iters, unsigned long long
         }
       }
       if (kVar == 6 && (it & 1) == 0) mbar_wait(&done, 0);
-      if (kVar >= 2) tc_fence_after();
+      if (kVar >= 2 && kVar != 8) tc_fence_after();
 #pragma unroll
-      for (int k = 0; k < 4; ++k) tc_mma<kI8>(tmem, ad + 2 * k, bd + 2 * k, idesc, (it | k) != 0);
-      if (kVar >= 1) tc_commit(&bars[it & 7]);
+      for (int k = 0; k < 4; ++k) {
+        // var 0: one accumulator; var 8: two accumulators alternated
+        // (breaks the accumulate-dependency chain between consecutive MMAs)
+        const uint32_t dd = (kVar == 8 && (k & 1)) ? tmem + N : tmem;
+        tc_mma<kI8>(dd, ad + 2 * k, bd + 2 * k, idesc, (it | (k >> 1)) != 0);
+      }
+      if (kVar >= 1 && kVar != 8) tc_commit(&bars[it & 7]);
     }
     tc_commit(&bar);
     mbar_wait(&bar, 0);
@@ -116,5 +121,7 @@ int main() {
   unsigned long long* d;
   cudaMalloc(&d, 64);
   run<false, 128, 2>(d); run<false, 128, 3>(d); run<false, 128, 7>(d); run<false, 64, 7>(d);
+  run<false, 64, 0>(d); run<false, 64, 8>(d); run<false, 128, 0>(d); run<false, 128, 8>(d); run<false, 32, 0>(d);
+  run<false, 32, 8>(d); run<true, 64, 0>(d); run<true, 128, 0>(d); run<true, 256, 0>(d);
   return 0;
 }

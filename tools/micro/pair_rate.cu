@@ -95,5 +95,6 @@ int main() {
   cudaMalloc(&d, 8);
   run<0, 128>(d); run<1, 128>(d); run<2, 128>(d); run<3, 128>(d);
   run<0, 256>(d); run<1, 256>(d);
+  run<0, 64>(d); run<1, 64>(d); run<2, 64>(d);
   return 0;
 }
