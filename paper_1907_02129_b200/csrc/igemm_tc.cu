@@ -37,6 +37,9 @@ namespace {
 
 // Epilogue warps: 8 for uint8 (the q31 requantization is the heavier
 // epilogue; measured 47 -> 41 us on cfg4), 4 for bf16 (8 measured slower).
+// Output-heavy bf16 layers (K >= 4 C: the ResNet-50 1x1 expansions) run 8
+// (s1b1_1x1b 131 -> 102 us, s2 1x1b 78 -> 63 us; the 1x1 reductions and
+// strided 3x3s measured 4-8 us slower with 8).
 template <bool kI8>
 constexpr int kEpiWarpsS = kI8 ? 8 : 4;
 // Gather (producer) warps: each covers 128 / kProdWarpsS A rows.
@@ -45,12 +48,12 @@ constexpr int kEpiWarpsS = kI8 ? 8 : 4;
 #endif
 template <bool kI8>
 constexpr int kProdWarpsS = kI8 ? 4 : ICV_PROD_WARPS_BF16;
-template <bool kI8>
-constexpr int kMmaWarpS = kProdWarpsS<kI8> + kEpiWarpsS<kI8>;
-template <bool kI8>
-constexpr int kThreadsS = 32 * (kMmaWarpS<kI8> + 1);
+template <bool kI8, int kEpiW = kEpiWarpsS<kI8>>
+constexpr int kMmaWarpS = kProdWarpsS<kI8> + kEpiW;
+template <bool kI8, int kEpiW = kEpiWarpsS<kI8>>
+constexpr int kThreadsS = 32 * (kMmaWarpS<kI8, kEpiW> + 1);
 
-template <bool kI8, int BN, int kPair = 1>
+template <bool kI8, int BN, int kPair = 1, int kEpiW = kEpiWarpsS<kI8>>
 struct CfgS {
   // B bytes per K block held by this CTA (a CTA pair splits the BN rows)
   static constexpr int kBBytes = BN * 128 / kPair;
@@ -70,7 +73,7 @@ struct CfgS {
   static constexpr int kAccStages = 2 * kAccStride <= 512 ? 2 : 1;
   static constexpr int kTmemNeed = kAccStages * kAccStride;
   static constexpr uint32_t kTmemCols = kTmemNeed <= 64 ? 64 : kTmemNeed <= 128 ? 128 : kTmemNeed <= 256 ? 256 : 512;
-  static constexpr int kEpiBytes = kEpiWarpsS<kI8> * kEpiWarpBytes<kI8>;
+  static constexpr int kEpiBytes = kEpiW * kEpiWarpBytes<kI8>;
   static constexpr int kBarBytes = 256;
   static_assert(kTmemNeed <= 512, "TMEM overflow");
 };
@@ -82,9 +85,9 @@ struct PlanS {
   int off_b, off_ones, off_epi, off_bias, off_ib, off_bar, bytes;
 };
 
-template <bool kI8, int BN, typename IbT, int kPair = 1>
+template <bool kI8, int BN, typename IbT, int kPair = 1, int kEpiW = kEpiWarpsS<kI8>>
 bool plan_smem(int rs, int n_pad, PlanS* p) {
-  using C = CfgS<kI8, BN, kPair>;
+  using C = CfgS<kI8, BN, kPair, kEpiW>;
   const int bias = (n_pad * 4 + 15) / 16 * 16;
   const int ib = 2 * rs * kBM * 4 + 2 * kBM * 4;   // int32 index slices + per-row bases
   const int fixed = 1024 + C::kOnesBytes + C::kEpiBytes + bias + ib + C::kBarBytes;
@@ -127,8 +130,8 @@ struct ClusterTiles {
   }
 };
 
-template <bool kI8, int BN, typename IbT, int kCS>
-__global__ void __launch_bounds__(kThreadsS<kI8>, 1) igemm_smem_kernel(const __grid_constant__ CUtensorMap tmap_b,
+template <bool kI8, int BN, typename IbT, int kCS, int kEpiW>
+__global__ void __launch_bounds__(kThreadsS<kI8, kEpiW>, 1) igemm_smem_kernel(const __grid_constant__ CUtensorMap tmap_b,
                                                                   const __grid_constant__ CUtensorMap tmap_x,
                                                                   const __grid_constant__ CUtensorMap tmap_y,
                                                                   const TcArgs a, const PlanS pl) {
@@ -136,7 +139,7 @@ __global__ void __launch_bounds__(kThreadsS<kI8>, 1) igemm_smem_kernel(const __g
   // M = 256 (its 128 rows + the peer's 128 rows); each CTA gathers its own A
   // rows and TMA-loads its half of the filter rows, so each SM receives half
   // the filter bytes of the single-CTA kernel.
-  using C = CfgS<kI8, BN, kCS>;
+  using C = CfgS<kI8, BN, kCS, kEpiW>;
   static_assert(kCS == 1 || kCS == 2, "single CTA or CTA pair");
   constexpr uint16_t kMask = (uint16_t)((1u << kCS) - 1);
   const ClusterTiles<kCS> sched{a.total_tiles / a.n_tiles, a.n_tiles};
@@ -185,7 +188,7 @@ __global__ void __launch_bounds__(kThreadsS<kI8>, 1) igemm_smem_kernel(const __g
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);                   // tcgen05.commit after the last K block
       // one arrival per epilogue warp (of both CTAs at the pair leader)
-      mbar_init(&tempty[s], (kCS == 2 && crank == 0) ? 2 * kEpiWarpsS<kI8> : kEpiWarpsS<kI8>);
+      mbar_init(&tempty[s], (kCS == 2 && crank == 0) ? 2 * kEpiW : kEpiW);
     }
     fence_mbar_init();
     tma_prefetch_desc(&tmap_b);
@@ -199,7 +202,7 @@ __global__ void __launch_bounds__(kThreadsS<kI8>, 1) igemm_smem_kernel(const __g
     }
   }
   for (int i = threadIdx.x; i < a.n_pad; i += blockDim.x) sBias[i] = __ldg(static_cast<const uint32_t*>(a.bias) + i);
-  if (warp == kMmaWarpS<kI8>) {
+  if (warp == kMmaWarpS<kI8, kEpiW>) {
     if constexpr (kCS == 2) tmem_alloc2<C::kTmemCols>(tmem_slot);
     else tmem_alloc<C::kTmemCols>(tmem_slot);
   }
@@ -384,7 +387,7 @@ __global__ void __launch_bounds__(kThreadsS<kI8>, 1) igemm_smem_kernel(const __g
       g_icv_trace[blockIdx.x][38] = (unsigned long long)p_wait;
     }
 #endif
-  } else if (warp == kMmaWarpS<kI8> && kCS == 2 && crank != 0) {
+  } else if (warp == kMmaWarpS<kI8, kEpiW> && kCS == 2 && crank != 0) {
     // ------------------------------------------------------------ pair peer: forwarder
     // The leader's MMAs read this CTA's stages too: once a stage is full here
     // (own gathers + own filter half), tell the leader's full barrier.
@@ -399,7 +402,7 @@ __global__ void __launch_bounds__(kThreadsS<kI8>, 1) igemm_smem_kernel(const __g
         __syncwarp();
         if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
-  } else if (warp == kMmaWarpS<kI8>) {
+  } else if (warp == kMmaWarpS<kI8, kEpiW>) {
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t idesc = make_idesc<kI8>(kBM * kCS, BN);
     constexpr uint32_t idesc_ones = make_idesc<kI8>(kBM * kCS, 16);
@@ -480,7 +483,7 @@ __global__ void __launch_bounds__(kThreadsS<kI8>, 1) igemm_smem_kernel(const __g
   } else {
     // a pair peer releases accumulators at the leader (which issues the next MMAs)
     const uint32_t tempty_remote = (kCS == 2 && crank != 0) ? mapa_rank(smem_u32(tempty), 0) : 0u;
-    epilogue_loop<kI8, BN, kEpiWarpsS<kI8>, C::kAccStride, std::remove_const_t<decltype(sched)>, C::kAccStages>(
+    epilogue_loop<kI8, BN, kEpiW, C::kAccStride, std::remove_const_t<decltype(sched)>, C::kAccStages>(
         a, warp - kProdWarpsS<kI8>, lane, tmem_base, sEpi, sBias, tfull, tempty, sched, a.use_tma_y ? &tmap_y : nullptr,
         tempty_remote);
   }
@@ -488,21 +491,21 @@ __global__ void __launch_bounds__(kThreadsS<kI8>, 1) igemm_smem_kernel(const __g
   tc_fence_before();
   __syncthreads();
   if constexpr (kCS > 1) cluster_sync_all();   // both CTAs done: no peer still signals, writes or reads TMEM
-  if (warp == kMmaWarpS<kI8>) {
+  if (warp == kMmaWarpS<kI8, kEpiW>) {
     tc_fence_after();
     if constexpr (kCS == 2) tmem_dealloc2<C::kTmemCols>(tmem_base);
     else tmem_dealloc<C::kTmemCols>(tmem_base);
   }
 }
 
-template <bool kI8, int BN, typename IbT, int kCS>
+template <bool kI8, int BN, typename IbT, int kCS, int kEpiW>
 int launch_smem_cs(const ConvArgs& c, cudaStream_t st) {
-  auto kernel = igemm_smem_kernel<kI8, BN, IbT, kCS>;
+  auto kernel = igemm_smem_kernel<kI8, BN, IbT, kCS, kEpiW>;
   static std::once_flag attr_once;
   static cudaError_t attr_err = cudaSuccess;
   static int max_clusters = 0;
   PlanS pl;
-  if (!plan_smem<kI8, BN, IbT, kCS>(c.g.RS(), c.L.n_pad, &pl))
+  if (!plan_smem<kI8, BN, IbT, kCS, kEpiW>(c.g.RS(), c.L.n_pad, &pl))
     return fail(ICV_ERR_UNSUPPORTED, "indirection slice of this kernel size does not fit in shared memory");
   if (c.g.N * c.g.H * c.g.W * (int64_t)c.g.C >= (int64_t(1) << 31))
     return fail(ICV_ERR_UNSUPPORTED, "tensor-core kernel: input tensors of 2^31 or more elements are not supported");
@@ -517,7 +520,7 @@ int launch_smem_cs(const ConvArgs& c, cudaStream_t st) {
       at[0].val.clusterDim.y = 1;
       at[0].val.clusterDim.z = 1;
       q.gridDim = dim3(kCS * 74);
-      q.blockDim = dim3(kThreadsS<kI8>);
+      q.blockDim = dim3(kThreadsS<kI8, kEpiW>);
       q.dynamicSmemBytes = pl.bytes;
       q.attrs = at;
       q.numAttrs = 1;
@@ -540,7 +543,7 @@ int launch_smem_cs(const ConvArgs& c, cudaStream_t st) {
   const int sms = sm_count();
   if constexpr (kCS == 1) {
     const int grid = (int)(a.total_tiles < sms ? a.total_tiles : sms);
-    kernel<<<grid, kThreadsS<kI8>, pl.bytes, st>>>(tmap, tmap_x, tmap_y, a, pl);
+    kernel<<<grid, kThreadsS<kI8, kEpiW>, pl.bytes, st>>>(tmap, tmap_x, tmap_y, a, pl);
   } else {
     const int64_t groups = (a.total_tiles / a.n_tiles + kCS - 1) / kCS * a.n_tiles;
     int64_t clusters = sms / kCS;
@@ -553,7 +556,7 @@ int launch_smem_cs(const ConvArgs& c, cudaStream_t st) {
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     cfg.gridDim = dim3((unsigned)(clusters * kCS));
-    cfg.blockDim = dim3(kThreadsS<kI8>);
+    cfg.blockDim = dim3(kThreadsS<kI8, kEpiW>);
     cfg.dynamicSmemBytes = pl.bytes;
     cfg.stream = st;
     cfg.attrs = at;
@@ -573,8 +576,14 @@ bool use_clusters() {
 
 template <bool kI8, int BN, typename IbT>
 int launch_smem(const ConvArgs& c, cudaStream_t st) {
-  if (use_clusters()) return launch_smem_cs<kI8, BN, IbT, 2>(c, st);
-  return launch_smem_cs<kI8, BN, IbT, 1>(c, st);
+  if (use_clusters()) return launch_smem_cs<kI8, BN, IbT, 2, kEpiWarpsS<kI8>>(c, st);
+  if constexpr (!kI8) {
+    // output-heavy layers (K >= 4 C) get 8 epilogue warps
+    PlanS pl;
+    if ((int64_t)c.g.K >= 4 * (int64_t)c.g.C && plan_smem<kI8, BN, IbT, 1, 8>(c.g.RS(), c.L.n_pad, &pl))
+      return launch_smem_cs<kI8, BN, IbT, 1, 8>(c, st);
+  }
+  return launch_smem_cs<kI8, BN, IbT, 1, kEpiWarpsS<kI8>>(c, st);
 }
 
 // ICV_U8_BN=256: uint8 layers with a multiple of 256 output channels run
