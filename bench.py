@@ -527,7 +527,7 @@ def stack_bench(device, peaks: dict, flush, batch: int = 256, passes: int = 5) -
            "value": round(stack.flops / (total * 1e-3) / 1e12, 2), "unit": "TFLOP/s (end to end, max pool included)",
            "value_convs_only": round(stack.flops / (conv * 1e-3) / 1e12, 2),
            "sum_of_layer_rooflines_ms": round(roof_ms, 4), "frac_of_sum_roofline": round(roof_ms / conv, 3),
-           "per_layer": "profiles/r01d_cfg5_layers.json (tools/time_stack.py)"}
+           "per_layer": "profiles/r01e_cfg5_layers.json (tools/time_stack.py)"}
     del stack
     torch.cuda.empty_cache()
     return res
