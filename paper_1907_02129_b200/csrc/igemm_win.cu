@@ -752,7 +752,11 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
 #pragma unroll
               for (int h = 0; h < 4; ++h) {
                 const int32_t acc = (int32_t)((long long)(int32_t)v[4 * qd + h] + bb[h] + corr);
+#ifndef ICV_WEXP_NOREQ
                 word |= (uint32_t)requant_u8(acc, a.t.m0, a.t.shift, a.t.zo, a.t.qmin, a.t.qmax) << (8 * h);
+#else   // experiment: no requantization (timing only)
+                word |= ((uint32_t)acc & 0xFFu) << (8 * h);
+#endif
               }
               w[qd] = word;
             }
