@@ -88,7 +88,20 @@ struct WinArgs {
   int32_t php[4];
   int32_t g_shift, rel_shift;   // window row / in-window position of a tile's first pixel (see win_tile)
   const int32_t* tapcorr;       // u8 with TMA windows: per (tap, channel) zx * sum_c (w - zw), added for padded taps
+  // u8 border classes (ncls > 0): a pixel's padded-tap set depends only on
+  // its row class (top rows oy < cls_tb, bottom rows oy >= cls_ohb, one
+  // interior class) and its column class; the epilogue adds one staged
+  // correction vector per class instead of one per padded tap
+  int32_t ncls, cls_tb, cls_ohb, cls_nr, cls_lb, cls_owb, cls_ncc;
 };
+
+// border class of output row / column v (top / bottom prefix and suffix, else interior = n - 1)
+__device__ __forceinline__ int border_class(int v, int tb, int ohb, int n) {
+  return v < tb ? v : (v >= ohb ? tb + v - ohb : n - 1);
+}
+__device__ __forceinline__ int border_rep(int k, int tb, int ohb, int n) {
+  return k < tb ? k : (k < n - 1 ? ohb + k - tb : tb);
+}
 
 struct PlanW {
   int wstages, bslots;
@@ -652,6 +665,41 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
         sCorr[i] = __ldg(a.tapcorr + (int64_t)e * a.t.n_pad + n);
       }
     named_bar_sync(kEpiBarId, 32 * kEpiWarpsW);
+    const bool cls_mode = corr_staged && a.ncls > 0;
+    if (cls_mode) {
+      // per-class sums of the staged per-tap corrections, written in place
+      // over the per-tap table (ncls <= RS, at most kClsPer entries a thread)
+      constexpr int kClsPer = 16;
+      const int R = a.t.RS / a.S;
+      int32_t tmp[kClsPer];
+#pragma unroll
+      for (int j = 0; j < kClsPer; ++j) {
+        const int idx = threadIdx.x - 32 * kProdWarpsW + j * 32 * kEpiWarpsW;
+        tmp[j] = 0;
+        if (idx < a.ncls * BN) {
+          const int cl = idx / BN, n = idx - cl * BN;
+          const int oy = border_rep(cl / a.cls_ncc, a.cls_tb, a.cls_ohb, a.cls_nr);
+          const int ox = border_rep(cl % a.cls_ncc, a.cls_lb, a.cls_owb, a.cls_ncc);
+          int32_t sum = 0;
+          for (int ky = 0; ky < R; ++ky) {
+            const int iy = oy * a.sy - a.PT + ky * a.DY;
+            const bool row_out = iy < 0 || iy >= a.H;
+            for (int kx = 0; kx < a.S; ++kx) {
+              const int ix = ox * a.sy - a.PL + kx * a.DX;
+              if (row_out || ix < 0 || ix >= a.W) sum += sCorr[(ky * a.S + kx) * BN + n];
+            }
+          }
+          tmp[j] = sum;
+        }
+      }
+      named_bar_sync(kEpiBarId, 32 * kEpiWarpsW);
+#pragma unroll
+      for (int j = 0; j < kClsPer; ++j) {
+        const int idx = threadIdx.x - 32 * kProdWarpsW + j * 32 * kEpiWarpsW;
+        if (idx < a.ncls * BN) sCorr[idx] = tmp[j];
+      }
+      named_bar_sync(kEpiBarId, 32 * kEpiWarpsW);
+    }
     const uint32_t tempty_remote = kCS == 2 && crank != 0 ? mapa_rank(smem_u32(tempty), 0) : 0u;
     const int32_t img_px = a.Hz * a.Wp;   // virtual pixels per image
     int as = 0;
@@ -682,7 +730,11 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
         // u8 with zero-filled TMA windows: padded taps contributed x = 0
         // instead of the zero point; their per-channel correction is added below
         uint64_t oob = 0;
-        if (kI8 && a.tapcorr != nullptr && myp >= 0)
+        const int32_t* clsCorr = sCorr;
+        if (cls_mode)
+          clsCorr = sCorr + (border_class(oy < a.OH ? oy : a.OH - 1, a.cls_tb, a.cls_ohb, a.cls_nr) * a.cls_ncc +
+                             border_class(ox < a.OW ? ox : a.OW - 1, a.cls_lb, a.cls_owb, a.cls_ncc)) * BN;
+        else if (kI8 && a.tapcorr != nullptr && myp >= 0)
           for (int e = 0; e < a.t.RS; ++e) {
             const int ky = e / a.S, kx = e - ky * a.S;
             const int iy = oy * a.sy - a.PT + ky * a.DY, ix = ox * a.sy - a.PL + kx * a.DX;
@@ -741,6 +793,10 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
 #pragma unroll
             for (int qd = 0; qd < 8; ++qd) {
               int4 b = cst4[qd];
+              if (cls_mode) {
+                const int4 t = reinterpret_cast<const int4*>(clsCorr + (n0 - nt * BN))[qd];
+                b.x += t.x; b.y += t.y; b.z += t.z; b.w += t.w;
+              }
               for (uint64_t m = oob; m != 0; m &= m - 1) {
                 const int e = __ffsll((long long)m) - 1;
                 const int4 t = corr_staged ? reinterpret_cast<const int4*>(sCorr + e * BN + (n0 - nt * BN))[qd]
@@ -1041,6 +1097,23 @@ int launch_win(const ConvArgs& c, const WinGeom& w, cudaStream_t st, bool reside
   a.zero_known = tma_zero_ok(c);
   a.tapcorr = (kI8 && !c.zero_known && c.zero_is_zp && c.L.tapcorr_off)
                   ? reinterpret_cast<const int32_t*>(c.packed + c.L.tapcorr_off) : nullptr;
+  a.ncls = 0;
+  if (a.tapcorr != nullptr && env_int("ICV_WIN_U8_CLS", 1) == 1) {
+    // border classes (WinArgs): top rows iy0 < 0, bottom rows with the last tap row >= H
+    const auto border = [&](int64_t O, int64_t I, int P, int span, int st, int* tb, int* ohb, int* n) {
+      const int64_t t = std::min<int64_t>(O, (P + st - 1) / st);
+      const int64_t first_bot = std::max<int64_t>(0, (I + P - span + st) / st);   // ceil((I + P - span + 1) / st)
+      const int64_t b0 = std::max<int64_t>(t, std::min<int64_t>(O, first_bot));
+      *tb = (int)t; *ohb = (int)b0; *n = (int)(t + (O - b0) + 1);
+    };
+    int nr, ncc;
+    border(c.g.OH, c.g.H, c.g.PT, (c.g.R - 1) * c.g.DY + 1, w.sy, &a.cls_tb, &a.cls_ohb, &nr);
+    border(c.g.OW, c.g.W, c.g.PL, (c.g.S - 1) * c.g.DX + 1, w.sy, &a.cls_lb, &a.cls_owb, &ncc);
+    a.cls_nr = nr;
+    a.cls_ncc = ncc;
+    const int ncls = nr * ncc;
+    if (ncls <= c.g.RS() && ncls * BN <= 16 * 32 * kEpiWarpsW && c.L.n_pad <= BN) a.ncls = ncls;
+  }
   a.sy = w.sy;
   a.nph = w.nph;
   for (int p = 0; p < 4; ++p) a.php[p] = p < w.nph ? w.php[p] : 0;

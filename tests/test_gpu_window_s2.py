@@ -131,10 +131,13 @@ def test_cfg4_window_selectable(monkeypatch):
     (dict(r=5, s=5, pt=2, pl=2, c=32, k=64, n=2, h=16, w=16), 255, 0),
 ])
 @pytest.mark.parametrize("cs", [1, 2])
-def test_stride2_window_u8_zero_point_row(geom, zx, zw, cs, monkeypatch):
+@pytest.mark.parametrize("cls", ["1", "0"])
+def test_stride2_window_u8_zero_point_row(geom, zx, zw, cs, cls, monkeypatch):
     """Zero row = input zero point (the reference's quantized padding): TMA
-    zero fill + per-tap correction must give the oracle's bytes exactly."""
+    zero fill + padding correction (per border class, or per padded tap with
+    ICV_WIN_U8_CLS=0) must give the oracle's bytes exactly."""
     monkeypatch.setenv("ICV_WIN_CS", str(cs))
+    monkeypatch.setenv("ICV_WIN_U8_CLS", cls)
     p, shape = _params(geom)
     y, ref = _u8_run(p, shape, zx, zw, zero_fill=zx)
     assert np.array_equal(y, ref), int((y != ref).sum())
@@ -148,12 +151,22 @@ def test_stride2_window_u8_zeros_row_nonzero_zp():
     assert np.array_equal(y, ref), int((y != ref).sum())
 
 
-def test_stride1_window_u8_zero_point_row_pairs(monkeypatch):
+@pytest.mark.parametrize("geom", [
+    dict(r=3, s=3, pt=1, pl=1, c=128, k=256, h=14, w=14),                      # 9 border classes
+    dict(r=3, s=3, pt=2, pl=2, dy=2, dx=2, c=128, k=256, h=13, w=12),          # 25 classes > RS: per-tap
+    dict(r=3, s=3, pt=1, pl=0, pb=1, pr=2, c=64, k=128, h=11, w=10),           # asymmetric pads
+    dict(r=3, s=3, pt=1, pl=1, c=64, k=64, h=3, w=2),                          # tiny: rows both top and bottom
+])
+@pytest.mark.parametrize("cls", ["1", "0"])
+def test_stride1_window_u8_zero_point_row_pairs(geom, cls, monkeypatch):
     """Stride-1 uint8 with a zero-point zero row now also takes TMA windows
-    (and CTA pairs) through the per-tap correction."""
+    (and CTA pairs) through the padding correction."""
     monkeypatch.setenv("ICV_WIN_CS", "2")
-    p = make_params(r=3, s=3, pt=1, pl=1, c=128, k=256)
-    y, ref = _u8_run(p, icv.Shape4(3, 14, 14, 128), 128, 127, zero_fill=128)
+    monkeypatch.setenv("ICV_WIN_U8_CLS", cls)
+    g = dict(geom)
+    h, wd = g.pop("h"), g.pop("w")
+    p = make_params(**g)
+    y, ref = _u8_run(p, icv.Shape4(3, h, wd, g["c"]), 128, 127, zero_fill=128)
     assert np.array_equal(y, ref), int((y != ref).sum())
 
 

@@ -14,8 +14,15 @@ name = sys.argv[1] if len(sys.argv) > 1 else "cfg4"
 dev = torch.device("cuda", 0)
 w, x, xh, pf, ib, y, tile = bench.setup_problem(name, 0, CONFIGS[name].in_shape.n, dev)
 flush = bench.make_l2_flush(dev)
-runs = [("default", {}, False), ("BN128", {"ICV_WIN_U8_BN": "128"}, False), ("CS1", {"ICV_WIN_CS": "1"}, False),
-        ("zeros-row flags (no tapcorr; timing only)", {}, True), ("smem kernel", {"ICV_WIN": "0"}, False)]
+W = {"ICV_WIN": "1"}
+runs = [("default dispatch", {}, False),
+        ("window u8 (class corrections)", W, False),
+        ("window u8 per-tap corrections", {**W, "ICV_WIN_U8_CLS": "0"}, False),
+        ("window u8 BN128", {**W, "ICV_WIN_U8_BN": "128"}, False),
+        ("window u8 BN128 MT1", {**W, "ICV_WIN_U8_BN": "128", "ICV_WIN_MT": "1"}, False),
+        ("window u8 CS1", {**W, "ICV_WIN_CS": "1"}, False),
+        ("window u8 zeros-row flags (no corr; timing only)", W, True),
+        ("gather kernel", {"ICV_WIN": "0"}, False)]
 for label, env, zeros in runs:
     old = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
