@@ -239,7 +239,8 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
         }
       } else {
         const int4* cst4 = reinterpret_cast<const int4*>(sBias + n);
-        const long long corr = -(long long)a.zw * rowsum;
+        // exact mod 2^32: the true accumulator fits int32
+        const uint32_t corr = 0u - (uint32_t)a.zw * (uint32_t)rowsum;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const int4 b = cst4[q];
@@ -247,7 +248,7 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
           uint32_t word = 0;
 #pragma unroll
           for (int h = 0; h < 4; ++h) {
-            const int32_t acc = (int32_t)((long long)(int32_t)v[4 * q + h] + bb[h] + corr);
+            const int32_t acc = (int32_t)(v[4 * q + h] + (uint32_t)bb[h] + corr);
             word |= (uint32_t)requant_u8(acc, a.m0, a.shift, a.zo, a.qmin, a.qmax) << (8 * h);
           }
           w[q] = word;

@@ -47,7 +47,16 @@ __device__ __forceinline__ unsigned long long rt_now() {
 #define RTK(base, k)
 #endif
 
-constexpr int kRing = 16;                 // converted input rows resident
+#ifndef ICV_ROWS_RING
+#define ICV_ROWS_RING 32
+#endif
+#ifndef ICV_ROWS_STAGES
+#define ICV_ROWS_STAGES 6
+#endif
+#ifndef ICV_ROWS_READY
+#define ICV_ROWS_READY 12
+#endif
+constexpr int kRingBig = ICV_ROWS_RING;   // converted input rows resident (power of 2) when the smem plan fits, else 16
 constexpr int kConvWarps = 4;
 constexpr int kConvThreads = 32 * kConvWarps;
 #ifndef ICV_ROWS_EPI
@@ -58,8 +67,8 @@ constexpr int kMmaWarpR = kConvWarps + kEpiWarpsR;
 constexpr int kLoadWarpR = kMmaWarpR + 1;
 constexpr int kThreadsR = 32 * (kLoadWarpR + 1);
 constexpr int kMDone = 4;                 // MMA-done barriers (tile k -> k % 4)
-constexpr int kStagesR = 6;               // raw-row stages in flight (the loader runs this many tiles ahead)
-constexpr int kRowsReady = 8;             // converted-tile barriers (converters run up to kLag + 1 tiles ahead of the MMA)
+constexpr int kStagesR = ICV_ROWS_STAGES;             // raw-row stages in flight (the loader runs this many tiles ahead)
+constexpr int kRowsReady = ICV_ROWS_READY;            // converted-tile barriers (converters run up to kLag + 1 tiles ahead of the MMA)
 // TMEM accumulators (the MMA may run kAccR tiles ahead of the epilogue)
 template <int BN>
 constexpr int kAccRFor = BN <= 64 ? 8 : 4;
@@ -138,7 +147,7 @@ struct TileWalk {
   }
 };
 
-template <int BN, int kR, int kKS, int kC>
+template <int BN, int kR, int kKS, int kC, int kRing>
 __global__ void __launch_bounds__(kThreadsR, 1) igemm_rows_kernel(const __grid_constant__ CUtensorMap tmap_y,
                                                                   const RowsArgs a, const RowsPlan pl) {
   constexpr int kAccR = kAccRFor<BN>;
@@ -368,7 +377,7 @@ __global__ void __launch_bounds__(kThreadsR, 1) igemm_rows_kernel(const __grid_c
   }
 }
 
-bool plan_rows(const ConvArgs& c, int BN, int tpr, RowsPlan* p, int* ring_row_bytes) {
+bool plan_rows(const ConvArgs& c, int BN, int tpr, int kRing, RowsPlan* p, int* ring_row_bytes) {
   const int ring_px_needed = 2 * (tpr * kBM - 1) + 8;
   int ring_px = ring_px_needed > c.g.PL + (int)c.g.W ? ring_px_needed : c.g.PL + (int)c.g.W;
   ring_px = (ring_px + 1) / 2 * 2;   // 16-byte rows
@@ -390,13 +399,9 @@ bool plan_rows(const ConvArgs& c, int BN, int tpr, RowsPlan* p, int* ring_row_by
   return p->bytes <= 232448;
 }
 
-template <int BN, int kR, int kKS, int kC>
-int launch_rows_t(const ConvArgs& c, cudaStream_t st) {
-  const int tpr = (int)((c.g.OW + kBM - 1) / kBM);
-  RowsPlan pl;
-  int ring_row_bytes = 0;
-  if (!plan_rows(c, BN, tpr, &pl, &ring_row_bytes)) return fail(ICV_ERR_UNSUPPORTED, "row kernel: smem plan");
-  auto kernel = igemm_rows_kernel<BN, kR, kKS, kC>;
+template <int BN, int kR, int kKS, int kC, int kRing>
+int launch_rows_ring(const ConvArgs& c, cudaStream_t st, const RowsPlan& pl, int ring_row_bytes, int tpr) {
+  auto kernel = igemm_rows_kernel<BN, kR, kKS, kC, kRing>;
   static std::once_flag once;
   static cudaError_t err = cudaSuccess;
   std::call_once(once, [&] { err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448); });
@@ -440,6 +445,20 @@ int launch_rows_t(const ConvArgs& c, cudaStream_t st) {
   kernel<<<grid, kThreadsR, pl.bytes, st>>>(tmap_y, a, pl);
   note_launch();
   return cuda_check(cudaGetLastError(), "igemm_rows launch");
+}
+
+// The deeper ring (converters up to kAccR - 1 tiles ahead of the MMA: cfg3a
+// 30.8 -> 28.7 us) when the smem plan fits, else 16 rows (wide input rows).
+template <int BN, int kR, int kKS, int kC>
+int launch_rows_t(const ConvArgs& c, cudaStream_t st) {
+  const int tpr = (int)((c.g.OW + kBM - 1) / kBM);
+  RowsPlan pl;
+  int ring_row_bytes = 0;
+  if (plan_rows(c, BN, tpr, kRingBig, &pl, &ring_row_bytes))
+    return launch_rows_ring<BN, kR, kKS, kC, kRingBig>(c, st, pl, ring_row_bytes, tpr);
+  if (plan_rows(c, BN, tpr, 16, &pl, &ring_row_bytes))
+    return launch_rows_ring<BN, kR, kKS, kC, 16>(c, st, pl, ring_row_bytes, tpr);
+  return fail(ICV_ERR_UNSUPPORTED, "row kernel: smem plan");
 }
 
 }  // namespace

@@ -789,7 +789,8 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
             }
           } else {
             const int4* cst4 = reinterpret_cast<const int4*>(sBias + n0);
-            const long long corr = -(long long)a.t.zw * rowsum;
+            // exact mod 2^32: the true accumulator fits int32
+            const uint32_t corr = 0u - (uint32_t)a.t.zw * (uint32_t)rowsum;
 #pragma unroll
             for (int qd = 0; qd < 8; ++qd) {
               int4 b = cst4[qd];
@@ -807,7 +808,7 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
               uint32_t word = 0;
 #pragma unroll
               for (int h = 0; h < 4; ++h) {
-                const int32_t acc = (int32_t)((long long)(int32_t)v[4 * qd + h] + bb[h] + corr);
+                const int32_t acc = (int32_t)(v[4 * qd + h] + (uint32_t)bb[h] + corr);
 #ifndef ICV_WEXP_NOREQ
                 word |= (uint32_t)requant_u8(acc, a.t.m0, a.t.shift, a.t.zo, a.t.qmin, a.t.qmax) << (8 * h);
 #else   // experiment: no requantization (timing only)
