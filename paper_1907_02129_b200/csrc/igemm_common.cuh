@@ -60,6 +60,7 @@ struct TcArgs {
   int32_t tiles_per_row;     // row-tiled kernels: tile = (output row, 128-pixel block); 3-D output map
   int32_t ow;                // row-tiled kernels: output row width (pixels >= ow are not stored)
   int64_t ohw, img_elems;    // Ho*Wo, H*W*C
+  int32_t oh;                // row-pair tiles (kSubRows 2): output rows per image
 };
 
 // Where the references of output pixel p = tile_m*128 + row live: entry of
@@ -142,7 +143,7 @@ constexpr int kEpiWarpBytes = kI8 ? 2048 : 4096;
 // alternate tiles (each warp all BN columns of its 32 rows), so several
 // tiles are in the epilogue at once; otherwise extra warps split columns.
 template <bool kI8, int BN, int kEpiWarps, int kAccStride, typename Sched = StridedTiles, int kAccStages = 2,
-          bool kRowTiles = false, int kTileGroups = 1>
+          bool kRowTiles = false, int kTileGroups = 1, int kSubRows = 1>
 __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane, uint32_t tmem_base, uint8_t* sEpi,
                                               const uint32_t* sBias, uint64_t* tfull, uint64_t* tempty,
                                               Sched sched = Sched{0}, const CUtensorMap* tmap_y = nullptr,
@@ -168,11 +169,15 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
 #ifdef ICV_ROWS_PHASES
   long long _et = clock64(), _ep[6] = {0, 0, 0, 0, 0, 0};
 #endif
-  if constexpr (kTileGroups > 1) {   // this group's first tile
+  // kSubRows 2 (row-tiled, two groups): a tile covers two output rows, one
+  // accumulator each; group g stores row g of every tile
+  static_assert(kSubRows == 1 || (kRowTiles && kTileGroups == 2), "sub-rows: one group per row");
+  constexpr int kTileStep = kSubRows > 1 ? 1 : kTileGroups;
+  if constexpr (kTileGroups > 1 && kSubRows == 1) {   // this group's first tile
     as = group % kAccStages;
     aphase = (uint32_t)(group / kAccStages) & 1u;
   }
-  for (int64_t ti = group; ti < n_local; ti += kTileGroups) {
+  for (int64_t ti = kSubRows > 1 ? 0 : group; ti < n_local; ti += kTileStep) {
     const int64_t tile = sched(ti);
     const int64_t mt = a.n_tiles == 1 ? tile : tile / a.n_tiles;
     const int nt = a.n_tiles == 1 ? 0 : (int)(tile - mt * a.n_tiles);
@@ -192,12 +197,20 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
     // first pixel of this warp's rows; row-tiled: (output row, first pixel of the block)
     int64_t row0 = mt * kBM + slot * 32;
     int32_t rt_row = 0, rt_ox0 = 0;
+    bool row_valid = true;
     if constexpr (kRowTiles) {
       rt_row = (int32_t)((uint32_t)mt / (uint32_t)a.tiles_per_row);
       rt_ox0 = ((int32_t)mt - rt_row * a.tiles_per_row) * kBM + slot * 32;
+      if constexpr (kSubRows > 1) {   // rt_row is a row-pair index: (image, output row 2 * pair + group)
+        const int32_t ohp = (a.oh + 1) >> 1;
+        const int32_t img = (int32_t)((uint32_t)rt_row / (uint32_t)ohp);
+        const int32_t oy = 2 * (rt_row - img * ohp) + group;
+        row_valid = oy < a.oh;
+        rt_row = img * a.oh + oy;
+      }
       row0 = (int64_t)rt_row * a.ow + rt_ox0;
     }
-    const uint32_t taddr = tmem_base + ((uint32_t)(slot * 32) << 16) + as * kAccStride;
+    const uint32_t taddr = tmem_base + ((uint32_t)(slot * 32) << 16) + as * kAccStride + (kSubRows > 1 ? group * BN : 0);
     int32_t rowsum = 0;
     if constexpr (kI8) {
       uint32_t rs;
@@ -210,7 +223,7 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
     const int nchunks = 0;
     (void)cols_left;
 #else
-    const int nchunks = cols_left > 0 ? (min(kColsPerWarp, cols_left) + 31) / 32 : 0;
+    const int nchunks = cols_left > 0 && row_valid ? (min(kColsPerWarp, cols_left) + 31) / 32 : 0;
 #endif
     uint32_t v[32];
     if (nchunks > 0) {
@@ -334,7 +347,9 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
     }
 #endif
     if (ew == 0 && lane == 0 && ti_ < 8) TRACE(18 + ti_);
-    if constexpr (kTileGroups > 1) {
+    if constexpr (kSubRows > 1) {
+      if (++as == kAccStages) { as = 0; aphase ^= 1; }
+    } else if constexpr (kTileGroups > 1) {
       static_assert(kAccStages % kTileGroups == 0, "groups must map to fixed accumulator stages");
       as += kTileGroups;
       if (as >= kAccStages) { as -= kAccStages; aphase ^= 1; }

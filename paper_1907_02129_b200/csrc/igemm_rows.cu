@@ -77,6 +77,7 @@ struct RowsArgs {
   TcArgs t;                     // epilogue fields (y, K, bias, n_tiles = 1, tiles_per_row, P)
   const uint8_t* wrows;         // packed row-sliding filter: [R][BN/8][4][8][8] bf16
   int32_t H, W, C, R, S, PT, PL, OH, tpr;
+  int32_t rp, OHT;              // output rows per tile (1 or 2), row tiles per image = ceil(OH / rp)
   int32_t ring_row_bytes;       // 8 * padded pixels
   int32_t row_bytes;            // W * C * 2 (one raw input row)
   int32_t ksteps;               // MMA K steps per kernel row (1 or 2)
@@ -120,8 +121,8 @@ struct TileWalk {
   __device__ __forceinline__ void start(const RowsArgs& a, int64_t t0) {
     const int32_t row = (int32_t)(t0 / a.tpr);
     oxb = (int32_t)(t0 - (int64_t)row * a.tpr);
-    n = row / a.OH;
-    oy = row - n * a.OH;
+    n = row / a.OHT;
+    oy = (row - n * a.OHT) * a.rp;
     prev_n = -1;
     prev_hi = -1;
   }
@@ -132,8 +133,9 @@ struct TileWalk {
     r.oy = oy;
     r.oxb = oxb;
     const int32_t first = 2 * oy - a.PT;
+    const int32_t nrows = min(a.rp, a.OH - oy);
     r.lo = max(first, 0);
-    r.hi = min(first + a.R - 1, a.H - 1);
+    r.hi = min(first + 2 * (nrows - 1) + a.R - 1, a.H - 1);
     r.fresh = prev_n != n;
     r.new_lo = r.fresh ? r.lo : max(r.lo, prev_hi + 1);
     r.new_hi = r.hi;
@@ -141,22 +143,23 @@ struct TileWalk {
     prev_hi = r.hi;
     if (++oxb == a.tpr) {
       oxb = 0;
-      if (++oy == a.OH) { oy = 0; ++n; }
+      oy += a.rp;
+      if (oy >= a.OH) { oy = 0; ++n; }
     }
     return r;
   }
 };
 
-template <int BN, int kR, int kKS, int kC, int kRing>
+template <int BN, int kR, int kKS, int kC, int kRing, int kRP>
 __global__ void __launch_bounds__(kThreadsR, 1) igemm_rows_kernel(const __grid_constant__ CUtensorMap tmap_y,
                                                                   const RowsArgs a, const RowsPlan pl) {
-  constexpr int kAccR = kAccRFor<BN>;
+  constexpr int kAccR = kAccRFor<BN> / kRP;   // tiles in TMEM (kRP accumulators each)
   // Ring-slot reuse: the 2 rows tile k adds evict rows last read by tile
   // k - (kRing + 1 - kR) / 2 or earlier, so within an image the converters
   // only wait for the MMAs of tile k - kLag (bounded by the accumulator ring
   // so the tfull phase they wait on is unambiguous); a new image may evict
   // anything, so its first tile waits for all earlier MMAs.
-  constexpr int kLagRing = (kRing + 1 - kR) / 2;
+  constexpr int kLagRing = (kRing + 1 - (kR + 2 * (kRP - 1))) / (2 * kRP);
   constexpr int kLagCap = kAccR - 1 < kRowsReady - 2 ? kAccR - 1 : kRowsReady - 2;
   constexpr int kLag = kLagRing < kLagCap ? kLagRing : kLagCap;
   static_assert(kLag + 2 <= kRowsReady, "rows_ready phases must stay unambiguous");
@@ -195,7 +198,7 @@ __global__ void __launch_bounds__(kThreadsR, 1) igemm_rows_kernel(const __grid_c
     for (int s = 0; s < kRowsReady; ++s) mbar_init(&rows_ready[s], kConvWarps);
     for (int s = 0; s < kAccR; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 4);   // one arrival per warp of the epilogue group that owns the tile
+      mbar_init(&tempty[s], 4 * kRP);   // one arrival per warp of the epilogue group(s) storing the tile
     }
     for (int s = 0; s < kMDone; ++s) mbar_init(&mdone[s], 1);
     mbar_init(bfull, 1);
@@ -206,7 +209,7 @@ __global__ void __launch_bounds__(kThreadsR, 1) igemm_rows_kernel(const __grid_c
   for (int i = threadIdx.x; i < (kRing + 1) * a.ring_row_bytes / 16; i += blockDim.x)
     sts128(ring_u32 + i * 16, 0u, 0u, 0u, 0u);
   fence_proxy_async_smem();
-  if (warp == kMmaWarpR) tmem_alloc<(kAccR * BN <= 256 ? 256 : 512)>(tmem_slot);
+  if (warp == kMmaWarpR) tmem_alloc<(kAccR * kRP * BN <= 256 ? 256 : 512)>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -331,25 +334,28 @@ __global__ void __launch_bounds__(kThreadsR, 1) igemm_rows_kernel(const __grid_c
       tc_fence_after();
       RP_ACC(3);
       if (elect_one()) {
-        const uint32_t d = tmem_base + as * BN;
         const uint32_t col0 = (uint32_t)tr.oxb * kBM * 2 * 8;   // padded pixel 2*ox of the tile's first pixel
-        // all row addresses first (independent), then kR*kKS back-to-back MMAs
-        uint32_t rowa[kR];
 #pragma unroll
-        for (int ky = 0; ky < kR; ++ky) {
-          const int32_t iy = 2 * tr.oy - a.PT + ky;
-          rowa[ky] = (iy >= 0 && iy < a.H) ? ring_u32 + (uint32_t)(iy & (kRing - 1)) * a.ring_row_bytes + col0
-                                           : zero_row;
-        }
+        for (int sr = 0; sr < kRP; ++sr) {   // output row oy + sr -> accumulator sr of the tile
+          const uint32_t d = tmem_base + (as * kRP + sr) * BN;
+          // all row addresses first (independent), then kR*kKS back-to-back MMAs
+          uint32_t rowa[kR];
 #pragma unroll
-        for (int ky = 0; ky < kR; ++ky) {
+          for (int ky = 0; ky < kR; ++ky) {
+            const int32_t iy = 2 * (tr.oy + sr) - a.PT + ky;
+            rowa[ky] = (iy >= 0 && iy < a.H) ? ring_u32 + (uint32_t)(iy & (kRing - 1)) * a.ring_row_bytes + col0
+                                             : zero_row;
+          }
 #pragma unroll
-          for (int j = 0; j < kKS; ++j) {
-            const uint64_t ad = adesc0 + ((rowa[ky] + 32 * j) >> 4);
-            const uint64_t bd = bdesc0 + ((ky * BN * 64 + j * 256) >> 4);
+          for (int ky = 0; ky < kR; ++ky) {
+#pragma unroll
+            for (int j = 0; j < kKS; ++j) {
+              const uint64_t ad = adesc0 + ((rowa[ky] + 32 * j) >> 4);
+              const uint64_t bd = bdesc0 + ((ky * BN * 64 + j * 256) >> 4);
 #ifndef ICV_EXP_NOMMA
-            tc_mma<false>(d, ad, bd, idesc, (ky | j) != 0 ? 1u : 0u);
+              tc_mma<false>(d, ad, bd, idesc, (ky | j) != 0 ? 1u : 0u);
 #endif
+            }
           }
         }
 #ifdef ICV_ROWS_PHASES
@@ -364,7 +370,8 @@ __global__ void __launch_bounds__(kThreadsR, 1) igemm_rows_kernel(const __grid_c
     }
     RP_FLUSH(38, lane == 0);
   } else {
-    epilogue_loop<false, BN, kEpiWarpsR, BN, RowTiles, kAccR, true, kEpiWarpsR / 4>(a.t, warp - kConvWarps, lane, tmem_base, sEpi, sBias,
+    static_assert(kRP == 1 || kEpiWarpsR == 8, "row pairs: one epilogue group per row");
+    epilogue_loop<false, BN, kEpiWarpsR, BN * kRP, RowTiles, kAccR, true, kEpiWarpsR / 4, kRP>(a.t, warp - kConvWarps, lane, tmem_base, sEpi, sBias,
                                                                  tfull, tempty, sched,
                                                                  a.t.use_tma_y ? &tmap_y : nullptr);
   }
@@ -373,18 +380,18 @@ __global__ void __launch_bounds__(kThreadsR, 1) igemm_rows_kernel(const __grid_c
   __syncthreads();
   if (warp == kMmaWarpR) {
     tc_fence_after();
-    tmem_dealloc<(kAccR * BN <= 256 ? 256 : 512)>(tmem_base);
+    tmem_dealloc<(kAccR * kRP * BN <= 256 ? 256 : 512)>(tmem_base);
   }
 }
 
-bool plan_rows(const ConvArgs& c, int BN, int tpr, int kRing, RowsPlan* p, int* ring_row_bytes) {
+bool plan_rows(const ConvArgs& c, int BN, int tpr, int kRing, int rp, RowsPlan* p, int* ring_row_bytes) {
   const int ring_px_needed = 2 * (tpr * kBM - 1) + 8;
   int ring_px = ring_px_needed > c.g.PL + (int)c.g.W ? ring_px_needed : c.g.PL + (int)c.g.W;
   ring_px = (ring_px + 1) / 2 * 2;   // 16-byte rows
   *ring_row_bytes = ring_px * 8;
   const int b = c.g.R * BN * 64;
   const int ring = (kRing + 1) * *ring_row_bytes;
-  const int stage = (c.g.R * (int)c.g.W * c.g.C * 2 + 15) / 16 * 16;
+  const int stage = ((c.g.R + 2 * (rp - 1)) * (int)c.g.W * c.g.C * 2 + 15) / 16 * 16;   // a fresh tile's rows
   const int epi = kEpiWarpsR * kEpiWarpBytes<false>;
   (void)BN;
   int off = 0;
@@ -399,9 +406,9 @@ bool plan_rows(const ConvArgs& c, int BN, int tpr, int kRing, RowsPlan* p, int* 
   return p->bytes <= 232448;
 }
 
-template <int BN, int kR, int kKS, int kC, int kRing>
+template <int BN, int kR, int kKS, int kC, int kRing, int kRP>
 int launch_rows_ring(const ConvArgs& c, cudaStream_t st, const RowsPlan& pl, int ring_row_bytes, int tpr) {
-  auto kernel = igemm_rows_kernel<BN, kR, kKS, kC, kRing>;
+  auto kernel = igemm_rows_kernel<BN, kR, kKS, kC, kRing, kRP>;
   static std::once_flag once;
   static cudaError_t err = cudaSuccess;
   std::call_once(once, [&] { err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448); });
@@ -423,7 +430,10 @@ int launch_rows_ring(const ConvArgs& c, cudaStream_t st, const RowsPlan& pl, int
   a.ring_row_bytes = ring_row_bytes;
   a.row_bytes = (int32_t)(c.g.W * c.g.C * 2);
   a.ksteps = c.g.S * 4 <= 16 ? 1 : 2;
-  a.total_tiles = c.P / c.g.OW * tpr;
+  a.rp = kRP;
+  a.OHT = (int32_t)((c.g.OH + kRP - 1) / kRP);
+  a.t.oh = (int32_t)c.g.OH;
+  a.total_tiles = c.P / (c.g.OH * c.g.OW) * a.OHT * tpr;
   // 3-D output view (channel, pixel in the row, output row)
   CUtensorMap tmap_y;
   {
@@ -454,10 +464,18 @@ int launch_rows_t(const ConvArgs& c, cudaStream_t st) {
   const int tpr = (int)((c.g.OW + kBM - 1) / kBM);
   RowsPlan pl;
   int ring_row_bytes = 0;
-  if (plan_rows(c, BN, tpr, kRingBig, &pl, &ring_row_bytes))
-    return launch_rows_ring<BN, kR, kKS, kC, kRingBig>(c, st, pl, ring_row_bytes, tpr);
-  if (plan_rows(c, BN, tpr, 16, &pl, &ring_row_bytes))
-    return launch_rows_ring<BN, kR, kKS, kC, 16>(c, st, pl, ring_row_bytes, tpr);
+  // opt-in ICV_ROWS_RP=2: tiles of two output rows (half the per-tile
+  // hand-offs; BN 64: 8 accumulators = 4 tile pairs).  Correct, measured
+  // slower (cfg3a 30.8 vs 28.7 us): the kernel is bound by shared-memory
+  // bandwidth per output row, not by hand-offs per tile
+  const char* rpe = getenv("ICV_ROWS_RP");
+  const bool rp2 = BN == 64 && rpe && rpe[0] == '2';
+  if (rp2 && plan_rows(c, BN, tpr, kRingBig, 2, &pl, &ring_row_bytes))
+    return launch_rows_ring<BN, kR, kKS, kC, kRingBig, 2>(c, st, pl, ring_row_bytes, tpr);
+  if (plan_rows(c, BN, tpr, kRingBig, 1, &pl, &ring_row_bytes))
+    return launch_rows_ring<BN, kR, kKS, kC, kRingBig, 1>(c, st, pl, ring_row_bytes, tpr);
+  if (plan_rows(c, BN, tpr, 16, 1, &pl, &ring_row_bytes))
+    return launch_rows_ring<BN, kR, kKS, kC, 16, 1>(c, st, pl, ring_row_bytes, tpr);
   return fail(ICV_ERR_UNSUPPORTED, "row kernel: smem plan");
 }
 

@@ -486,8 +486,12 @@ def _stem_problem(g, index_dtype=torch.int64, per_image=True, seed=13):
     dict(r=3, s=3, sy=2, sx=2, pt=1, pl=1, c=3, k=64, n=2, h=80, w=72),     # 3x3/2 (one K step)
     dict(r=7, s=7, sy=2, sx=2, pt=2, pl=4, pb=4, pr=1, c=3, k=64, n=2, h=70, w=80),   # asymmetric padding
 ])
-@pytest.mark.parametrize("per_image,index_dtype", [(True, torch.int64), (False, torch.int64), (True, torch.int32)])
-def test_rows_kernel_matches_oracle(geom, per_image, index_dtype):
+@pytest.mark.parametrize("per_image,index_dtype,rows_per_tile", [(True, torch.int64, "1"), (False, torch.int64, "1"),
+                                                                 (True, torch.int32, "1"), (True, torch.int64, "2")])
+def test_rows_kernel_matches_oracle(geom, per_image, index_dtype, rows_per_tile, monkeypatch):
+    """rows_per_tile 2: the opt-in two-output-row tiles (ICV_ROWS_RP=2; BN 64
+    filters only, others keep one row per tile)."""
+    monkeypatch.setenv("ICV_ROWS_RP", rows_per_tile)
     p, shape, xh, wh, bias, x, pf, ib, tile, o = _stem_problem(geom, index_dtype, per_image)
     assert L.kernel_name(p, shape, torch.bfloat16) == "icv_igemm_rows<bf16>"
     y = icv.indirect_conv(x, pf, ib, p, tile).numpy().reshape(-1, p.out_channels)
