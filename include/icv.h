@@ -196,6 +196,15 @@ ICV_API int64_t icv_launch_count(void);
 ICV_API int icv_maxpool2d(const icv_shape4* in, int32_t kh, int32_t kw, int32_t sh, int32_t sw, int32_t ph,
                           int32_t pw, int32_t dtype, const void* x, void* y, void* stream);
 
+/* ---- GEMM-based baseline: im2row patch matrix (reference im2col.py:48-114) --
+ * Writes the (batch*OH*OW) x (R*S*C) patch matrix of `x` (dtype ICV_F32 /
+ * ICV_BF16 / ICV_U8, NHWC): row p = output pixel, column e*C + c = tap e's
+ * channel c, padding taps = `zero_row` (C elements) or zeros when NULL.
+ * Replaces build_patch_matrix's copy loop (im2col.py:86-113); the paper's
+ * GEMM baseline multiplies it with the filter (gemm_conv, im2col.py:117-131). */
+ICV_API int icv_im2col(const icv_conv_desc* desc, const icv_shape4* in, int64_t batch, int32_t dtype, const void* x,
+                       const void* zero_row, void* patches, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -68,6 +68,7 @@ SIGNATURES = {
                                             ctypes.POINTER(ctypes.c_char_p)]),
     "icv_launch_count": (_I64, []),
     "icv_maxpool2d": (ctypes.c_int, [ctypes.POINTER(Shape), _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P, _P, _P]),
+    "icv_im2col": (ctypes.c_int, [ctypes.POINTER(Desc), ctypes.POINTER(Shape), _I64, _I32, _P, _P, _P, _P]),
 }
 
 _lock = threading.Lock()

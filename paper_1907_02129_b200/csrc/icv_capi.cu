@@ -162,6 +162,17 @@ ICV_API int icv_device_info(int32_t device, int32_t* sm_count, int32_t* cc_major
   return ICV_OK;
 }
 
+ICV_API int icv_im2col(const icv_conv_desc* desc, const icv_shape4* in, int64_t batch, int32_t dtype, const void* x,
+                       const void* zero_row, void* patches, void* stream) {
+  Geom g;
+  if (int s = make_geom(desc, in, &g)) return s;
+  if (!x || !patches) return fail(ICV_ERR_ARG, "icv_im2col: null tensor");
+  if (batch < 1 || batch > in->n) return fail(ICV_ERR_ARG, "batch must be within the physical input batch");
+  const int elem = dtype == ICV_F32 ? 4 : dtype == ICV_BF16 ? 2 : dtype == ICV_U8 ? 1 : 0;
+  if (elem == 0) return fail(ICV_ERR_ARG, "icv_im2col: unsupported dtype");
+  return launch_im2col(g, batch, elem, x, zero_row, patches, static_cast<cudaStream_t>(stream));
+}
+
 ICV_API int icv_out_shape(const icv_conv_desc* desc, const icv_shape4* in, icv_shape4* out) {
   Geom g;
   if (int s = make_geom(desc, in, &g)) return s;

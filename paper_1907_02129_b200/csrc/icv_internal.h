@@ -14,6 +14,9 @@ void set_error(const std::string& msg);
 int fail(int status, const std::string& msg);
 int cuda_check(cudaError_t e, const char* what);
 void note_launch(int n = 1);
+struct Geom;
+int launch_im2col(const Geom& g, int64_t batch, int elem, const void* x, const void* zero, void* out,
+                  cudaStream_t st);
 int launch_maxpool(const icv_shape4& in, int kh, int kw, int sh, int sw, int ph, int pw, int dtype, const void* x,
                    void* y, cudaStream_t st);
 

@@ -46,8 +46,11 @@ constexpr int kEpiWarpsS = kI8 ? 8 : 4;
 #ifndef ICV_PROD_WARPS_BF16
 #define ICV_PROD_WARPS_BF16 4   // 8 measured equal on cfg2 / cfg3b (the fill is L2->SM bound, not issue bound)
 #endif
+#ifndef ICV_PROD_WARPS_U8
+#define ICV_PROD_WARPS_U8 4
+#endif
 template <bool kI8>
-constexpr int kProdWarpsS = kI8 ? 4 : ICV_PROD_WARPS_BF16;
+constexpr int kProdWarpsS = kI8 ? ICV_PROD_WARPS_U8 : ICV_PROD_WARPS_BF16;
 template <bool kI8, int kEpiW = kEpiWarpsS<kI8>>
 constexpr int kMmaWarpS = kProdWarpsS<kI8> + kEpiW;
 template <bool kI8, int kEpiW = kEpiWarpsS<kI8>>

@@ -73,6 +73,7 @@ class PackedFilter:
     packed: torch.Tensor          # uint8 device buffer written by icv_pack_filter
     bias: torch.Tensor            # host copy of the caller's bias (float32 / int32)
     quant: QuantParams | None = None
+    source: torch.Tensor | None = None   # the KRSC weights on the device (GEMM-baseline repack, im2col.py)
 
     @property
     def reduction_len(self) -> int:
@@ -150,4 +151,4 @@ def pack_filter(filt: FilterTensor, bias, params: ConvParams, tile: TileConfig, 
     # keep the temporaries alive until the packing kernels have consumed them
     torch.cuda.current_stream(device).synchronize()
     return PackedFilter(k, params.kernel_elems, params.in_channels, tile.nr, compute_dtype, params, packed,
-                        bias_t, quant)
+                        bias_t, quant, source=w)
