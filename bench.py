@@ -444,6 +444,28 @@ def gpu_bench(args) -> None:
                             "roofline": roofline_for(ow_, oms, peaks)}
             del ox, opf, oib_, oy
         other["cfg5"] = stack_bench(device, peaks, flush)
+        # the paper's comparison: the GEMM-based variant (im2row patch matrix in
+        # HBM + the same tcgen05 GEMM as a 1x1 conv over it) on the headline workload
+        if not w.params.is_pointwise_unit_stride():
+            pm = icv.build_patch_matrix(x, w.params)
+            icv.gemm_only(pm, pf, tile)
+
+            def gemm_step():
+                icv.build_patch_matrix(x, w.params, out=pm)
+                icv.gemm_only(pm, pf, tile)
+
+            gt = time_steps(gemm_step, max(10, args.steps // 5), 3, flush)
+            gms = statistics.median(gt)
+            other["im2col_gemm_" + name] = {
+                "workload": w.name, "dtype": w.dtype, "ms_per_step": round(gms, 5),
+                "value": round(w.flops / (gms * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
+                "kernels": ["icv_im2col", _lib.kernel_name(icv.ConvParams(1, 1, in_channels=pm.cols,
+                                                                            out_channels=pf.k_out),
+                                                          icv.Shape4(1, 1, pm.rows, pm.cols), x.dtype)],
+                "patch_matrix_mb": round(pm.allocated_bytes / 1e6, 2),
+                "indirect_speedup": None,   # filled below from the headline ms
+                "note": "reference im2col.py gemm_conv: patch matrix built every step (build_patch_matrix + gemm_only)"}
+            del pm
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -458,6 +480,9 @@ def gpu_bench(args) -> None:
     ms_step = total_ms / args.steps
     med = statistics.median(times)
     roof = roofline_for(w0, statistics.mean(times), peaks)
+    for k, v in other.items():
+        if k.startswith("im2col_gemm_"):
+            v["indirect_speedup"] = round(v["ms_per_step"] / med, 3)
     roof["traffic"] = load_traffic(w0.name)
     roof["peak_source"] = peaks["which"] + " (MEASURED_PEAKS.json bf16_tflops burst / hbm_gbs)"
     line = {
