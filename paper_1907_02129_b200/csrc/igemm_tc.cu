@@ -63,7 +63,10 @@ struct CfgS {
   // One smem slot = one 128-byte K block of A (128 rows) and of B (BN rows).
   // A stage groups kKB slots behind one full/empty barrier pair so the MMA
   // warp pays one barrier round trip per kKB*4 MMAs.
-  static constexpr int kKB = BN >= 256 ? 1 : 2;
+#ifndef ICV_KKB
+#define ICV_KKB 2
+#endif
+  static constexpr int kKB = BN >= 256 ? 1 : ICV_KKB;
   static constexpr int kSlotBytes = kABytes + kBBytes;
 #ifndef ICV_MAX_SLOTS
 #define ICV_MAX_SLOTS 8
