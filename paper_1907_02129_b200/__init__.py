@@ -10,6 +10,7 @@ for allocation, streams and torch.distributed only.
 
 from .errors import InvalidGeometryError, NativeLibraryError, StaleBufferError, UnsupportedError
 from .gemm import PackedFilter, QuantParams, TileConfig, pack_filter
+from .ib_cache import CacheStats, IndirectionCache
 from .im2col import PatchMatrix, build_patch_matrix, gemm_conv, gemm_only
 from .indirect import (
     ZERO_REF,
@@ -34,7 +35,7 @@ from .tensors import (
 __version__ = "0.1.0"
 
 __all__ = [
-    "ZERO_REF", "ConvParams", "FilterTensor", "PatchMatrix", "build_patch_matrix", "gemm_conv", "gemm_only", "IndirectionBuffer", "InvalidGeometryError",
+    "ZERO_REF", "CacheStats", "ConvParams", "FilterTensor", "IndirectionCache", "PatchMatrix", "build_patch_matrix", "gemm_conv", "gemm_only", "IndirectionBuffer", "InvalidGeometryError",
     "NativeLibraryError", "NhwcTensor", "PackedFilter", "QuantParams", "Shape4", "StaleBufferError",
     "TileConfig", "UnsupportedError", "conv_output_shape", "filter_fill_random", "indirect_conv",
     "init_indirection_buffer", "make_zero_row", "pack_filter", "rebind_input", "tensor_fill_random",
