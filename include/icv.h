@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define ICV_ABI_VERSION 1
+#define ICV_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define ICV_API __attribute__((visibility("default")))
@@ -77,6 +77,12 @@ typedef enum icv_dtype {
  * prescribe for quantized padding).  Windowed layers may then zero-fill
  * padding and add the packed per-tap correction zx * sum_c (w - zw). */
 #define ICV_ZERO_ROW_ZP 0x800
+
+/* Flag OR-ed into icv_conv's `ib_dtype`: run the IB-gather kernels (every
+ * A row fetched through its indirection-buffer entry, the paper's mainloop),
+ * not the window / row-sliding / dense-A specialisations that a canonical
+ * buffer otherwise permits.  For measuring the indirect algorithm itself. */
+#define ICV_PREFER_GATHER 0x1000
 
 /* Convolution geometry; field-for-field convbench.tensors.ConvParams
  * (tensors.py:41-72). */
@@ -180,10 +186,19 @@ ICV_API int icv_conv(const icv_conv_desc* desc, const icv_shape4* in, int64_t ba
              const icv_quant* quant, void* y, void* stream);
 
 /* Which kernel icv_conv would launch for this problem (for tests/benches)
- * with a canonical buffer (ICV_IB_CANONICAL, as init_indirection_buffer
- * builds) and a 16-byte aligned input: writes a static NUL-terminated name
- * into *name. */
-ICV_API int icv_conv_kernel_name(const icv_conv_desc* desc, const icv_shape4* in, int32_t dtype, const char** name);
+ * given the layout flags of its `ib_dtype` argument (ICV_IB_CANONICAL,
+ * ICV_ZERO_ROW_ZEROS, ICV_PREFER_GATHER, ...) and 16-byte aligned tensors:
+ * writes a static NUL-terminated name into *name. */
+ICV_API int icv_conv_kernel_name(const icv_conv_desc* desc, const icv_shape4* in, int32_t dtype, int32_t flags,
+                                 const char** name);
+
+/* Plan knobs for A/B measurement (DESIGN.md §4 lists them; the defaults are
+ * the measured-best plans): set / read a process-wide value by name.
+ * Unknown names return ICV_ERR_ARG; a negative value restores the default
+ * (except "win", where -1 is the default "auto").  Not synchronized with
+ * concurrent icv_conv calls: set knobs before launching. */
+ICV_API int icv_set_tuning(const char* key, int32_t value);
+ICV_API int icv_get_tuning(const char* key, int32_t* value);
 
 /* Launch counter: number of kernels this library has launched in this
  * process (all entry points).  For the bench's gpu_launches claim. */

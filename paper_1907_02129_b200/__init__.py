@@ -16,6 +16,7 @@ from .indirect import (
     ZERO_REF,
     IndirectionBuffer,
     indirect_conv,
+    indirect_gemm_microkernel,
     init_indirection_buffer,
     make_zero_row,
     rebind_input,
@@ -38,6 +39,6 @@ __all__ = [
     "ZERO_REF", "CacheStats", "ConvParams", "FilterTensor", "IndirectionCache", "PatchMatrix", "build_patch_matrix", "gemm_conv", "gemm_only", "IndirectionBuffer", "InvalidGeometryError",
     "NativeLibraryError", "NhwcTensor", "PackedFilter", "QuantParams", "Shape4", "StaleBufferError",
     "TileConfig", "UnsupportedError", "conv_output_shape", "filter_fill_random", "indirect_conv",
-    "init_indirection_buffer", "make_zero_row", "pack_filter", "rebind_input", "tensor_fill_random",
+    "indirect_gemm_microkernel", "init_indirection_buffer", "make_zero_row", "pack_filter", "rebind_input", "tensor_fill_random",
     "tensor_fill_sequential", "update_for_batch_growth",
 ]

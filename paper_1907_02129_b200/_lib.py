@@ -9,6 +9,7 @@ raises :class:`NativeLibraryError`.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import os
 import threading
@@ -25,6 +26,7 @@ ICV_IB_PER_IMAGE = 0x100
 ICV_IB_CANONICAL = 0x200   # buffer is exactly icv_ib_build's output (row-sliding kernels may use it)
 ICV_ZERO_ROW_ZEROS = 0x400  # bound zero row is all zero bytes (window kernels may zero-fill padding)
 ICV_ZERO_ROW_ZP = 0x800     # uint8: every zero-row byte is the input zero point (zero fill + per-tap correction)
+ICV_PREFER_GATHER = 0x1000  # run the IB-gather kernels (no window / row-sliding / dense-A specialisation)
 
 TORCH_TO_ICV = {torch.float32: ICV_F32, torch.bfloat16: ICV_BF16, torch.uint8: ICV_U8,
                 torch.int32: ICV_I32, torch.int64: ICV_I64}
@@ -64,8 +66,10 @@ SIGNATURES = {
     "icv_requant_params": (ctypes.c_int, [_F32, _F32, _F32, ctypes.POINTER(_I32), ctypes.POINTER(_I32)]),
     "icv_conv": (ctypes.c_int, [ctypes.POINTER(Desc), ctypes.POINTER(Shape), _I64, _I32, _P, _P, _P, _I32, _I32,
                                 _P, ctypes.POINTER(Quant), _P, _P]),
-    "icv_conv_kernel_name": (ctypes.c_int, [ctypes.POINTER(Desc), ctypes.POINTER(Shape), _I32,
+    "icv_conv_kernel_name": (ctypes.c_int, [ctypes.POINTER(Desc), ctypes.POINTER(Shape), _I32, _I32,
                                             ctypes.POINTER(ctypes.c_char_p)]),
+    "icv_set_tuning": (ctypes.c_int, [ctypes.c_char_p, _I32]),
+    "icv_get_tuning": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(_I32)]),
     "icv_launch_count": (_I64, []),
     "icv_maxpool2d": (ctypes.c_int, [ctypes.POINTER(Shape), _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P, _P, _P]),
     "icv_im2col": (ctypes.c_int, [ctypes.POINTER(Desc), ctypes.POINTER(Shape), _I64, _I32, _P, _P, _P, _P]),
@@ -152,9 +156,43 @@ def launch_count() -> int:
     return int(lib().icv_launch_count())
 
 
-def kernel_name(params, in_shape, dtype: torch.dtype) -> str:
+DEFAULT_FLAGS = ICV_IB_CANONICAL | ICV_ZERO_ROW_ZEROS | ICV_IB_PER_IMAGE
+
+
+def kernel_name(params, in_shape, dtype: torch.dtype, flags: int | None = None) -> str:
+    """Kernel icv_conv launches for this problem; ``flags`` are the layout
+    flags of its ``ib_dtype`` argument (default: a canonical per-image buffer
+    with a zero zero row, as init_indirection_buffer / make_zero_row build;
+    uint8 adds ICV_ZERO_ROW_ZP when the zero row holds the zero point)."""
     out = ctypes.c_char_p()
     d, s = desc_of(params), shape_of(in_shape)
-    check(lib().icv_conv_kernel_name(ctypes.byref(d), ctypes.byref(s), TORCH_TO_ICV[dtype], ctypes.byref(out)),
+    if flags is None:
+        flags = DEFAULT_FLAGS if dtype != torch.uint8 else (ICV_IB_CANONICAL | ICV_IB_PER_IMAGE | ICV_ZERO_ROW_ZP)
+    f = int(flags)
+    check(lib().icv_conv_kernel_name(ctypes.byref(d), ctypes.byref(s), TORCH_TO_ICV[dtype], f, ctypes.byref(out)),
           "icv_conv_kernel_name")
     return out.value.decode()
+
+
+def set_tuning(key: str, value: int) -> None:
+    """Set a plan knob of the native library (include/icv.h icv_set_tuning)."""
+    check(lib().icv_set_tuning(key.encode(), int(value)), "icv_set_tuning")
+
+
+def get_tuning(key: str) -> int:
+    v = _I32()
+    check(lib().icv_get_tuning(key.encode(), ctypes.byref(v)), "icv_get_tuning")
+    return int(v.value)
+
+
+@contextlib.contextmanager
+def tuning(**knobs):
+    """Temporarily set plan knobs (A/B measurement, tests); restored on exit."""
+    saved = {k: get_tuning(k) for k in knobs}
+    try:
+        for k, v in knobs.items():
+            set_tuning(k, v)
+        yield
+    finally:
+        for k, v in saved.items():
+            set_tuning(k, v)

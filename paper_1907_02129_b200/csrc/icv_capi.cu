@@ -5,8 +5,10 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
+#include <tuple>
 
 #include "icv_internal.h"
 
@@ -25,6 +27,63 @@ int cuda_check(cudaError_t e, const char* what) {
   return fail(ICV_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+int kernel_setup(const void* fn, int smem_bytes, int cluster, int threads, int* max_clusters) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, int>, int> done;   // (kernel, device, smem) -> max clusters
+  int dev = 0;
+  if (int s = cuda_check(cudaGetDevice(&dev), "cudaGetDevice")) return s;
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_tuple(fn, dev, smem_bytes);
+  auto it = done.find(key);
+  if (it == done.end()) {
+    if (int s = cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes),
+                           "cudaFuncSetAttribute(max dynamic smem)"))
+      return s;
+    int mc = 0;
+    if (cluster > 1) {
+      cudaLaunchConfig_t q = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = cluster;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      q.gridDim = dim3(cluster * 74);
+      q.blockDim = dim3(threads);
+      q.dynamicSmemBytes = smem_bytes;
+      q.attrs = at;
+      q.numAttrs = 1;
+      if (int s = cuda_check(cudaOccupancyMaxActiveClusters(&mc, fn, &q), "cudaOccupancyMaxActiveClusters")) return s;
+    }
+    it = done.emplace(key, mc).first;
+  }
+  if (max_clusters) *max_clusters = it->second;
+  return ICV_OK;
+}
+
+// ---- tuning knobs --------------------------------------------------------------
+static const char* const kTuneNames[kTuneCount] = {
+    "win", "win_min_useful_pm", "win_s2", "win_u8", "win_ws", "win_tma", "win_u8_cls", "win_split",
+    "win_debug", "win_cs", "win_mt", "win_res", "win_u8_bn", "cluster", "u8_bn", "tma_store", "rows_rp",
+    "dense_a"};
+static const int kTuneDefaults[kTuneCount] = {-1, 700, 0, 0, 0, 1, 1, 2, 0, 2, 2, 1, 256, 1, 0, 1, 1, 1};
+static std::atomic<int> g_tune[kTuneCount];
+static std::once_flag g_tune_once;
+static void tune_init() {
+  std::call_once(g_tune_once, [] {
+    for (int i = 0; i < kTuneCount; ++i) g_tune[i].store(kTuneDefaults[i], std::memory_order_relaxed);
+  });
+}
+int tune(TuneKey k) {
+  tune_init();
+  return g_tune[k].load(std::memory_order_relaxed);
+}
+static int tune_index(const char* key) {
+  if (!key) return -1;
+  for (int i = 0; i < kTuneCount; ++i)
+    if (std::strcmp(key, kTuneNames[i]) == 0) return i;
+  return -1;
+}
 
 int make_geom(const icv_conv_desc* d, const icv_shape4* in, Geom* g) {
   if (!d || !in || !g) return fail(ICV_ERR_ARG, "null argument");
@@ -140,6 +199,21 @@ ICV_API int32_t icv_abi_version(void) { return ICV_ABI_VERSION; }
 ICV_API const char* icv_last_error(void) { return g_last_error.c_str(); }
 
 ICV_API int64_t icv_launch_count(void) { return g_launches.load(); }
+
+ICV_API int icv_set_tuning(const char* key, int32_t value) {
+  const int i = tune_index(key);
+  if (i < 0) return fail(ICV_ERR_ARG, std::string("icv_set_tuning: unknown key ") + (key ? key : "(null)"));
+  tune_init();
+  g_tune[i].store(value < 0 && i != kTuneWin ? kTuneDefaults[i] : value, std::memory_order_relaxed);
+  return ICV_OK;
+}
+
+ICV_API int icv_get_tuning(const char* key, int32_t* value) {
+  const int i = tune_index(key);
+  if (i < 0) return fail(ICV_ERR_ARG, std::string("icv_get_tuning: unknown key ") + (key ? key : "(null)"));
+  if (value) *value = tune((TuneKey)i);
+  return ICV_OK;
+}
 
 ICV_API int icv_maxpool2d(const icv_shape4* in, int32_t kh, int32_t kw, int32_t sh, int32_t sw, int32_t ph,
                           int32_t pw, int32_t dtype, const void* x, void* y, void* stream) {
@@ -280,19 +354,26 @@ static const char* kernel_name_for(const ConvArgs& a) {
     case kFamTcBf16:
     case kFamTcU8: return tc_kernel_name(a);
     case kFamStemBf16:
-      return (a.L.rows_off && rows_kernel_eligible(a.g)) ? "icv_igemm_rows<bf16>" : "icv_igemm_stem<bf16>";
+      return (!a.prefer_gather && a.ib_canonical && a.L.rows_off && rows_kernel_eligible(a.g))
+                 ? "icv_igemm_rows<bf16>" : "icv_igemm_stem<bf16>";
   }
   return "?";
 }
 
-ICV_API int icv_conv_kernel_name(const icv_conv_desc* desc, const icv_shape4* in, int32_t dtype, const char** name) {
+ICV_API int icv_conv_kernel_name(const icv_conv_desc* desc, const icv_shape4* in, int32_t dtype, int32_t flags,
+                                 const char** name) {
   ConvArgs a{};
   if (int s = make_geom(desc, in, &a.g)) return s;
   if (int s = packed_layout(desc, dtype, &a.L)) return s;
   a.P = in->n * a.g.OH * a.g.OW;
-  a.ib_canonical = 1;   // as for every buffer init_indirection_buffer builds
-  a.zero_known = 1;     // (a float zero row from make_zero_row)
-  a.x = reinterpret_cast<const void*>(uintptr_t(256));   // (16-byte aligned input assumed)
+  a.ib_per_image = (flags & ICV_IB_PER_IMAGE) != 0;
+  a.ib_canonical = (flags & ICV_IB_CANONICAL) != 0;
+  a.zero_known = (flags & ICV_ZERO_ROW_ZEROS) != 0;
+  a.zero_is_zp = (flags & ICV_ZERO_ROW_ZP) != 0;
+  a.prefer_gather = (flags & ICV_PREFER_GATHER) != 0;
+  a.x = reinterpret_cast<const void*>(uintptr_t(256));   // (16-byte aligned tensors assumed)
+  a.y = reinterpret_cast<void*>(uintptr_t(256));
+  a.zero_row = a.x;
   if (name) *name = kernel_name_for(a);
   return ICV_OK;
 }
@@ -308,7 +389,8 @@ ICV_API int icv_conv(const icv_conv_desc* desc, const icv_shape4* in, int64_t ba
   a.ib_canonical = (ib_dtype & ICV_IB_CANONICAL) != 0;
   a.zero_known = (ib_dtype & ICV_ZERO_ROW_ZEROS) != 0;
   a.zero_is_zp = (ib_dtype & ICV_ZERO_ROW_ZP) != 0;
-  ib_dtype &= ~(ICV_IB_PER_IMAGE | ICV_IB_CANONICAL | ICV_ZERO_ROW_ZEROS | ICV_ZERO_ROW_ZP);
+  a.prefer_gather = (ib_dtype & ICV_PREFER_GATHER) != 0;
+  ib_dtype &= ~(ICV_IB_PER_IMAGE | ICV_IB_CANONICAL | ICV_ZERO_ROW_ZEROS | ICV_ZERO_ROW_ZP | ICV_PREFER_GATHER);
   if (ib_dtype != ICV_I64 && ib_dtype != ICV_I32) return fail(ICV_ERR_ARG, "ib dtype must be int64 or int32");
   if (!x || !zero_row || !ib || !packed || !y) return fail(ICV_ERR_ARG, "null tensor pointer");
   if (int s = packed_layout(desc, dtype, &a.L)) return s;
@@ -320,6 +402,12 @@ ICV_API int icv_conv(const icv_conv_desc* desc, const icv_shape4* in, int64_t ba
   a.ib_is_i32 = ib_dtype == ICV_I32;
   a.packed = static_cast<const uint8_t*>(packed);
   a.y = y;
+  if (a.L.family == kFamTcBf16 || a.L.family == kFamTcU8 || a.L.family == kFamStemBf16) {
+    // the tensor-core kernels move 16-byte vectors of x, the zero row and y
+    const uintptr_t mis = (reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(zero_row) |
+                           reinterpret_cast<uintptr_t>(y)) & 15;
+    if (mis) return fail(ICV_ERR_UNSUPPORTED, "tensor-core convolution needs 16-byte aligned input, zero row and output");
+  }
   if (dtype == ICV_U8) {
     if (!quant) return fail(ICV_ERR_ARG, "uint8 convolution needs quantization parameters");
     if (quant->output_min < 0 || quant->output_max > 255 || quant->output_min > quant->output_max)

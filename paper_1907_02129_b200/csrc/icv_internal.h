@@ -20,6 +20,40 @@ int launch_im2col(const Geom& g, int64_t batch, int elem, const void* x, const v
 int launch_maxpool(const icv_shape4& in, int kh, int kw, int sh, int sw, int ph, int pw, int dtype, const void* x,
                    void* y, cudaStream_t st);
 
+// ---- tuning knobs (icv_set_tuning) -------------------------------------------
+// Plan choices exposed for A/B measurement and tests.  The defaults are the
+// measured-best plans; nothing reads the environment.  Values
+// are process-wide atomics, read once per icv_conv call.
+enum TuneKey {
+  kTuneWin = 0,          // window kernel: -1 auto, 0 never (IB-gather kernel), 1 whenever it fits
+  kTuneWinMinUsefulPm,   // auto mode: minimum fraction (per mille) of computed rows that are real pixels
+  kTuneWinS2,            // 1: stride-2 phase-plane window kernel (measured slower; opt-in)
+  kTuneWinU8,            // 1: uint8 window kernel (measured slower; opt-in)
+  kTuneWinWs,            // window stages (0 = plan default)
+  kTuneWinTma,           // 1: TMA windows when the zero row allows, 0: cp.async windows
+  kTuneWinU8Cls,         // 1: uint8 padding corrections per border class, 0: per tap
+  kTuneWinSplit,         // TMA issuers per window
+  kTuneWinDebug,         // 1: print the window plan to stderr
+  kTuneWinCs,            // 2: CTA pairs allowed, 1: single CTAs only
+  kTuneWinMt,            // 2: two-tile units allowed, 1: one tile per unit
+  kTuneWinRes,           // 1: resident-filter plans allowed
+  kTuneWinU8Bn,          // uint8 window tile width when K = 256 (256 or 128)
+  kTuneCluster,          // gather kernel: 2 = CTA pairs (measured slower; opt-in), 1 = single CTAs
+  kTuneU8Bn,             // gather kernel uint8 tile width: 256 (opt-in) or 0 = default 128
+  kTuneTmaStore,         // 1: TMA tile stores in the epilogue, 0: thread stores
+  kTuneRowsRp,           // row kernel: output rows per tile (1, or 2 = opt-in)
+  kTuneDenseA,           // 1: 1x1 stride-1 layers load A as dense TMA boxes, 0: IB gathers
+  kTuneCount
+};
+int tune(TuneKey k);
+
+// One-time per (kernel, device) setup before a launch: opt in to
+// `smem_bytes` of dynamic shared memory and, for cluster launches
+// (cluster > 1), query how many clusters of `threads`-thread CTAs can be
+// co-resident (written to *max_clusters; 0 otherwise).  Function attributes
+// are per device, so a process driving several GPUs sets them on each.
+int kernel_setup(const void* fn, int smem_bytes, int cluster, int threads, int* max_clusters);
+
 // ---- geometry --------------------------------------------------------------
 struct Geom {
   int R, S, SY, SX, DY, DX, PT, PL, PB, PR, C, K;
@@ -70,6 +104,7 @@ struct ConvArgs {
   int32_t ib_canonical;  // caller guarantees the icv_ib_build layout (ICV_IB_CANONICAL)
   int32_t zero_known;    // caller guarantees the zero row is all zero bytes (ICV_ZERO_ROW_ZEROS)
   int32_t zero_is_zp;    // uint8: caller guarantees every zero-row byte is the input zero point (ICV_ZERO_ROW_ZP)
+  int32_t prefer_gather; // caller asks for the IB-gather kernels (ICV_PREFER_GATHER)
   const uint8_t* packed;
   PackedLayout L;
   void* y;
@@ -80,6 +115,7 @@ int launch_conv_f32_exact(const ConvArgs& a, cudaStream_t st);
 int launch_conv_core(const ConvArgs& a, cudaStream_t st);       // bf16 / u8, any C (CUDA cores)
 int launch_conv_tc(const ConvArgs& a, cudaStream_t st);         // bf16 / u8 tcgen05
 bool win_kernel_eligible(const ConvArgs& a);                   // stride-1 window kernel applies
+bool dense_a_eligible(const ConvArgs& a);                      // 1x1 stride-1: A is the dense input matrix
 int launch_conv_win(const ConvArgs& a, cudaStream_t st);        // bf16 / u8 tcgen05, sliding window A
 const char* tc_kernel_name(const ConvArgs& a);
 int launch_conv_stem(const ConvArgs& a, cudaStream_t st);   // channel-poor bf16 (tcgen05)

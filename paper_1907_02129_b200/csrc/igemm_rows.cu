@@ -409,10 +409,7 @@ bool plan_rows(const ConvArgs& c, int BN, int tpr, int kRing, int rp, RowsPlan* 
 template <int BN, int kR, int kKS, int kC, int kRing, int kRP>
 int launch_rows_ring(const ConvArgs& c, cudaStream_t st, const RowsPlan& pl, int ring_row_bytes, int tpr) {
   auto kernel = igemm_rows_kernel<BN, kR, kKS, kC, kRing, kRP>;
-  static std::once_flag once;
-  static cudaError_t err = cudaSuccess;
-  std::call_once(once, [&] { err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448); });
-  if (err != cudaSuccess) return cuda_check(err, "cudaFuncSetAttribute(rows smem)");
+  if (int s = kernel_setup(reinterpret_cast<const void*>(kernel), 232448, 1, kThreadsR, nullptr)) return s;
   RowsArgs a;
   fill_tc_args(c, BN, &a.t);
   a.t.tiles_per_row = tpr;
@@ -448,8 +445,7 @@ int launch_rows_ring(const ConvArgs& c, cudaStream_t st, const RowsPlan& pl, int
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) return fail(ICV_ERR_CUDA, "row kernel: output tensor map");
   }
-  static const char* ts = getenv("ICV_TMA_STORE");
-  a.t.use_tma_y = !(ts && ts[0] == '0');
+  a.t.use_tma_y = tune(kTuneTmaStore) != 0;
   const int sms = sm_count();
   const int grid = (int)(a.total_tiles < sms ? a.total_tiles : sms);
   kernel<<<grid, kThreadsR, pl.bytes, st>>>(tmap_y, a, pl);
@@ -464,12 +460,11 @@ int launch_rows_t(const ConvArgs& c, cudaStream_t st) {
   const int tpr = (int)((c.g.OW + kBM - 1) / kBM);
   RowsPlan pl;
   int ring_row_bytes = 0;
-  // opt-in ICV_ROWS_RP=2: tiles of two output rows (half the per-tile
+  // opt-in knob rows_rp = 2: tiles of two output rows (half the per-tile
   // hand-offs; BN 64: 8 accumulators = 4 tile pairs).  Correct, measured
   // slower (cfg3a 30.8 vs 28.7 us): the kernel is bound by shared-memory
   // bandwidth per output row, not by hand-offs per tile
-  const char* rpe = getenv("ICV_ROWS_RP");
-  const bool rp2 = BN == 64 && rpe && rpe[0] == '2';
+  const bool rp2 = BN == 64 && tune(kTuneRowsRp) == 2;
   if (rp2 && plan_rows(c, BN, tpr, kRingBig, 2, &pl, &ring_row_bytes))
     return launch_rows_ring<BN, kR, kKS, kC, kRingBig, 2>(c, st, pl, ring_row_bytes, tpr);
   if (plan_rows(c, BN, tpr, kRingBig, 1, &pl, &ring_row_bytes))

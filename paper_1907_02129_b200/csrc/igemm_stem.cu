@@ -535,12 +535,7 @@ int launch_stem_t(const ConvArgs& c, cudaStream_t st) {
   const int64_t x_elems = c.g.N * c.g.H * c.g.W * (int64_t)c.g.C;
   if (x_elems >= (int64_t(1) << 31)) return fail(ICV_ERR_UNSUPPORTED, "stem kernel: input too large");
   auto kernel = igemm_stem_kernel<C, RS, BN, IbT>;
-  static std::once_flag once;
-  static cudaError_t err = cudaSuccess;
-  std::call_once(once, [&] {
-    err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::kSmemBytes);
-  });
-  if (err != cudaSuccess) return cuda_check(err, "cudaFuncSetAttribute(stem smem)");
+  if (int s = kernel_setup(reinterpret_cast<const void*>(kernel), Cf::kSmemBytes, 1, 0, nullptr)) return s;
   CUtensorMap tmap;
   if (int s = make_filter_tmap(c, BN, Cf::kBlocks, &tmap)) return s;
   TcArgs a;
@@ -578,7 +573,7 @@ bool stem_kernel_eligible(int C, int RS, int K) {
 
 int launch_conv_stem(const ConvArgs& c, cudaStream_t st) {
   // stride-2 layers with a canonical buffer: the row-sliding kernel (igemm_rows.cu)
-  if (c.ib_canonical && c.L.rows_off && rows_kernel_eligible(c.g)) return launch_conv_rows(c, st);
+  if (!c.prefer_gather && c.ib_canonical && c.L.rows_off && rows_kernel_eligible(c.g)) return launch_conv_rows(c, st);
   if (c.ib_is_i32) return dispatch_stem<int32_t>(c, st);
   return dispatch_stem<int64_t>(c, st);
 }

@@ -1,7 +1,5 @@
 // K2/K3: indirect-GEMM mainloop on sm_100a tensor cores, A operand staged in
-// SHARED memory ("kernel S").  Used for wide output tiles (BLOCK_N = 256,
-// whose two TMEM accumulators fill all 512 TMEM columns) and for problems
-// with too few K blocks per tile for the TMEM-A kernel (igemm_tmem.cu).
+// SHARED memory ("kernel S", the IB-gather kernel).
 //
 // Replaces indirect_conv's hot loop (reference indirect.py:287-294).  GEMM
 // view: M = output pixels, N = output channels, K = R*S taps x C channels.
@@ -56,7 +54,13 @@ constexpr int kMmaWarpS = kProdWarpsS<kI8> + kEpiW;
 template <bool kI8, int kEpiW = kEpiWarpsS<kI8>>
 constexpr int kThreadsS = 32 * (kMmaWarpS<kI8, kEpiW> + 1);
 
-template <bool kI8, int BN, int kPair = 1, int kEpiW = kEpiWarpsS<kI8>>
+// Index type tag of the dense-A instantiation (no indirection buffer read:
+// the A tile is TMA-loaded as 128 consecutive pixel rows; dense_a_eligible).
+struct DenseA {};
+template <typename IbT>
+constexpr bool kIsDense = std::is_same<IbT, DenseA>::value;
+
+template <bool kI8, int BN, int kPair = 1, int kEpiW = kEpiWarpsS<kI8>, bool kDense = false>
 struct CfgS {
   // B bytes per K block held by this CTA (a CTA pair splits the BN rows)
   static constexpr int kBBytes = BN * 128 / kPair;
@@ -66,12 +70,14 @@ struct CfgS {
 #ifndef ICV_KKB
 #define ICV_KKB 2
 #endif
-  static constexpr int kKB = BN >= 256 ? 1 : ICV_KKB;
+  // (dense A: one K block per stage -- 1x1 layers have few K blocks per
+  // tile, and the stages then run straight across tile boundaries)
+  static constexpr int kKB = (kDense || BN >= 256) ? 1 : ICV_KKB;
   static constexpr int kSlotBytes = kABytes + kBBytes;
 #ifndef ICV_MAX_SLOTS
 #define ICV_MAX_SLOTS 8
 #endif
-  static constexpr int kMaxSlots = ICV_MAX_SLOTS;
+  static constexpr int kMaxSlots = kDense ? 12 : ICV_MAX_SLOTS;
   static constexpr int kOnesBytes = kI8 ? 16 * 128 : 0;
   // TMEM columns per accumulator stage (uint8: row sums at +BN; BN = 256
   // keeps 32 columns for them and runs one accumulator stage)
@@ -93,9 +99,9 @@ struct PlanS {
 
 template <bool kI8, int BN, typename IbT, int kPair = 1, int kEpiW = kEpiWarpsS<kI8>>
 bool plan_smem(int rs, int n_pad, PlanS* p) {
-  using C = CfgS<kI8, BN, kPair, kEpiW>;
+  using C = CfgS<kI8, BN, kPair, kEpiW, kIsDense<IbT>>;
   const int bias = (n_pad * 4 + 15) / 16 * 16;
-  const int ib = 2 * rs * kBM * 4 + 2 * kBM * 4;   // int32 index slices + per-row bases
+  const int ib = kIsDense<IbT> ? 0 : 2 * rs * kBM * 4 + 2 * kBM * 4;   // int32 index slices + per-row bases
   const int fixed = 1024 + C::kOnesBytes + C::kEpiBytes + bias + ib + C::kBarBytes;
   int slots = (232448 - fixed) / C::kSlotBytes;
   slots = (slots > C::kMaxSlots ? C::kMaxSlots : slots) / C::kKB * C::kKB;
@@ -145,8 +151,9 @@ __global__ void __launch_bounds__(kThreadsS<kI8, kEpiW>, 1) igemm_smem_kernel(co
   // M = 256 (its 128 rows + the peer's 128 rows); each CTA gathers its own A
   // rows and TMA-loads its half of the filter rows, so each SM receives half
   // the filter bytes of the single-CTA kernel.
-  using C = CfgS<kI8, BN, kCS, kEpiW>;
+  using C = CfgS<kI8, BN, kCS, kEpiW, kIsDense<IbT>>;
   static_assert(kCS == 1 || kCS == 2, "single CTA or CTA pair");
+  static_assert(!kIsDense<IbT> || kCS == 1, "dense A: single CTAs");
   constexpr uint16_t kMask = (uint16_t)((1u << kCS) - 1);
   const ClusterTiles<kCS> sched{a.total_tiles / a.n_tiles, a.n_tiles};
   const uint32_t crank = kCS > 1 ? cluster_ctarank() : 0;
@@ -173,22 +180,19 @@ __global__ void __launch_bounds__(kThreadsS<kI8, kEpiW>, 1) igemm_smem_kernel(co
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) TRACE(0);
-  // TMA gathers realize padding taps as out-of-bounds (zero-filled) rows, so
-  // they are used only when the bound zero row really is all zeros (always
-  // true for make_zero_row of a float convolution); any other zero row takes
-  // the cp.async path, which reads it.
-  int nonzero = 0;
-  if (a.use_tma_x)
-    for (int i = threadIdx.x; i < a.c_bytes / 16; i += blockDim.x) {
-      const uint4 z = __ldg(reinterpret_cast<const uint4*>(a.zero_row) + i);
-      nonzero |= (z.x | z.y | z.z | z.w) != 0;
-    }
-  const bool tma_gather = kCS == 1 && a.use_tma_x && !__syncthreads_or(nonzero);
+  // Dense A (a.use_tma_x): a 1x1 stride-1 layer with a canonical buffer
+  // references pixel p at tap 0 for output pixel p, so the A tile of M tile
+  // mt is the 128 consecutive pixel rows [128 mt, 128 mt + 128) of the input
+  // -- one 2-D TMA box per 128-byte channel block (rows past the batch and
+  // channels past C are zero-filled; those rows are never stored).  The
+  // launcher sets it only for such layers (and for the GEMM baseline's patch
+  // matrix, a 1 x P image of R*S*C channels).
+  constexpr bool dense_a = kIsDense<IbT>;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       // TMA path: 1 expect_tx arrival; cp.async path: 128 producer arrivals + 1
       // cp.async path: 128 producer arrivals + 1 expect_tx (+ 1 forwarded from the peer, pair leader)
-      mbar_init(&full[s], tma_gather ? 1 : 32 * kProdWarpsS<kI8> + 1 + (kCS == 2 && crank == 0 ? 1 : 0));
+      mbar_init(&full[s], dense_a ? 1 : 32 * kProdWarpsS<kI8> + 1 + (kCS == 2 && crank == 0 ? 1 : 0));
       mbar_init(&empty[s], 1);       // tcgen05.commit (multicast to both CTAs of a pair)
     }
     for (int s = 0; s < 2; ++s) {
@@ -198,7 +202,7 @@ __global__ void __launch_bounds__(kThreadsS<kI8, kEpiW>, 1) igemm_smem_kernel(co
     }
     fence_mbar_init();
     tma_prefetch_desc(&tmap_b);
-    if (tma_gather) tma_prefetch_desc(&tmap_x);
+    if (dense_a) tma_prefetch_desc(&tmap_x);
   }
   if constexpr (kI8) {
     if (threadIdx.x >= 128 && threadIdx.x < 256) {  // all-ones B tile (16 rows x 128 bytes)
@@ -232,14 +236,16 @@ __global__ void __launch_bounds__(kThreadsS<kI8, kEpiW>, 1) igemm_smem_kernel(co
     const int64_t my_tiles = sched.count();
     // cp.async the (R*S taps x 128 pixels) index slice of local tile k into buffer k&1
     auto stage_index_slice = [&](int64_t k) {
-      if (k < my_tiles && threadIdx.x < kBM) {
-        const int64_t mt = sched(k) / a.n_tiles;
-        const uint32_t base = smem_u32(sIB + (k & 1) * slice_elems) + threadIdx.x * 4;
-        const RowRef rr = row_ref(a, mt, threadIdx.x);                        // row = threadIdx.x
-        const IbT* src = static_cast<const IbT*>(a.ib) + rr.ent0;
-        sRowBase[(k & 1) * kBM + threadIdx.x] = (int32_t)rr.base;
-        for (int e = 0; e < a.RS; ++e)
-          cp_async_ca<4>(base + e * kBM * 4, src + (int64_t)e * a.mr);
+      if constexpr (!dense_a) {
+        if (k < my_tiles && threadIdx.x < kBM) {
+          const int64_t mt = sched(k) / a.n_tiles;
+          const uint32_t base = smem_u32(sIB + (k & 1) * slice_elems) + threadIdx.x * 4;
+          const RowRef rr = row_ref(a, mt, threadIdx.x);                        // row = threadIdx.x
+          const IbT* src = static_cast<const IbT*>(a.ib) + rr.ent0;
+          sRowBase[(k & 1) * kBM + threadIdx.x] = (int32_t)rr.base;
+          for (int e = 0; e < a.RS; ++e)
+            cp_async_ca<4>(base + e * kBM * 4, src + (int64_t)e * a.mr);
+        }
       }
       cp_async_commit();
     };
@@ -258,47 +264,27 @@ __global__ void __launch_bounds__(kThreadsS<kI8, kEpiW>, 1) igemm_smem_kernel(co
       const int32_t* slice = sIB + (k & 1) * slice_elems;
       const int32_t* rbase = sRowBase + (k & 1) * kBM;
       const int nt = (int)(tile % a.n_tiles);
-      if (tma_gather) {
-        // TMA path: warp 0 issues, per K block, one tile::gather4 per lane
-        // (rows 4l..4l+3: pixel-row index = offset / C, ZERO_REF -> row -1,
-        // which TMA zero-fills) plus the filter block; one expect_tx covers
-        // both, so the stage completes without any thread-side arrivals.
-        if (warp == 0) {
-          int kb = 0;
-          for (int e = 0; e < a.RS; ++e) {
-            int32_t rows4[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int64_t off = resolve_ref((int64_t)slice[e * kBM + 4 * lane + i], rbase[4 * lane + i]);
-              rows4[i] = off < 0 ? -1 : pixel_row(a, off);
+      if constexpr (dense_a) {
+        // one thread issues, per stage, the kKB A boxes and the filter box
+        // under one expect_tx: no thread-side arrivals
+        if (threadIdx.x == 0) {
+          const int64_t mt = tile / a.n_tiles;
+          for (int kb = 0; kb < num_kb; ++kb) {
+            const int j = kb % C::kKB;
+            if (j == 0) {
+              mbar_wait(&empty[stage], phase ^ 1);
+              mbar_arrive_expect_tx(&full[stage], min(C::kKB, num_kb - kb) * kABytes + C::kKB * C::kBBytes);
+              tma_load_3d(sB_u32 + stage * C::kKB * C::kBBytes, &tmap_b, &full[stage], 0, nt * BN, kb);
             }
-            for (int cb = 0; cb < a.cblocks; ++cb, ++kb) {
-              const int j = kb % C::kKB;
-              if (j == 0) {
-#ifdef ICV_TRACE
-                long long pw0 = clock64();
-#endif
-                mbar_wait(&empty[stage], phase ^ 1);
-#ifdef ICV_TRACE
-                p_wait += clock64() - pw0;
-#endif
-                if (lane == 0) {
-                  mbar_arrive_expect_tx(&full[stage], min(C::kKB, num_kb - kb) * kABytes + C::kKB * C::kBBytes);
-                  tma_load_3d(sB_u32 + stage * C::kKB * C::kBBytes, &tmap_b, &full[stage], 0, nt * BN, kb);
-                }
-                __syncwarp();
-              }
-              const int slot = stage * C::kKB + j;
-              tma_gather4(sA_u32 + slot * kABytes + lane * 512, &tmap_x, &full[stage], cb * a.cblock_elems,
-                          rows4[0], rows4[1], rows4[2], rows4[3]);
-              if (j == C::kKB - 1 || kb == num_kb - 1) {
-                if (++stage == kStages) { stage = 0; phase ^= 1; }
-              }
+            tma_load_2d(sA_u32 + (stage * C::kKB + j) * kABytes, &tmap_x, &full[stage], kb * a.cblock_elems,
+                        (int32_t)(mt * kBM));
+            if (j == C::kKB - 1 || kb == num_kb - 1) {
+              if (++stage == kStages) { stage = 0; phase ^= 1; }
             }
           }
         }
       } else {
-        // cp.async path (any zero row): 8 lanes per 128-byte row (lane & 7 =
+        // IB gather (cp.async, any zero row): 8 lanes per 128-byte row (lane & 7 =
         // 16-byte chunk), 4 rows per instruction -- whole 128-byte lines per
         // request, which the LSU/L2 path moves fastest.  Per tap each lane
         // resolves ONE row reference (its own row of the warp's 32) and the 8
@@ -507,42 +493,27 @@ __global__ void __launch_bounds__(kThreadsS<kI8, kEpiW>, 1) igemm_smem_kernel(co
 template <bool kI8, int BN, typename IbT, int kCS, int kEpiW>
 int launch_smem_cs(const ConvArgs& c, cudaStream_t st) {
   auto kernel = igemm_smem_kernel<kI8, BN, IbT, kCS, kEpiW>;
-  static std::once_flag attr_once;
-  static cudaError_t attr_err = cudaSuccess;
-  static int max_clusters = 0;
   PlanS pl;
   if (!plan_smem<kI8, BN, IbT, kCS, kEpiW>(c.g.RS(), c.L.n_pad, &pl))
     return fail(ICV_ERR_UNSUPPORTED, "indirection slice of this kernel size does not fit in shared memory");
   if (c.g.N * c.g.H * c.g.W * (int64_t)c.g.C >= (int64_t(1) << 31))
     return fail(ICV_ERR_UNSUPPORTED, "tensor-core kernel: input tensors of 2^31 or more elements are not supported");
-  std::call_once(attr_once, [&] {
-    attr_err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-    if (attr_err == cudaSuccess && kCS > 1) {
-      // how many clusters fit at once (some GPCs may not hold a whole pair)
-      cudaLaunchConfig_t q = {};
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = kCS;
-      at[0].val.clusterDim.y = 1;
-      at[0].val.clusterDim.z = 1;
-      q.gridDim = dim3(kCS * 74);
-      q.blockDim = dim3(kThreadsS<kI8, kEpiW>);
-      q.dynamicSmemBytes = pl.bytes;
-      q.attrs = at;
-      q.numAttrs = 1;
-      attr_err = cudaOccupancyMaxActiveClusters(&max_clusters, kernel, &q);
-    }
-  });
-  if (attr_err != cudaSuccess) return cuda_check(attr_err, "kernel attributes (smem / clusters)");
+  int max_clusters = 0;
+  if (int s = kernel_setup(reinterpret_cast<const void*>(kernel), 232448, kCS, kThreadsS<kI8, kEpiW>, &max_clusters))
+    return s;
   CUtensorMap tmap, tmap_x;
-  if (int s = make_filter_tmap(c, BN / kCS, CfgS<kI8, BN>::kKB, &tmap)) return s;
+  if (int s = make_filter_tmap(c, BN / kCS, CfgS<kI8, BN, 1, kEpiW, kIsDense<IbT>>::kKB, &tmap)) return s;
   TcArgs a;
   fill_tc_args(c, BN, &a);
-  // TMA tile::gather4 for A is correct but ~2.5x slower than the cp.async
-  // gather on B200 (measured); kept behind ICV_TMA_GATHER=1 for experiments.
-  static const char* tg = getenv("ICV_TMA_GATHER");
-  a.use_tma_x = kCS == 1 && (tg && tg[0] == '1') && make_input_tmap(c, &tmap_x) == ICV_OK;
-  if (!a.use_tma_x) tmap_x = tmap;   // unused placeholder
+  // dense A: 1x1 stride-1 layers with a canonical buffer (and the GEMM
+  // baseline's patch matrix) load the A tile as TMA boxes of consecutive rows
+  a.use_tma_x = 0;
+  if constexpr (kIsDense<IbT>) {
+    if (int s = make_input_tmap(c, &tmap_x)) return fail(s, "dense-A input tensor map");
+    a.use_tma_x = 1;
+  } else {
+    tmap_x = tmap;   // unused placeholder
+  }
   CUtensorMap tmap_y;
   a.use_tma_y = make_output_tmap(c, &tmap_y) == ICV_OK;
   if (!a.use_tma_y) tmap_y = tmap;   // unused placeholder
@@ -574,15 +545,19 @@ int launch_smem_cs(const ConvArgs& c, cudaStream_t st) {
   return cuda_check(cudaGetLastError(), "igemm_smem launch");
 }
 
-// CTA pairs (cta_group::2, M = 256): ICV_CLUSTER=2 (see the kernel).
-bool use_clusters() {
-  static const char* v = getenv("ICV_CLUSTER");
-  return v && v[0] == '2';
-}
+// CTA pairs (cta_group::2, M = 256): tuning knob "cluster" = 2 (see the kernel).
+bool use_clusters() { return tune(kTuneCluster) == 2; }
 
 template <bool kI8, int BN, typename IbT>
 int launch_smem(const ConvArgs& c, cudaStream_t st) {
   if (use_clusters()) return launch_smem_cs<kI8, BN, IbT, 2, kEpiWarpsS<kI8>>(c, st);
+  if (tune(kTuneDenseA) && dense_a_eligible(c)) {
+    PlanS pl;
+    if (!kI8 && (int64_t)c.g.K >= 4 * (int64_t)c.g.C && plan_smem<kI8, BN, DenseA, 1, 8>(1, c.L.n_pad, &pl))
+      return launch_smem_cs<kI8, BN, DenseA, 1, 8>(c, st);
+    if (plan_smem<kI8, BN, DenseA, 1, kEpiWarpsS<kI8>>(1, c.L.n_pad, &pl))
+      return launch_smem_cs<kI8, BN, DenseA, 1, kEpiWarpsS<kI8>>(c, st);
+  }
   if constexpr (!kI8) {
     // output-heavy layers (K >= 4 C) get 8 epilogue warps
     PlanS pl;
@@ -592,15 +567,14 @@ int launch_smem(const ConvArgs& c, cudaStream_t st) {
   return launch_smem_cs<kI8, BN, IbT, 1, kEpiWarpsS<kI8>>(c, st);
 }
 
-// ICV_U8_BN=256: uint8 layers with a multiple of 256 output channels run
+// knob u8_bn = 256: uint8 layers with a multiple of 256 output channels run
 // BLOCK_N 256 (half the A gathers per output, one accumulator stage); correct
 // but measured slower on cfg4 (51 vs 40 us: 1.3 waves of tiles, no epilogue
 // overlap), so BLOCK_N 128 stays the default
 template <bool kI8, int BN>
 bool smem_plan_ok(const ConvArgs& c);
 int smem_block_n(const ConvArgs& c) {
-  const char* v = getenv("ICV_U8_BN");   // (read per call: tests switch it)
-  if (c.L.family == kFamTcU8 && c.L.n_pad % 256 == 0 && v && atoi(v) == 256 && smem_plan_ok<true, 256>(c)) return 256;
+  if (c.L.family == kFamTcU8 && c.L.n_pad % 256 == 0 && tune(kTuneU8Bn) == 256 && smem_plan_ok<true, 256>(c)) return 256;
   return c.L.block_n;
 }
 
@@ -617,14 +591,6 @@ int dispatch_smem(const ConvArgs& c, cudaStream_t st) {
     if (bn == 256) return launch_smem<true, 256, IbT>(c, st);
   }
   return fail(ICV_ERR_UNSUPPORTED, "no tensor-core kernel for this tile width");
-}
-
-bool use_tmem_kernel() {
-  // The TMEM-A kernel (igemm_tmem.cu) is correct but slower than kernel S
-  // on B200 today (its register-staged gathers cannot cover L2 latency);
-  // ICV_TC_KERNEL=tmem selects it for experiments.
-  static const char* sel = getenv("ICV_TC_KERNEL");
-  return sel && sel[0] == 't';
 }
 
 template <bool kI8, int BN>
@@ -665,17 +631,12 @@ int make_filter_tmap(const ConvArgs& c, int block_n, int depth, CUtensorMap* tma
   return ICV_OK;
 }
 
-// 2-D view of the bound input for TMA gathers: rows = N*H*W pixels, columns
-// = C elements; box = one 128-byte channel block of one row; 128-byte
-// swizzle (the A tile's canonical layout).  Rows < 0 or >= N*H*W and
-// columns >= C are zero-filled by TMA.
 // 2-D view of the output (rows = output pixels of the batch, columns = K)
 // for the epilogue's TMA tile stores: box = 32 columns x 32 rows; bf16 rows
 // of the box are 64 bytes with the 64-byte swizzle, uint8 rows 32 bytes
 // unswizzled.  Needs 16-byte aligned rows (K*elem % 16 == 0).
 int make_output_tmap(const ConvArgs& c, CUtensorMap* tmap) {
-  static const char* off = getenv("ICV_TMA_STORE");
-  if (off && off[0] == '0') return ICV_ERR_UNSUPPORTED;
+  if (tune(kTuneTmaStore) == 0) return ICV_ERR_UNSUPPORTED;
   const bool i8 = c.L.family == kFamTcU8;
   if (!i8 && c.L.family != kFamTcBf16 && c.L.family != kFamStemBf16) return ICV_ERR_UNSUPPORTED;
   const int eb = i8 ? 1 : 2;
@@ -694,18 +655,32 @@ int make_output_tmap(const ConvArgs& c, CUtensorMap* tmap) {
   return cr == CUDA_SUCCESS ? ICV_OK : ICV_ERR_CUDA;
 }
 
+// A 1x1, stride-1, unpadded layer over a canonical buffer reads pixel row p
+// for output pixel p (indirect.py:112-125 with R = S = 1), so its A operand
+// is the dense [pixels][C] input matrix.
+bool dense_a_eligible(const ConvArgs& c) {
+  const Geom& g = c.g;
+  if (c.prefer_gather || !c.ib_canonical) return false;
+  if (g.R != 1 || g.S != 1 || g.SY != 1 || g.SX != 1 || g.PT || g.PL || g.PB || g.PR) return false;
+  const int eb = c.L.family == kFamTcU8 ? 1 : 2;
+  if ((reinterpret_cast<uintptr_t>(c.x) & 15) != 0 || (g.C * eb) % 16 != 0) return false;
+  return g.N * g.H * g.W < (int64_t(1) << 31);
+}
+
+// 2-D view of the bound input for dense-A TMA loads: rows = N*H*W pixels,
+// columns = C elements; box = one 128-byte channel block of 128 rows,
+// 128-byte swizzle (the A tile's canonical K-major layout).  Rows past the
+// tensor and columns past C are zero-filled.
 int make_input_tmap(const ConvArgs& c, CUtensorMap* tmap) {
   if (c.L.family != kFamTcBf16 && c.L.family != kFamTcU8) return ICV_ERR_UNSUPPORTED;
   const int64_t rows = c.g.N * c.g.H * c.g.W;
-  if (rows >= (int64_t(1) << 31)) return ICV_ERR_UNSUPPORTED;
-  if (rows * c.g.C >= (int64_t(1) << 32)) return ICV_ERR_UNSUPPORTED;   // exact 32-bit offset -> row division
   auto encode = get_tensor_map_encoder();
   if (!encode) return ICV_ERR_CUDA;
   const bool i8 = c.L.family == kFamTcU8;
   const int eb = i8 ? 1 : 2;
   const cuuint64_t dims[2] = {(cuuint64_t)c.g.C, (cuuint64_t)rows};
   const cuuint64_t strides[1] = {(cuuint64_t)c.g.C * eb};
-  const cuuint32_t box[2] = {(cuuint32_t)(128 / eb), 1};
+  const cuuint32_t box[2] = {(cuuint32_t)(128 / eb), (cuuint32_t)kBM};
   const cuuint32_t estr[2] = {1, 1};
   CUresult cr = encode(tmap, i8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                        const_cast<void*>(c.x), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -757,12 +732,8 @@ int sm_count() {
   return sms;
 }
 
-int launch_conv_tmem(const ConvArgs& c, cudaStream_t st);   // igemm_tmem.cu
-bool tmem_kernel_eligible(const ConvArgs& c);                // igemm_tmem.cu
-
 bool tc_kernel_available(const ConvArgs& c) {
   if (c.L.n_pad > kMaxBias) return false;
-  if (use_tmem_kernel() && tmem_kernel_eligible(c)) return true;
   const int bn = c.L.block_n;
   if (c.L.family == kFamTcU8) return bn == 64 ? smem_plan_ok<true, 64>(c) : smem_plan_ok<true, 128>(c);
   return bn == 64 ? smem_plan_ok<false, 64>(c) : bn == 128 ? smem_plan_ok<false, 128>(c) : smem_plan_ok<false, 256>(c);
@@ -771,7 +742,6 @@ bool tc_kernel_available(const ConvArgs& c) {
 int launch_conv_tc(const ConvArgs& c, cudaStream_t st) {
   if (c.L.n_pad > kMaxBias) return fail(ICV_ERR_UNSUPPORTED, "more than 2048 output channels");
   if (win_kernel_eligible(c)) return launch_conv_win(c, st);
-  if (use_tmem_kernel() && tmem_kernel_eligible(c)) return launch_conv_tmem(c, st);
   if (c.ib_is_i32) return dispatch_smem<int32_t>(c, st);
   return dispatch_smem<int64_t>(c, st);
 }
@@ -779,7 +749,8 @@ int launch_conv_tc(const ConvArgs& c, cudaStream_t st) {
 const char* tc_kernel_name(const ConvArgs& c) {
   const bool i8 = c.L.family == kFamTcU8;
   if (win_kernel_eligible(c)) return i8 ? "icv_igemm_win<u8>" : "icv_igemm_win<bf16>";
-  if (use_tmem_kernel() && tmem_kernel_eligible(c)) return i8 ? "icv_igemm_tmem<u8>" : "icv_igemm_tmem<bf16>";
+  if (dense_a_eligible(c) && tune(kTuneDenseA) && !use_clusters())
+    return i8 ? "icv_igemm_smem<u8,dense>" : "icv_igemm_smem<bf16,dense>";
   return i8 ? "icv_igemm_smem<u8>" : "icv_igemm_smem<bf16>";
 }
 

@@ -134,8 +134,7 @@ bool plan_win(int win_stage, int rs, int kblocks, int n_pad, bool resident, Plan
   p->resident = 0;
   if (resident) {   // every K block of this CTA's filter rows + as many window stages (2..4) as fit
     if (kblocks > kMaxBSlots || fixed + 2 * win_stage + kblocks * C::kBBytes > 232448) return false;
-    const char* wse = getenv("ICV_WIN_WS");
-    int ws = wse && wse[0] ? atoi(wse) : kMaxWinStages;
+    int ws = tune(kTuneWinWs) > 0 ? tune(kTuneWinWs) : kMaxWinStages;
     ws = ws > kMaxWinStages ? kMaxWinStages : (ws < 2 ? 2 : ws);
     while (ws > 2 && fixed + ws * win_stage + kblocks * C::kBBytes > 232448) --ws;
     p->resident = 1;
@@ -152,8 +151,7 @@ bool plan_win(int win_stage, int rs, int kblocks, int n_pad, bool resident, Plan
     p->bytes = 1024 + p->off_bar + bars;
     return true;
   }
-  const char* wse = getenv("ICV_WIN_WS");   // tuning: force the window stage count
-  const int ws_max = wse && wse[0] ? atoi(wse) : (kS2 ? kMaxWinStages : 3);
+  const int ws_max = tune(kTuneWinWs) > 0 ? tune(kTuneWinWs) : (kS2 ? kMaxWinStages : 3);   // knob: force the stage count
   for (int ws = ws_max; ws >= 2; --ws) {
     const int left = 232448 - fixed - ws * win_stage;
     int bs = left / C::kBBytes;
@@ -889,11 +887,6 @@ done:
   }
 }
 
-// ICV_WIN_MT=1: one M tile per unit; ICV_WIN_CS=1: no CTA pairs (tuning / tests)
-int env_int(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return v && v[0] ? atoi(v) : dflt;
-}
 
 // TMA (zero-filled) windows are exact for this call's zero row
 bool tma_zero_ok(const ConvArgs& c) {
@@ -1057,37 +1050,17 @@ bool win_plan_for(const ConvArgs& c, const WinGeom& w, PlanW* pl, bool resident 
 template <bool kI8, int BN, int kMT, int kCS, bool kS2>
 int launch_win(const ConvArgs& c, const WinGeom& w, cudaStream_t st, bool resident) {
   auto kernel = igemm_win_kernel<kI8, BN, kMT, kCS, kS2>;
-  static std::once_flag attr_once;
-  static cudaError_t attr_err = cudaSuccess;
-  static int max_clusters = 0;
   PlanW pl;
   if (!win_plan_for<kI8, BN, kMT, kCS, kS2>(c, w, &pl, resident))
     return fail(ICV_ERR_UNSUPPORTED, "window does not fit in shared memory");
-  std::call_once(attr_once, [&] {
-    attr_err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-    if (attr_err == cudaSuccess && kCS > 1) {
-      // how many pairs fit at once (a GPC with an odd SM count leaves one idle)
-      cudaLaunchConfig_t q = {};
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = kCS;
-      at[0].val.clusterDim.y = 1;
-      at[0].val.clusterDim.z = 1;
-      q.gridDim = dim3(kCS * 74);
-      q.blockDim = dim3(kThreadsW);
-      q.dynamicSmemBytes = 232448;
-      q.attrs = at;
-      q.numAttrs = 1;
-      attr_err = cudaOccupancyMaxActiveClusters(&max_clusters, kernel, &q);
-    }
-  });
-  if (attr_err != cudaSuccess) return cuda_check(attr_err, "window kernel attributes");
+  int max_clusters = 0;
+  if (int s = kernel_setup(reinterpret_cast<const void*>(kernel), 232448, kCS, kThreadsW, &max_clusters)) return s;
   WinArgs a;
   fill_tc_args(c, BN, &a.t);
   CUtensorMap tmap_b;
   if (int s = make_filter_tmap(c, BN / kCS, 1, &tmap_b)) return s;
   WinMaps maps;
-  a.t.use_tma_x = env_int("ICV_WIN_TMA", 1) == 1 && window_maps(c, w, &maps) == ICV_OK;
+  a.t.use_tma_x = tune(kTuneWinTma) == 1 && window_maps(c, w, &maps) == ICV_OK;
   if (!a.t.use_tma_x) {
     if (kCS > 1) return fail(ICV_ERR_UNSUPPORTED, "window pair kernel needs TMA window maps");
     if (w.sy != 1) return fail(ICV_ERR_UNSUPPORTED, "stride-2 window kernel needs TMA window maps");
@@ -1099,7 +1072,7 @@ int launch_win(const ConvArgs& c, const WinGeom& w, cudaStream_t st, bool reside
   a.tapcorr = (kI8 && !c.zero_known && c.zero_is_zp && c.L.tapcorr_off)
                   ? reinterpret_cast<const int32_t*>(c.packed + c.L.tapcorr_off) : nullptr;
   a.ncls = 0;
-  if (a.tapcorr != nullptr && env_int("ICV_WIN_U8_CLS", 1) == 1) {
+  if (a.tapcorr != nullptr && tune(kTuneWinU8Cls) == 1) {
     // border classes (WinArgs): top rows iy0 < 0, bottom rows with the last tap row >= H
     const auto border = [&](int64_t O, int64_t I, int P, int span, int st, int* tb, int* ohb, int* n) {
       const int64_t t = std::min<int64_t>(O, (P + st - 1) / st);
@@ -1120,7 +1093,7 @@ int launch_win(const ConvArgs& c, const WinGeom& w, cudaStream_t st, bool reside
   for (int p = 0; p < 4; ++p) a.php[p] = p < w.nph ? w.php[p] : 0;
   a.g_shift = w.g_shift;
   a.rel_shift = w.rel_shift;
-  a.win_split = env_int("ICV_WIN_SPLIT", 2);
+  a.win_split = tune(kTuneWinSplit);
   if (a.win_split < 1) a.win_split = 1;
   if (a.win_split > kProdWarpsW) a.win_split = kProdWarpsW;
   if (a.win_split > w.WR) a.win_split = w.WR;
@@ -1158,7 +1131,7 @@ int launch_win(const ConvArgs& c, const WinGeom& w, cudaStream_t st, bool reside
   a.cbe = 128 / a.t.elem_bytes;
   a.win_lead = slot_lead(w, kMT, kCS);
   if (clusters > a.units) clusters = a.units;
-  if (env_int("ICV_WIN_DEBUG", 0))
+  if (tune(kTuneWinDebug))
     fprintf(stderr, "igemm_win: BN %d MT %d CS %d S2 %d resident %d wstages %d bslots %d win_stage %d smem %d | "
                     "Wp %d Hz %d WR %d WR2 %d tiles %d units %d (two %d) clusters %lld split %d\n",
             BN, kMT, kCS, (int)kS2, pl.resident, pl.wstages, pl.bslots, pl.win_stage, pl.bytes, w.Wp, w.Hz, w.WR, w.WR2,
@@ -1196,9 +1169,9 @@ template <bool kI8, int BN, bool kS2>
 int dispatch_bn(const ConvArgs& c, const WinGeom& w, cudaStream_t st, bool launch) {
   PlanW pl;
   // CTA pairs need TMA windows, hence a zero row the host certifies
-  const bool pair = tma_zero_ok(c) && env_int("ICV_WIN_CS", 2) == 2;
-  const bool mt2 = env_int("ICV_WIN_MT", 2) == 2;
-  const bool res = env_int("ICV_WIN_RES", 1) == 1;
+  const bool pair = tma_zero_ok(c) && tune(kTuneWinCs) == 2;
+  const bool mt2 = tune(kTuneWinMt) == 2;
+  const bool res = tune(kTuneWinRes) == 1;
   // preference: pair with two-tile units (measured fastest on every stride-1
   // layer: cfg2 25.5 vs 27.5 us resident, ResNet-50 s1 3x3 85 vs 121 us --
   // two tiles share each filter block and one window of WR2 rows), pair
@@ -1224,7 +1197,7 @@ int dispatch_win_s(const ConvArgs& c, const WinGeom& w, cudaStream_t st, bool la
   int bn = c.L.block_n;
   // uint8 with 256 output channels: one N tile of 256 (the TMEM layout keeps
   // 32 columns for the row sums, one accumulator stage)
-  if (c.L.family == kFamTcU8 && c.L.n_pad == 256 && env_int("ICV_WIN_U8_BN", 256) == 256) bn = 256;
+  if (c.L.family == kFamTcU8 && c.L.n_pad == 256 && tune(kTuneWinU8Bn) == 256) bn = 256;
   if (c.L.family == kFamTcBf16) {
     if (bn == 64) return dispatch_bn<false, 64, kS2>(c, w, st, launch);
     if (bn == 128) return dispatch_bn<false, 128, kS2>(c, w, st, launch);
@@ -1245,12 +1218,12 @@ int dispatch_win(const ConvArgs& c, const WinGeom& w, cudaStream_t st, bool laun
 
 // The window kernel takes a stride-1 tensor-core layer when the call
 // certifies a canonical buffer, the window geometry fits, and at least
-// ICV_WIN_MIN_USEFUL (default 0.7) of the computed rows are real output
-// pixels.  ICV_WIN=0 disables it (tap-by-tap gather kernel), ICV_WIN=1
-// forces it whenever it fits.
+// win_min_useful_pm / 1000 (default 0.7) of the computed rows are real
+// output pixels.  Knob win = 0 or the call flag ICV_PREFER_GATHER disable it
+// (tap-by-tap IB-gather kernel); win = 1 forces it whenever it fits.
 bool win_kernel_eligible(const ConvArgs& c) {
-  const char* env = getenv("ICV_WIN");   // read per call: tests switch it at run time
-  if (env && env[0] == '0') return false;
+  const int mode = tune(kTuneWin);
+  if (mode == 0 || c.prefer_gather) return false;
   if (!c.ib_canonical) return false;
   if (c.L.family != kFamTcBf16 && c.L.family != kFamTcU8) return false;
   if (c.L.n_pad > kMaxBias) return false;
@@ -1258,18 +1231,17 @@ bool win_kernel_eligible(const ConvArgs& c) {
   if ((reinterpret_cast<uintptr_t>(c.x) & 15) != 0) return false;
   // 1x1 layers have no tap re-reads for the window to save; measured slower
   // than the gather kernel on every ResNet-50 1x1 (profiles/r01d_cfg5_layers.json)
-  if (c.g.R * c.g.S == 1 && !(env && env[0] == '1')) return false;
+  if (c.g.R * c.g.S == 1 && mode != 1) return false;
   WinGeom w;
   if (!win_geom(c, &w)) return false;
   if (w.sy == 2 && !tma_zero_ok(c)) return false;   // (no cp.async phase-plane gather)
-  // Opt-in only (ICV_WIN=1, or ICV_WIN_S2=1 / ICV_WIN_U8=1), measured slower
+  // Opt-in only (win = 1, or win_s2 = 1 / win_u8 = 1), measured slower
   // than the gather kernel today: stride-2 phase planes (ResNet-50 s2b1 3x3
   // 115 vs 84 us, s3b1 88 vs 60 us) and the uint8 epilogue (cfg4 85 vs 41 us).
-  const bool forced = env && env[0] == '1';
-  if (w.sy == 2 && !forced && env_int("ICV_WIN_S2", 0) != 1) return false;
-  if (c.L.family == kFamTcU8 && !forced && env_int("ICV_WIN_U8", 0) != 1) return false;
-  const char* mu = getenv("ICV_WIN_MIN_USEFUL");
-  const double min_useful = (env && env[0] == '1') ? 0.0 : (mu ? atof(mu) : 0.7);
+  const bool forced = mode == 1;
+  if (w.sy == 2 && !forced && tune(kTuneWinS2) != 1) return false;
+  if (c.L.family == kFamTcU8 && !forced && tune(kTuneWinU8) != 1) return false;
+  const double min_useful = forced ? 0.0 : tune(kTuneWinMinUsefulPm) / 1000.0;
   if (w.useful < min_useful) return false;
   return dispatch_win(c, w, nullptr, false) == ICV_OK;
 }

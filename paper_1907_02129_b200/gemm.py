@@ -73,7 +73,13 @@ class PackedFilter:
     packed: torch.Tensor          # uint8 device buffer written by icv_pack_filter
     bias: torch.Tensor            # host copy of the caller's bias (float32 / int32)
     quant: QuantParams | None = None
-    source: torch.Tensor | None = None   # the KRSC weights on the device (GEMM-baseline repack, im2col.py)
+    # pack_filter's own copy of the K x R x S x C weights (device, compute
+    # dtype's source precision).  The reference PackedFilter likewise holds a
+    # second copy of the weights (lane_weights, gemm.py:101-106); this one
+    # backs the reference-layout views below and the GEMM baseline's 1x1
+    # repack (im2col.py).  Never an alias of the caller's tensor, so editing
+    # the caller's filter after packing changes nothing here.
+    krsc: torch.Tensor | None = None
 
     @property
     def reduction_len(self) -> int:
@@ -86,6 +92,44 @@ class PackedFilter:
     @property
     def device(self) -> torch.device:
         return self.packed.device
+
+    def _krsc(self) -> torch.Tensor:
+        if self.krsc is None:
+            raise ValueError("this packed filter holds no weight copy (built by hand, not by pack_filter)")
+        return self.krsc
+
+    @property
+    def weights(self) -> torch.Tensor:
+        """(n_tiles, kernel_elems * in_channels, nr) column-tile panels, zero
+        in the padded lanes: the reference's canonical packed layout
+        (gemm.py:99-106, :153-157), on the device.  Built on first use."""
+        cached = getattr(self, "_weights_view", None)
+        if cached is None:
+            k, rs, c, nr, nt = self.k_out, self.kernel_elems, self.in_channels, self.nr, self.n_tiles
+            w = self._krsc().reshape(k, rs, c)
+            lanes = torch.zeros((nt * nr, rs, c), dtype=w.dtype, device=w.device)
+            lanes[:k] = w
+            cached = lanes.reshape(nt, nr, rs, c).permute(0, 2, 3, 1).reshape(nt, rs * c, nr).contiguous()
+            self._weights_view = cached
+        return cached
+
+    @property
+    def lane_weights(self) -> torch.Tensor:
+        """(kernel_elems * in_channels, n_tiles, nr): one reduction step across
+        all column tiles (gemm.py:101-106, :158)."""
+        cached = getattr(self, "_lane_view", None)
+        if cached is None:
+            cached = self.weights.permute(1, 0, 2).contiguous()
+            self._lane_view = cached
+        return cached
+
+    def tile(self, jt: int) -> torch.Tensor:
+        """(reduction_len, nr) panel of column tile jt; a view (gemm.py:116-118)."""
+        return self.weights[jt]
+
+    def lane_view(self) -> torch.Tensor:
+        """(reduction_len, n_tiles, nr) reduction-step-major copy (gemm.py:120-124)."""
+        return self.lane_weights
 
     def padded_bias(self) -> np.ndarray:
         """(n_tiles, nr) bias with zero in the padded lanes (gemm.py:128-132)."""
@@ -134,7 +178,8 @@ def pack_filter(filt: FilterTensor, bias, params: ConvParams, tile: TileConfig, 
     device = filt.data.device if device is None else torch.device(device)
     if device.type != "cuda":
         raise L.NativeLibraryError(f"filters are packed on a CUDA device (got {device}); there is no CPU fallback")
-    w = filt.data.to(device)
+    # pack_filter's own copy (never an alias of the caller's tensor)
+    w = filt.data.detach().to(device=device, copy=True)
     d = L.desc_of(params)
     nbytes = ctypes.c_int64()
     L.check(L.lib().icv_packed_filter_bytes(ctypes.byref(d), L.TORCH_TO_ICV[compute_dtype], ctypes.byref(nbytes)),
@@ -151,4 +196,4 @@ def pack_filter(filt: FilterTensor, bias, params: ConvParams, tile: TileConfig, 
     # keep the temporaries alive until the packing kernels have consumed them
     torch.cuda.current_stream(device).synchronize()
     return PackedFilter(k, params.kernel_elems, params.in_channels, tile.nr, compute_dtype, params, packed,
-                        bias_t, quant, source=w)
+                        bias_t, quant, krsc=w)

@@ -36,7 +36,9 @@ class IndirectionCache:
     ``get(input, batch)`` returns a buffer bound to ``input`` that covers at
     least ``batch`` images (default: all of ``input``); pass the same
     ``batch`` to ``indirect_conv``.  ``zero_row`` is shared read-only
-    (indirect.py:42)."""
+    (indirect.py:42) and fixes the dtype and device: an input of another
+    dtype or device raises ValueError (as init_indirection_buffer does).
+    Every call is counted exactly once in ``stats``."""
 
     def __init__(self, params: ConvParams, tile: TileConfig, zero_row: torch.Tensor, *,
                  index_dtype: torch.dtype = torch.int64, per_image: bool = False):
@@ -61,9 +63,14 @@ class IndirectionCache:
             self.stats.builds += 1
             return self.ib
         if not _same_binding(ib.input_data, input.data):                                  # PAPER.md §2.3
-            self.ib = rebind_input(ib, input, self.zero_row)
+            # complete re-initialization at the new location, for the larger of
+            # the two batches (the zero row is unchanged: no re-scan of it)
+            out_shape = conv_output_shape(self.params, input.shape)
+            self.ib = init_indirection_buffer(input, self.zero_row, self.params, out_shape, self.tile,
+                                              batch=max(batch, ib.batch), index_dtype=self.index_dtype,
+                                              per_image=self.per_image, _zero_facts=(ib.zero_is_zero, ib.zero_fill_byte))
             self.stats.rebinds += 1
-            ib = self.ib
+            return self.ib
         if batch > ib.batch:                                                              # indirect.py:167-193
             self.ib = update_for_batch_growth(ib, batch)
             self.stats.growths += 1

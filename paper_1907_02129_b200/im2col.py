@@ -73,6 +73,12 @@ def build_patch_matrix(input: NhwcTensor, params: ConvParams, out: PatchMatrix |
         if out.is_view or out.params != params or out.input_shape != input.shape:
             raise ValueError("provided patch matrix was built for other geometry")      # :80-82
         matrix = out.matrix
+        # (the reference is float32-only; with several dtypes the buffer's
+        # element type, device and extent must match too, or the kernel
+        # would write past it)
+        if matrix.dtype != input.dtype or matrix.device != dev or matrix.numel() != m * cols:
+            raise ValueError(f"provided patch matrix is {matrix.dtype} x {matrix.numel()} on {matrix.device}; "
+                             f"this input needs {input.dtype} x {m * cols} on {dev}")
     if zero_row is not None and (zero_row.numel() != params.in_channels or zero_row.dtype != input.dtype
                                  or zero_row.device != dev):
         raise ValueError("zero_row must hold in_channels elements of the input dtype on its device")
@@ -92,11 +98,9 @@ def _gemm_view(pf: PackedFilter, tile: TileConfig) -> PackedFilter:
     view = getattr(pf, "_gemm_view", None)
     if view is not None and view.nr == tile.nr:
         return view
-    if pf.source is None:
-        raise ValueError("packed filter keeps no source weights for the GEMM view")
     red = pf.kernel_elems * pf.in_channels
     p1 = ConvParams(1, 1, in_channels=red, out_channels=pf.k_out)
-    filt = FilterTensor(pf.k_out, 1, 1, red, pf.source)
+    filt = FilterTensor(pf.k_out, 1, 1, red, pf.krsc)
     view = pack_filter(filt, pf.bias, p1, tile, compute_dtype=pf.dtype, quant=pf.quant)
     pf._gemm_view = view
     return view

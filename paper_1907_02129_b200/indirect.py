@@ -156,7 +156,8 @@ def _build(in_shape: Shape4, params: ConvParams, batch: int, mr: int, offsets: t
 
 def init_indirection_buffer(input: NhwcTensor, zero_row: torch.Tensor, params: ConvParams, out_shape: Shape4,
                             tile: TileConfig, batch: int | None = None, *,
-                            index_dtype: torch.dtype = torch.int64, per_image: bool = False) -> IndirectionBuffer:
+                            index_dtype: torch.dtype = torch.int64, per_image: bool = False,
+                            _zero_facts: tuple | None = None) -> IndirectionBuffer:
     """Build the buffer for ``input`` under ``params`` on the input's device
     (indirect.py:129-164).  ``batch`` limits initialization to the first
     images (extend later with update_for_batch_growth).  ``per_image=True``
@@ -179,9 +180,14 @@ def init_indirection_buffer(input: NhwcTensor, zero_row: torch.Tensor, params: C
     tiles = _tile_count(pixels, tile.mr)
     offsets = torch.empty((tiles, params.kernel_elems, tile.mr), dtype=index_dtype, device=input.data.device)
     _build(input.shape, params, batch, tile.mr, offsets, 0, per_image)
-    zb = zero_row.reshape(-1).view(torch.uint8)
-    lo, hi = (int(v) for v in torch.aminmax(zb))
-    fill = lo if lo == hi else None
+    if _zero_facts is None:
+        # one scan of the (read-only, indirect.py:42) zero row: is it all zero
+        # bytes, or one repeated byte (a uint8 zero point)?  (a host sync)
+        zb = zero_row.reshape(-1).view(torch.uint8)
+        lo, hi = (int(v) for v in torch.aminmax(zb))
+        fill = lo if lo == hi else None
+    else:   # facts of the same zero row, known from an earlier buffer
+        fill = _zero_facts[1]
     return IndirectionBuffer(tile.mr, batch, out_shape.h, out_shape.w, params, input.shape, input.data,
                              zero_row, offsets, per_image, zero_is_zero=fill == 0, zero_fill_byte=fill)
 
@@ -216,8 +222,34 @@ def rebind_input(ib: IndirectionBuffer, new_input: NhwcTensor, new_zero: torch.T
         raise ValueError(f"rebind requires identical shape; buffer has {ib.in_shape}, "
                          f"new input has {new_input.shape}")
     out_shape = Shape4(new_input.shape.n, ib.out_h, ib.out_w, ib.params.out_channels)
+    facts = (ib.zero_is_zero, ib.zero_fill_byte) if new_zero is ib.zero_row else None
     return init_indirection_buffer(new_input, new_zero, ib.params, out_shape, TileConfig(mr=ib.mr),
-                                   batch=ib.batch, index_dtype=ib.offsets.dtype, per_image=ib.per_image)
+                                   batch=ib.batch, index_dtype=ib.offsets.dtype, per_image=ib.per_image,
+                                   _zero_facts=facts)
+
+
+def indirect_gemm_microkernel(kernel_elems: int, channels: int, packed_b_tile: torch.Tensor,
+                              row_refs: list[torch.Tensor], acc: torch.Tensor) -> torch.Tensor:
+    """Single-tile semantics of the indirect GEMM (indirect.py:215-236; the
+    paper's Listing 3): per kernel element load ``mr`` fresh row references
+    and accumulate ``channels``-long dot products into ``acc`` (mr, nr), in
+    kernel-element-major, channel-minor order with one rounded multiply and
+    one rounded add per product (gemm.py:6-15) -- bit-exact with the
+    reference for float32.  Element-wise torch ops on whatever device the
+    tensors live on; it defines what one tile of ``icv_conv`` computes (the
+    tests compare the two) and is not itself the hot path.
+    ``packed_b_tile`` is ``PackedFilter.tile(jt)``; ``row_refs`` is
+    ``IndirectionBuffer.rows_for_tile(t)``."""
+    mr = acc.shape[0]
+    if len(row_refs) < kernel_elems * mr:
+        raise ValueError("row_refs must hold kernel_elems * mr rows")
+    k = 0
+    for e in range(kernel_elems):
+        rows = torch.stack([r[:channels] for r in row_refs[e * mr:(e + 1) * mr]]).to(acc.dtype)   # (mr, C)
+        for c in range(channels):
+            acc += rows[:, c:c + 1] * packed_b_tile[k].to(acc.dtype)
+            k += 1
+    return acc
 
 
 def _check_filter(pf: PackedFilter, params: ConvParams) -> None:
@@ -237,14 +269,38 @@ def _same_binding(bound: torch.Tensor, data: torch.Tensor) -> bool:
             and bound.data_ptr() == data.data_ptr())
 
 
+ALGORITHMS = ("auto", "gather")
+
+
+def conv_flags(ib: IndirectionBuffer, pf: PackedFilter, dtype: torch.dtype, algorithm: str = "auto") -> int:
+    """The ``ib_dtype`` argument of icv_conv: index type plus the layout
+    facts the host knows about this buffer and zero row."""
+    if algorithm not in ALGORITHMS:
+        raise ValueError(f"algorithm must be one of {ALGORITHMS}")
+    return (L.TORCH_TO_ICV[ib.offsets.dtype] | (L.ICV_IB_PER_IMAGE if ib.per_image else 0)
+            | (L.ICV_IB_CANONICAL if ib.canonical else 0)
+            | (L.ICV_ZERO_ROW_ZEROS if ib.zero_is_zero else 0)
+            | (L.ICV_ZERO_ROW_ZP if (dtype == torch.uint8 and pf.quant is not None
+                                     and ib.zero_fill_byte == pf.quant.input_zero_point) else 0)
+            | (L.ICV_PREFER_GATHER if algorithm == "gather" else 0))
+
+
 def indirect_conv(input: NhwcTensor, pf: PackedFilter, ib: IndirectionBuffer, params: ConvParams,
-                  tile: TileConfig, batch: int | None = None, *, out: NhwcTensor | None = None) -> NhwcTensor:
+                  tile: TileConfig, batch: int | None = None, *, out: NhwcTensor | None = None,
+                  algorithm: str = "auto") -> NhwcTensor:
     """Convolution through the indirection buffer; no patch matrix exists
     (indirect.py:239-300).  ``batch`` may name fewer images than the buffer
     covers (logical truncation); anything else the buffer was not built for
     raises StaleBufferError.  Output dtype: float32 for float32 input
     (bit-exact with the reference), bfloat16 for bfloat16, uint8 for uint8.
-    ``out`` optionally supplies a preallocated output tensor."""
+    ``out`` optionally supplies a preallocated output tensor.
+
+    ``algorithm="gather"`` runs the IB-gather kernels (every A row fetched
+    through its buffer entry, the paper's Listing 3 mainloop) instead of the
+    specialisations a canonical buffer permits (sliding windows for
+    stride-1 R*S > 1 layers, row-sliding for the channel-poor stem, dense
+    TMA rows for 1x1 layers); the results agree within the dtype's contract
+    (bit-exact for uint8 and float32)."""
     _check_filter(pf, params)                                                             # :253
     if not _same_binding(ib.input_data, input.data):
         raise StaleBufferError("buffer is bound to a different input tensor; rebind_input first")   # :254-257
@@ -273,14 +329,10 @@ def indirect_conv(input: NhwcTensor, pf: PackedFilter, ib: IndirectionBuffer, pa
         raise ValueError(f"out must be a {input.dtype} NhwcTensor of shape {out_shape} on {dev}")
     d, s = L.desc_of(params), L.shape_of(input.shape)
     q = L.quant_of(pf.quant)
+    flags = conv_flags(ib, pf, input.dtype, algorithm)
     with torch.cuda.device(dev):
         L.check(L.lib().icv_conv(ctypes.byref(d), ctypes.byref(s), batch, L.TORCH_TO_ICV[input.dtype],
-                                 L.ptr(input.data), L.ptr(ib.zero_row), L.ptr(ib.offsets),
-                                 L.TORCH_TO_ICV[ib.offsets.dtype] | (L.ICV_IB_PER_IMAGE if ib.per_image else 0)
-                                 | (L.ICV_IB_CANONICAL if ib.canonical else 0)
-                                 | (L.ICV_ZERO_ROW_ZEROS if ib.zero_is_zero else 0)
-                                 | (L.ICV_ZERO_ROW_ZP if (input.dtype == torch.uint8 and pf.quant is not None
-                                                          and ib.zero_fill_byte == pf.quant.input_zero_point) else 0),
+                                 L.ptr(input.data), L.ptr(ib.zero_row), L.ptr(ib.offsets), flags,
                                  ib.mr, L.ptr(pf.packed),
                                  ctypes.byref(q) if q is not None else None, L.ptr(out.data), L.stream_of(dev)),
                 "icv_conv")

@@ -43,3 +43,21 @@ def make_params(r=1, s=1, sy=1, sx=1, dy=1, dx=1, pt=0, pl=0, pb=None, pr=None, 
     return ConvParams(kernel_h=r, kernel_w=s, stride_h=sy, stride_w=sx, dilation_h=dy, dilation_w=dx,
                       pad_top=pt, pad_left=pl, pad_bottom=pt if pb is None else pb,
                       pad_right=pl if pr is None else pr, in_channels=c, out_channels=k)
+
+
+@pytest.fixture
+def tune():
+    """Set native plan knobs for one test (icv_set_tuning); restored afterwards."""
+    from paper_1907_02129_b200 import _lib as L
+
+    saved = {}
+
+    def set_(**knobs):
+        for k, v in knobs.items():
+            if k not in saved:
+                saved[k] = L.get_tuning(k)
+            L.set_tuning(k, v)
+
+    yield set_
+    for k, v in saved.items():
+        L.set_tuning(k, v)

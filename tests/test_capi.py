@@ -39,7 +39,39 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_abi_version():
-    assert L.lib().icv_abi_version() == 1
+    assert L.lib().icv_abi_version() == 2
+
+
+def test_tuning_knobs_roundtrip_and_reject_unknown():
+    assert L.get_tuning("win") == -1
+    assert L.get_tuning("dense_a") == 1
+    with L.tuning(win=0, win_cs=1):
+        assert L.get_tuning("win") == 0 and L.get_tuning("win_cs") == 1
+    assert L.get_tuning("win") == -1 and L.get_tuning("win_cs") == 2
+    with pytest.raises(ValueError):
+        L.set_tuning("no_such_knob", 1)
+
+
+def test_kernel_selection_flags():
+    import torch
+
+    from paper_1907_02129_b200.workloads import CFG2, CFG3A, resnet50_layers
+
+    # the IB-gather request turns off every canonical-buffer specialisation
+    assert L.kernel_name(CFG2.params, CFG2.in_shape, torch.bfloat16) == "icv_igemm_win<bf16>"
+    g = L.DEFAULT_FLAGS | L.ICV_PREFER_GATHER
+    assert L.kernel_name(CFG2.params, CFG2.in_shape, torch.bfloat16, g) == "icv_igemm_smem<bf16>"
+    assert L.kernel_name(CFG3A.params, CFG3A.in_shape, torch.bfloat16, g) == "icv_igemm_stem<bf16>"
+    # a non-canonical buffer never takes the window / row / dense-A kernels
+    nc = L.ICV_ZERO_ROW_ZEROS
+    assert L.kernel_name(CFG2.params, CFG2.in_shape, torch.bfloat16, nc) == "icv_igemm_smem<bf16>"
+    assert L.kernel_name(CFG3A.params, CFG3A.in_shape, torch.bfloat16, nc) == "icv_igemm_stem<bf16>"
+    # 1x1 stride-1 layers: dense TMA rows unless the gather kernel is requested
+    one = [(n, s, p) for n, s, p in resnet50_layers(8) if n == "s3b2_1x1a"][0]
+    assert L.kernel_name(one[2], one[1], torch.bfloat16) == "icv_igemm_smem<bf16,dense>"
+    assert L.kernel_name(one[2], one[1], torch.bfloat16, g) == "icv_igemm_smem<bf16>"
+    with L.tuning(dense_a=0):
+        assert L.kernel_name(one[2], one[1], torch.bfloat16) == "icv_igemm_smem<bf16>"
 
 
 def _out_shape(params, shape):

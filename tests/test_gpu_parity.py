@@ -488,10 +488,10 @@ def _stem_problem(g, index_dtype=torch.int64, per_image=True, seed=13):
 ])
 @pytest.mark.parametrize("per_image,index_dtype,rows_per_tile", [(True, torch.int64, "1"), (False, torch.int64, "1"),
                                                                  (True, torch.int32, "1"), (True, torch.int64, "2")])
-def test_rows_kernel_matches_oracle(geom, per_image, index_dtype, rows_per_tile, monkeypatch):
+def test_rows_kernel_matches_oracle(geom, per_image, index_dtype, rows_per_tile, tune):
     """rows_per_tile 2: the opt-in two-output-row tiles (ICV_ROWS_RP=2; BN 64
     filters only, others keep one row per tile)."""
-    monkeypatch.setenv("ICV_ROWS_RP", rows_per_tile)
+    tune(rows_rp=int(rows_per_tile))
     p, shape, xh, wh, bias, x, pf, ib, tile, o = _stem_problem(geom, index_dtype, per_image)
     assert L.kernel_name(p, shape, torch.bfloat16) == "icv_igemm_rows<bf16>"
     y = icv.indirect_conv(x, pf, ib, p, tile).numpy().reshape(-1, p.out_channels)

@@ -26,10 +26,10 @@ DEV = "cuda"
 
 
 @pytest.fixture(autouse=True)
-def force_window(monkeypatch):
+def force_window(tune):
     """ICV_WIN=1: the window kernel takes every stride-1 layer it fits, even
     small test images whose padded tiles are mostly discarded columns."""
-    monkeypatch.setenv("ICV_WIN", "1")
+    tune(win=1)
 
 WIN_GEOMS = [
     dict(r=3, s=3, pt=1, pl=1, c=128, k=128, n=3, h=28, w=28, mr=128),            # cfg2 shape, 3 images
@@ -82,11 +82,11 @@ def test_window_kernel_matches_oracle(geom):
 
 @pytest.mark.parametrize("cs,mt", [(1, 1), (1, 2), (2, 1), (2, 2)])
 @pytest.mark.parametrize("geom", [WIN_GEOMS[0], WIN_GEOMS[2], WIN_GEOMS[3], WIN_GEOMS[4]])
-def test_window_kernel_variants(geom, cs, mt, monkeypatch):
+def test_window_kernel_variants(geom, cs, mt, tune):
     """Single CTA / CTA pair (cta_group::2, M = 256, filter rows split) x one /
     two M tiles per unit; odd image counts leave the pair's peer a dummy."""
-    monkeypatch.setenv("ICV_WIN_CS", str(cs))
-    monkeypatch.setenv("ICV_WIN_MT", str(mt))
+    tune(win_cs=cs)
+    tune(win_mt=mt)
     p, shape, xh, wh, bias, x, pf, zero, ib, tile, o = _bf16_case(geom)
     assert ib.zero_is_zero
     y = icv.indirect_conv(x, pf, ib, p, tile).numpy().reshape(-1, p.out_channels)

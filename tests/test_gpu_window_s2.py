@@ -29,8 +29,8 @@ DEV = "cuda"
 
 
 @pytest.fixture(autouse=True)
-def force_window(monkeypatch):
-    monkeypatch.setenv("ICV_WIN", "1")
+def force_window(tune):
+    tune(win=1)
 
 
 S2_GEOMS = [
@@ -81,9 +81,9 @@ def test_stride2_window_matches_oracle(geom):
 
 @pytest.mark.parametrize("cs,mt", [(1, 1), (1, 2), (2, 1), (2, 2)])
 @pytest.mark.parametrize("geom", [S2_GEOMS[0], S2_GEOMS[3], S2_GEOMS[4]])
-def test_stride2_window_variants(geom, cs, mt, monkeypatch):
-    monkeypatch.setenv("ICV_WIN_CS", str(cs))
-    monkeypatch.setenv("ICV_WIN_MT", str(mt))
+def test_stride2_window_variants(geom, cs, mt, tune):
+    tune(win_cs=cs)
+    tune(win_mt=mt)
     p, shape, x, pf, ib, tile, ref = _bf16_case(geom)
     y = icv.indirect_conv(x, pf, ib, p, tile).numpy().reshape(-1, p.out_channels)
     assert_bf16_close(y, ref)
@@ -116,11 +116,11 @@ def _u8_run(p, shape, zx, zw, zero_fill, seed=5):
     return y, ref
 
 
-def test_cfg4_window_selectable(monkeypatch):
+def test_cfg4_window_selectable(tune):
     """uint8 takes the window kernel only when forced (ICV_WIN=1 here; the
     gather kernel is faster on cfg4 today)."""
     assert L.kernel_name(CFG4.params, CFG4.in_shape, torch.uint8) == "icv_igemm_win<u8>"
-    monkeypatch.setenv("ICV_WIN", "")
+    tune(win=-1)
     assert L.kernel_name(CFG4.params, CFG4.in_shape, torch.uint8) == "icv_igemm_smem<u8>"
 
 
@@ -132,12 +132,12 @@ def test_cfg4_window_selectable(monkeypatch):
 ])
 @pytest.mark.parametrize("cs", [1, 2])
 @pytest.mark.parametrize("cls", ["1", "0"])
-def test_stride2_window_u8_zero_point_row(geom, zx, zw, cs, cls, monkeypatch):
+def test_stride2_window_u8_zero_point_row(geom, zx, zw, cs, cls, tune):
     """Zero row = input zero point (the reference's quantized padding): TMA
     zero fill + padding correction (per border class, or per padded tap with
     ICV_WIN_U8_CLS=0) must give the oracle's bytes exactly."""
-    monkeypatch.setenv("ICV_WIN_CS", str(cs))
-    monkeypatch.setenv("ICV_WIN_U8_CLS", cls)
+    tune(win_cs=cs)
+    tune(win_u8_cls=int(cls))
     p, shape = _params(geom)
     y, ref = _u8_run(p, shape, zx, zw, zero_fill=zx)
     assert np.array_equal(y, ref), int((y != ref).sum())
@@ -158,11 +158,11 @@ def test_stride2_window_u8_zeros_row_nonzero_zp():
     dict(r=3, s=3, pt=1, pl=1, c=64, k=64, h=3, w=2),                          # tiny: rows both top and bottom
 ])
 @pytest.mark.parametrize("cls", ["1", "0"])
-def test_stride1_window_u8_zero_point_row_pairs(geom, cls, monkeypatch):
+def test_stride1_window_u8_zero_point_row_pairs(geom, cls, tune):
     """Stride-1 uint8 with a zero-point zero row now also takes TMA windows
     (and CTA pairs) through the padding correction."""
-    monkeypatch.setenv("ICV_WIN_CS", "2")
-    monkeypatch.setenv("ICV_WIN_U8_CLS", cls)
+    tune(win_cs=2)
+    tune(win_u8_cls=int(cls))
     g = dict(geom)
     h, wd = g.pop("h"), g.pop("w")
     p = make_params(**g)
@@ -174,11 +174,11 @@ def test_stride1_window_u8_zero_point_row_pairs(geom, cls, monkeypatch):
     (dict(r=3, s=3, pt=1, pl=1, c=256, k=256, n=3, h=28, w=28), 128, 127),   # cfg4 geometry
     (dict(r=3, s=3, pt=1, pl=0, pb=0, pr=1, c=64, k=512, n=2, h=9, w=11), 7, 200),
 ])
-def test_u8_gather_kernel_block_n_256(geom, zx, zw, monkeypatch):
+def test_u8_gather_kernel_block_n_256(geom, zx, zw, tune):
     """Opt-in BLOCK_N 256 of the uint8 gather kernel (one accumulator stage,
     32 TMEM columns for the row sums): bit-exact."""
-    monkeypatch.setenv("ICV_WIN", "0")
-    monkeypatch.setenv("ICV_U8_BN", "256")
+    tune(win=0)
+    tune(u8_bn=256)
     p, shape = _params(geom)
     y, ref = _u8_run(p, shape, zx, zw, zero_fill=zx)
     assert np.array_equal(y, ref), int((y != ref).sum())
