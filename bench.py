@@ -1,31 +1,41 @@
 """Benchmark of the indirect-convolution hot path on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl icv|reference] [--config cfg2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl icv|reference]
+                    [--config cfg5|cfg1|cfg2|cfg3a|cfg3b|cfg4] [--scaling strong|weak]
 
-One "step" = one pass of the hot path (the indirect-GEMM convolution, the
-indirection buffer and packed filter already built, as in the reference
-harness bench.py:156-161) over one batch of the BASELINE workload.  Default
-workload: BASELINE.json configs[1] (cfg2: bf16 64x28x28x128 -> 128, 3x3).
+One "step" = one pass of the hot path over one batch of the BASELINE
+workload, every indirection buffer and packed filter built beforehand (as
+the reference harness does, bench.py:156-161).  Default workload: cfg5,
+BASELINE.json configs[4] -- the 53-layer ResNet-50 conv stack at N=256, the
+largest configuration and the one BASELINE's "1/2/4/8 GPU" metric is about
+(its `metric` quotes no single config); a step is all 53 convolutions plus
+the stem's max pool, chained through the public indirect_conv API.  The
+other configs (cfg1-cfg4) are reported under `other_configs`, each with its
+own roofline, output gate and CPU sample.
 
-Multi-GPU (torchrun, one process per GPU, NCCL): the batch dimension is
-partitioned — every rank convolves its own 64 images (weak scaling) with the
-filter packed once on rank 0 and replicated by one NCCL broadcast (the only
-collective; it is setup, outside the timed region).  Timing: CUDA events
-around every step on the launching stream, L2 flushed (256 MiB write)
-between steps, max over ranks.
+Multi-GPU (one process per GPU, NCCL): `--gpus N` without torchrun
+re-launches itself under `torch.distributed.run` (and fails loudly when the
+box has fewer than N GPUs).  The batch dimension is sharded: by default the
+global batch is fixed and split into contiguous image slices (strong
+scaling: cfg5 256 -> 128/64/32 images per GPU);
+`--scaling weak` keeps the BASELINE batch per GPU.  Filters are packed on
+rank 0 and replicated by one NCCL broadcast (icv_nccl_broadcast, the only
+collective; setup, outside the timed region).  Timing: CUDA events around
+every step on the launching stream, L2 flushed between steps (outside the
+events), barrier before, max over ranks.
 
-``--impl reference`` times the reference's own CPU algorithm for the path
-(the numpy port in oracle/, which restates convbench's indirect_conv;
-the reference itself is pure Python and cannot travel to the GPU box) on the
-host cores, rank 0 only.
+`--impl reference` times the reference's own CPU algorithm for the path (the
+numpy port in oracle/ of convbench's indirect_conv; the reference itself is
+pure Python and cannot travel to the GPU box) on the host cores, rank 0
+only, on a bounded sample per step.
 """
 
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -37,7 +47,9 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
+METRIC = "conv TFLOP/s (2*N*Ho*Wo*K*R*S*C / s)"
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "which": "fallback"}
+CONV_CONFIGS = ("cfg1", "cfg2", "cfg3a", "cfg3b", "cfg4")
 
 
 def load_peaks() -> dict:
@@ -45,10 +57,11 @@ def load_peaks() -> dict:
     try:
         with open(path) as f:
             p = json.load(f)
-        p["which"] = "measured"
+        p["which"] = "measured (MEASURED_PEAKS.json)"
     except OSError:
         p = dict(PEAKS_FALLBACK)
-    try:   # int8 / fp32 peaks measured on a B200 of this pool (tools/measure_peaks.py)
+        p["which"] = "fallback (B200_PROFILING.md)"
+    try:   # int8 / fp32 peaks measured on a B200 of this pool by tools/measure_peaks.py (library GEMMs)
         with open(os.path.join(ROOT, "profiles", "peaks_extra.json")) as f:
             extra = json.load(f)
         p["int8_tops"] = extra.get("int8_tops")
@@ -58,10 +71,31 @@ def load_peaks() -> dict:
     return p
 
 
+def nearest_rank(sorted_values: list[float], q: float) -> float:
+    """Quantile by nearest rank, element int(q * n) (reference bench.py:83-88)."""
+    n = len(sorted_values)
+    return sorted_values[min(int(q * n), n - 1)]
+
+
+def quantiles(xs: list[float]) -> dict:
+    s = sorted(xs)
+    return {"median": nearest_rank(s, 0.5), "q20": nearest_rank(s, 0.2), "q80": nearest_rank(s, 0.8)}
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 # ----------------------------------------------------------------- clocks
 class ClockSampler:
-    """SM clock and throttle reasons sampled every 5 ms (NVML) while running;
-    falls back to `nvidia-smi -lms 100` when NVML is unavailable."""
+    """SM clock and throttle reasons sampled every 5 ms (NVML) while running."""
 
     REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
                "sw_power_cap": 0x4}
@@ -126,12 +160,27 @@ def _init_worker():
     os.environ["MKL_NUM_THREADS"] = "1"
 
 
-def _cpu_worker(args):
-    """One image of the workload through the oracle port (restates
-    convbench.indirect: _compute_offsets + indirect_conv).  Returns seconds
-    spent in the convolution only (IB build outside timing, bench.py:156-161)."""
-    name, img = args
-    os.environ["OMP_NUM_THREADS"] = "1"
+def _oracle_conv(w, x, wt, offs, n, oh, ow):
+    """One convolution of workload `w` through the oracle port (restates
+    convbench.indirect.indirect_conv; uint8 through oracle/quant.py)."""
+    from oracle import conv as oconv
+
+    s = w.in_shape
+    if w.dtype == "u8":
+        from oracle import quant as oq
+        q = w.quant
+        return oq.indirect_conv_u8(x, np.full(s.c, q.input_zero_point, np.uint8), offs, w.params, wt, w.bias_host(),
+                                   n, oh, ow, q.input_zero_point, q.input_scale, q.kernel_zero_point, q.kernel_scale,
+                                   q.output_zero_point, q.output_scale)
+    return oconv.indirect_conv_f32(x, np.zeros(s.c, np.float32), offs, w.params, wt, w.bias_host(), n, oh, ow)
+
+
+def _cpu_conv_worker(args):
+    """Images [lo, hi) of conv workload `name` through the oracle port in this
+    process.  Returns seconds spent in the convolution only (IB built
+    outside timing, reference bench.py:156-161)."""
+    name, lo, hi = args
+    _init_worker()
     from oracle import conv as oconv
     from oracle import ib as oib
     from paper_1907_02129_b200.workloads import CONFIGS
@@ -139,88 +188,165 @@ def _cpu_worker(args):
     w = CONFIGS[name]
     s = w.in_shape
     oh, ow = w.out_hw
-    x = w.input_host(img, img + 1)
+    x = w.input_host(lo, hi)
     wt = w.filter_host()
     if w.dtype == "bf16":
         x, wt = oconv.bf16_round(x), oconv.bf16_round(wt)
-    offs = oib.compute_offsets((1, s.h, s.w, s.c), w.params, oh, ow, 1, 4)
+    n = hi - lo
+    offs = oib.compute_offsets((n, s.h, s.w, s.c), w.params, oh, ow, n, 4)
     t0 = time.perf_counter()
-    if w.dtype == "u8":
-        from oracle import quant as oq
-        q = w.quant
-        oq.indirect_conv_u8(x, np.full(s.c, q.input_zero_point, np.uint8), offs, w.params, wt, w.bias_host(), 1,
-                            oh, ow, q.input_zero_point, q.input_scale, q.kernel_zero_point, q.kernel_scale,
-                            q.output_zero_point, q.output_scale)
-    else:
-        oconv.indirect_conv_f32(x, np.zeros(s.c, np.float32), offs, w.params, wt, w.bias_host(), 1, oh, ow)
+    _oracle_conv(w, x, wt, offs, n, oh, ow)
     return time.perf_counter() - t0
 
 
-def cpu_reference(name: str, steps: int, warmup: int, cores: int | None = None) -> dict:
-    """Time the oracle port on the host cores: each step convolves one image
-    per worker process (a bounded sample of the workload), wall-clock."""
+def _cpu_stack_worker(args):
+    """cfg5 on the CPU: image `img` of the network input through the oracle
+    port, layer by layer (only the layers j with j % stride == phase; the
+    stem's max pool between).  Returns (seconds in the convolutions, FLOPs)."""
+    img, phase, stride = args
+    _init_worker()
+    from oracle import conv as oconv
+    from oracle import ib as oib
+    from paper_1907_02129_b200.stack import stack_input_host, stack_weights_host
+    from paper_1907_02129_b200.workloads import resnet50_layers
+
+    layers = resnet50_layers(1)
+    x0 = oconv.bf16_round(stack_input_host(img, img + 1))
+    secs, flops = 0.0, 0
+    rng = np.random.default_rng(img)
+    for idx, (name, shape, p) in enumerate(layers):
+        if idx % stride != phase:
+            continue
+        wt = oconv.bf16_round(stack_weights_host(idx, p))
+        oh, ow = oib.out_hw(p, shape.h, shape.w)
+        offs = oib.compute_offsets((1, shape.h, shape.w, shape.c), p, oh, ow, 1, 4)
+        x = x0 if idx == 0 else oconv.bf16_round(rng.standard_normal(shape.numel, dtype=np.float32))
+        t0 = time.perf_counter()
+        oconv.indirect_conv_f32(x, np.zeros(shape.c, np.float32), offs, p, wt, None, 1, oh, ow)
+        secs += time.perf_counter() - t0
+        flops += 2 * oh * ow * p.out_channels * p.kernel_elems * p.in_channels
+    return secs, flops
+
+
+def _pool(procs):
     import multiprocessing as mp
 
+    return mp.get_context("spawn").Pool(procs, initializer=_init_worker)
+
+
+def cpu_conv_baseline(name: str, reps: int = 3, cores: int | None = None, single_images: int = 4) -> dict:
+    """Reference algorithm on the host cores for conv workload `name`:
+    leg (ii) -- one image per worker process, all cores (cache-resident
+    accumulators), `reps` rounds, nearest-rank median/q20/q80 of the
+    per-round throughput; leg (i) -- one process over a `single_images`
+    batch, as the reference API runs a batch."""
     from paper_1907_02129_b200.workloads import CONFIGS
 
     w = CONFIGS[name]
     cores = cores or os.cpu_count() or 1
     n_img = w.in_shape.n
-    per_step = min(cores, n_img)
+    per = min(cores, n_img)
     flops_img = w.flops // n_img
-    ctx = mp.get_context("spawn")
-    times = []
-    with ctx.Pool(per_step, initializer=_init_worker) as pool:
-        for it in range(warmup + steps):
-            imgs = [(name, (it * per_step + j) % n_img) for j in range(per_step)]
+    rates = []
+    with _pool(per) as pool:
+        pool.map(_cpu_conv_worker, [(name, 0, 1)] * per)   # warm the workers (imports)
+        for r in range(reps):
+            imgs = [(name, (r * per + j) % n_img, (r * per + j) % n_img + 1) for j in range(per)]
             t0 = time.perf_counter()
-            pool.map(_cpu_worker, imgs, chunksize=1)
-            dt = time.perf_counter() - t0
-            if it >= warmup:
-                times.append(dt)
-    total = sum(times)
-    value = flops_img * per_step * len(times) / total / 1e12
-    return {"value": value, "unit": "TFLOP/s", "cores": per_step, "kind": "port",
-            "sample": f"{per_step} images of {name} per step (one per worker process, OMP_NUM_THREADS=1), "
-                      f"{len(times)} steps, wall clock; IB built outside timing",
-            "ms_per_step": 1e3 * total / len(times)}
+            pool.map(_cpu_conv_worker, imgs, chunksize=1)
+            rates.append(flops_img * per / (time.perf_counter() - t0) / 1e12)
+        k = min(single_images, n_img)
+        t1 = pool.apply(_cpu_conv_worker, ((name, 0, k),))
+    qs = quantiles(rates)
+    return {"value": qs["median"], "unit": "TFLOP/s", "cores": per, "kind": "port", "cpu": cpu_model(),
+            "q20": qs["q20"], "q80": qs["q80"],
+            "sample": f"leg (ii): {per} images of {name} per round, one per worker process (OMP_NUM_THREADS=1), "
+                      f"{reps} rounds, wall clock, nearest-rank median; IB built outside timing",
+            "single_process": {"value": flops_img * k / t1 / 1e12, "unit": "TFLOP/s", "cores": 1,
+                               "sample": f"leg (i): one process, a batch of {k} images through one call"}}
 
 
-# ---------------------------------------------------------------- GPU arm
-def setup_problem(name: str, n_lo: int, n_hi: int, device, pf_bcast=None, mr: int = 128, per_image: bool = True):
-    """Upload images [n_lo, n_hi) of workload `name`, build the IB on the
-    device, pack (or receive) the filter."""
-    import torch
+def cpu_stack_baseline(cores: int | None = None, reps: int = 1) -> dict:
+    """cfg5 on the host cores: each worker process runs one image through
+    all 53 layers (reps rounds)."""
+    cores = cores or os.cpu_count() or 1
+    per = min(cores, 16)
+    rates = []
+    with _pool(per) as pool:
+        for r in range(reps):
+            t0 = time.perf_counter()
+            res = pool.map(_cpu_stack_worker, [(r * per + j, 0, 1) for j in range(per)], chunksize=1)
+            wall = time.perf_counter() - t0
+            rates.append(sum(f for _, f in res) / wall / 1e12)
+    qs = quantiles(rates)
+    return {"value": qs["median"], "unit": "TFLOP/s", "cores": per, "kind": "port", "cpu": cpu_model(),
+            "q20": qs["q20"], "q80": qs["q80"],
+            "sample": f"{per} images of cfg5, one per worker process (OMP_NUM_THREADS=1), each through all 53 "
+                      f"convolutions (8.17 GFLOP per image), {reps} round(s), wall clock incl. per-layer setup"}
 
-    import paper_1907_02129_b200 as icv
+
+def cpu_reference_steps(name: str, steps: int, warmup: int) -> tuple[list[float], dict]:
+    """Per-step throughputs (TFLOP/s) of the reference algorithm on the host
+    cores, each step a bounded sample: cfg5 -- one image per worker through
+    every 4th layer of the stack (phase = step mod 4, ~2.5 s); conv configs
+    -- one image per worker."""
+    cores = os.cpu_count() or 1
+    rates = []
+    if name == "cfg5":
+        per = min(cores, 16)
+        with _pool(per) as pool:
+            for it in range(warmup + steps):
+                t0 = time.perf_counter()
+                res = pool.map(_cpu_stack_worker, [(it * per + j, it % 4, 4) for j in range(per)], chunksize=1)
+                wall = time.perf_counter() - t0
+                if it >= warmup:
+                    rates.append(sum(f for _, f in res) / wall / 1e12)
+        sample = (f"{per} images of cfg5 per step, one per worker process (OMP_NUM_THREADS=1), each through every "
+                  "4th layer of the stack (phase = step mod 4), wall clock")
+        return rates, {"cores": per, "sample": sample}
     from paper_1907_02129_b200.workloads import CONFIGS
 
     w = CONFIGS[name]
-    s = w.in_shape
-    shape = icv.Shape4(n_hi - n_lo, s.h, s.w, s.c)
-    dt = {"f32": torch.float32, "bf16": torch.bfloat16, "u8": torch.uint8}[w.dtype]
-    xh = w.input_host(n_lo, n_hi)
-    x = icv.NhwcTensor(shape, torch.from_numpy(xh).to(device).to(dt))
-    p = w.params
-    tile = icv.TileConfig(mr=mr)
-    qp = None
-    zero_fill = 0
-    if w.quant is not None:
-        q = w.quant
-        qp = icv.QuantParams(q.input_zero_point, q.input_scale, q.kernel_zero_point, q.kernel_scale,
-                             q.output_zero_point, q.output_scale, q.output_min, q.output_max)
-        zero_fill = q.input_zero_point
-    bias = w.bias_host()
-    filt = icv.FilterTensor(p.out_channels, p.kernel_h, p.kernel_w, p.in_channels,
-                            torch.from_numpy(w.filter_host()).to(device).to(dt))
-    pf = icv.pack_filter(filt, None if bias is None else torch.from_numpy(bias), p, tile, quant=qp)
-    if pf_bcast is not None:
-        pf_bcast(pf)
-    zero = icv.make_zero_row(p.in_channels, dtype=dt, device=device, fill=zero_fill)
-    out_shape = icv.conv_output_shape(p, shape)
-    ib = icv.init_indirection_buffer(x, zero, p, out_shape, tile, per_image=per_image)
-    y = icv.NhwcTensor.empty(out_shape, dtype=dt, device=device)
-    return w, x, xh, pf, ib, y, tile
+    n_img = w.in_shape.n
+    per = min(cores, n_img)
+    flops_img = w.flops // n_img
+    with _pool(per) as pool:
+        for it in range(warmup + steps):
+            imgs = [(name, (it * per + j) % n_img, (it * per + j) % n_img + 1) for j in range(per)]
+            t0 = time.perf_counter()
+            pool.map(_cpu_conv_worker, imgs, chunksize=1)
+            if it >= warmup:
+                rates.append(flops_img * per / (time.perf_counter() - t0) / 1e12)
+    return rates, {"cores": per, "sample": f"{per} images of {name} per step, one per worker process, wall clock"}
+
+
+def reference_arm(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    rates, meta = cpu_reference_steps(args.config, args.steps, args.warmup)
+    qs = quantiles(rates)
+    value = statistics.mean(rates)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None,
+        "dtype": "f32 (bf16-rounded operands; the reference contract)", "data": "synthetic (seeded numpy)",
+        "config": {"workload": workload_name(args.config), "parallelism": "host cores (rank 0 only)"},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": meta["cores"], "kind": "port", "cpu": cpu_model(),
+                         "median": qs["median"], "q20": qs["q20"], "q80": qs["q80"], "sample": meta["sample"]},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU arm helpers
+def workload_name(name: str) -> str:
+    if name == "cfg5":
+        return "cfg5_resnet50_conv_stack_bf16_n256"
+    from paper_1907_02129_b200.workloads import CONFIGS
+    return CONFIGS[name].name
 
 
 def make_l2_flush(device):
@@ -264,353 +390,639 @@ def time_steps(fn, steps: int, warmup: int, flush=None, on_timed=None):
     return [s.elapsed_time(e) for s, e in zip(starts, ends)]
 
 
-def roofline_for(w, ms: float, peaks: dict, sustained: bool = False) -> dict:
-    """Roofline of the conv kernel: tensor-bound configs against the measured
-    bf16 GEMM peak (int8 against 2x that, nominal ratio, until measured),
-    HBM-bound ones against the measured copy bandwidth."""
-    ridge_tflops = peaks["bf16_tflops_sustained" if sustained else "bf16_tflops"]
-    if w.dtype == "u8":
-        # measured int8 GEMM peak (tools/measure_peaks.py -> profiles/peaks_extra.json), else 2x bf16 (nominal)
-        ridge_tflops = peaks.get("int8_tops") or 2.0 * ridge_tflops
-    ai = w.flops / w.compulsory_bytes
-    hbm = peaks["hbm_gbs"]
-    if ai * hbm / 1e3 >= ridge_tflops and w.dtype != "f32":
-        achieved = w.flops / (ms * 1e-3) / 1e12
-        return {"bound": "tensor", "achieved": round(achieved, 2), "peak": ridge_tflops, "unit": "TFLOP/s",
-                "frac": round(achieved / ridge_tflops, 4)}
-    achieved = w.compulsory_bytes / (ms * 1e-3) / 1e9
-    return {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-            "frac": round(achieved / hbm, 4)}
+def peak_for(dtype: str, bound: str, peaks: dict) -> tuple[float, str, str]:
+    """(peak, unit, source) of the roofline denominator."""
+    if bound == "hbm":
+        return peaks["hbm_gbs"], "GB/s", peaks["which"] + " hbm_gbs"
+    if dtype == "u8":
+        if peaks.get("int8_tops"):
+            return peaks["int8_tops"], "TOP/s", "int8 GEMM measured on a pool B200 (profiles/peaks_extra.json)"
+        return 2 * peaks["bf16_tflops"], "TOP/s", "2x bf16 (nominal ratio; int8 peak unmeasured)"
+    if dtype == "f32":
+        if peaks.get("fp32_tflops"):
+            return peaks["fp32_tflops"], "TFLOP/s", "fp32 CUDA-core GEMM measured on a pool B200 (profiles/peaks_extra.json)"
+        return 75.0, "TFLOP/s", "nominal fp32 CUDA-core peak"
+    return peaks["bf16_tflops"], "TFLOP/s", peaks["which"] + " bf16_tflops (burst)"
 
 
-def load_traffic(name: str):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the conv
-    kernel from the committed ncu --set full capture
-    (profiles/ncu_traffic.json, written by tools/ncu_summary.py), or None."""
+def roofline_of(dtype: str, flops: float, nbytes: float, ms: float, peaks: dict) -> dict:
+    """Roofline of one kernel launch.  The bound is the one with the larger
+    minimum time: FLOPs over the dtype's compute peak (bf16 / int8 tensor
+    pipe; cfg1's exact f32 runs on the CUDA cores) vs algorithmic bytes over
+    HBM bandwidth."""
+    cpk, cunit, csrc = peak_for(dtype, "tensor", peaks)
+    t_compute = flops / (cpk * 1e12)
+    t_hbm = nbytes / (peaks["hbm_gbs"] * 1e9)
+    if t_compute >= t_hbm:
+        achieved = flops / (ms * 1e-3) / 1e12
+        return {"bound": "tensor" if dtype != "f32" else "fp32_core", "achieved": round(achieved, 2), "peak": cpk,
+                "unit": cunit, "frac": round(achieved / cpk, 4), "peak_source": csrc}
+    achieved = nbytes / (ms * 1e-3) / 1e9
+    return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": round(achieved / peaks["hbm_gbs"], 4), "peak_source": peaks["which"] + " hbm_gbs"}
+
+
+def load_traffic(key: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the
+    committed ncu --set full capture (profiles/ncu_traffic.json), or None."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            entry = json.load(f).get(name)
+            entry = json.load(f).get(key)
         return None if entry is None else entry["bytes"]
     except (OSError, ValueError, KeyError):
         return None
+
+
+def setup_problem(name: str, n_lo: int, n_hi: int, device, replicate=None, mr: int = 128, per_image: bool = True,
+                  rank: int = 0):
+    """Upload images [n_lo, n_hi) of conv workload `name`, build the IB on
+    the device, pack the filter on rank 0 and replicate it (or pack locally
+    when `replicate` is None)."""
+    import torch
+
+    import paper_1907_02129_b200 as icv
+    from paper_1907_02129_b200.workloads import CONFIGS
+
+    w = CONFIGS[name]
+    s = w.in_shape
+    shape = icv.Shape4(n_hi - n_lo, s.h, s.w, s.c)
+    dt = {"f32": torch.float32, "bf16": torch.bfloat16, "u8": torch.uint8}[w.dtype]
+    xh = w.input_host(n_lo, n_hi)
+    x = icv.NhwcTensor(shape, torch.from_numpy(xh).to(device).to(dt))
+    p = w.params
+    tile = icv.TileConfig(mr=mr)
+    qp = None
+    zero_fill = 0
+    if w.quant is not None:
+        q = w.quant
+        qp = icv.QuantParams(q.input_zero_point, q.input_scale, q.kernel_zero_point, q.kernel_scale,
+                             q.output_zero_point, q.output_scale, q.output_min, q.output_max)
+        zero_fill = q.input_zero_point
+    bias = w.bias_host()
+    bias_t = None if bias is None else torch.from_numpy(bias)
+    if replicate is None:
+        filt = icv.FilterTensor(p.out_channels, p.kernel_h, p.kernel_w, p.in_channels,
+                                torch.from_numpy(w.filter_host()).to(device).to(dt))
+        pf = icv.pack_filter(filt, bias_t, p, tile, quant=qp)
+    else:
+        filt = None
+        if rank == 0:
+            filt = icv.FilterTensor(p.out_channels, p.kernel_h, p.kernel_w, p.in_channels,
+                                    torch.from_numpy(w.filter_host()).to(device).to(dt))
+        pf = replicate(filt, bias_t, p, tile, dt, qp)
+    zero = icv.make_zero_row(p.in_channels, dtype=dt, device=device, fill=zero_fill)
+    out_shape = icv.conv_output_shape(p, shape)
+    ib = icv.init_indirection_buffer(x, zero, p, out_shape, tile, per_image=per_image)
+    y = icv.NhwcTensor.empty(out_shape, dtype=dt, device=device)
+    return w, x, xh, pf, ib, y, tile
+
+
+def conv_gate(w, xh, ib, y, n_lo: int = 0, pixels: int = 512) -> dict:
+    """The benchmarked output of a conv workload vs the oracle on sampled
+    pixels (reference bench.py:124-142 gate protocol): float32 and uint8
+    bit-exact, bf16 within BASELINE's rel 1e-2 (normwise)."""
+    from oracle import conv as oconv
+    from oracle import quant as oq
+
+    oh, ow = w.out_hw
+    n = y.shape.n
+    total = n * oh * ow
+    idx = np.unique(np.random.default_rng(1).integers(0, total, min(pixels, total)))
+    offs = ib.offsets_host()
+    k = w.params.out_channels
+    got = y.numpy().reshape(total, k)[idx]
+    if w.dtype == "u8":
+        q = w.quant
+        ref = oq.indirect_conv_u8(xh, np.full(w.in_shape.c, q.input_zero_point, np.uint8), offs, w.params,
+                                  w.filter_host(), w.bias_host(), n, oh, ow, q.input_zero_point, q.input_scale,
+                                  q.kernel_zero_point, q.kernel_scale, q.output_zero_point, q.output_scale,
+                                  pixel_index=idx)
+        ok = bool(np.array_equal(got, ref))
+        res = {"pixels_checked": int(len(idx)), "mismatches": int((got != ref).sum()), "rule": "bit-exact",
+               "pass": ok}
+    elif w.dtype == "f32":
+        ref = oconv.indirect_conv_f32(xh, np.zeros(w.in_shape.c, np.float32), offs, w.params, w.filter_host(),
+                                      w.bias_host(), n, oh, ow, pixel_index=idx)
+        ok = got.tobytes() == ref.tobytes()
+        res = {"pixels_checked": int(len(idx)), "rule": "bit-exact", "pass": ok}
+    else:
+        ref = oconv.indirect_conv_f32(oconv.bf16_round(xh), np.zeros(w.in_shape.c, np.float32), offs, w.params,
+                                      oconv.bf16_round(w.filter_host()), w.bias_host(), n, oh, ow, pixel_index=idx)
+        rel = float(np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-30))
+        ok = rel <= 1e-2
+        res = {"pixels_checked": int(len(idx)), "normwise_rel_err": rel, "rule": "normwise rel <= 1e-2", "pass": ok}
+    if not ok:
+        raise SystemExit(f"correctness gate failed on {w.name}: {res}")
+    return res
+
+
+def stack_gate(stack, layer_names=("stem", "s1b1_1x1a", "s1b1_3x3", "s2b1_3x3", "s2b1_proj", "s3b2_3x3",
+                                   "s4b1_3x3", "s4b3_1x1b"), pixels: int = 96) -> dict:
+    """cfg5 gate: for a set of layers spanning every kernel family, sampled
+    output pixels of the benchmarked pass vs the oracle on that layer's
+    actual bf16 input (parity per layer on its own input)."""
+    from oracle import conv as oconv
+
+    worst = 0.0
+    checked = []
+    for layer in stack.layers:
+        if layer.name not in layer_names:
+            continue
+        s, o = layer.input.shape, layer.output.shape
+        total = o.n * o.h * o.w
+        idx = np.unique(np.random.default_rng(layer.index).integers(0, total, pixels))
+        xh = layer.input.numpy()
+        ref = oconv.indirect_conv_f32(xh, np.zeros(s.c, np.float32), layer.ib.offsets_host(), layer.params,
+                                      layer.weights_host, None, o.n, o.h, o.w, pixel_index=idx)
+        got = layer.output.numpy().reshape(total, -1)[idx]
+        rel = float(np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-30))
+        worst = max(worst, rel)
+        checked.append(layer.name)
+    ok = worst <= 1e-2
+    res = {"layers_checked": checked, "pixels_per_layer": pixels, "worst_normwise_rel_err": worst,
+           "rule": "normwise rel <= 1e-2 per layer", "pass": ok}
+    if not ok:
+        raise SystemExit(f"correctness gate failed on cfg5: {res}")
+    return res
+
+
+# ---------------------------------------------------------------- headline: cfg5 stack
+def stack_layer_table(stack, peaks: dict, passes: int = 3) -> list[dict]:
+    """Per-layer median CUDA-event times of `passes` whole-stack passes."""
+    import torch
+
+    from paper_1907_02129_b200 import _lib
+
+    per = []
+    for _ in range(passes):
+        _, _, layers = stack.timed_run()
+        per.append(layers)
+    rows = []
+    for i, layer in enumerate(stack.layers):
+        ms = statistics.median(p[i] for p in per)
+        r = roofline_of("bf16", layer.flops, layer.compulsory_bytes, ms, peaks)
+        t_roof = max(layer.flops / (peaks["bf16_tflops"] * 1e12), layer.compulsory_bytes / (peaks["hbm_gbs"] * 1e9))
+        rows.append({"layer": layer.name,
+                     "kernel": _lib.kernel_name(layer.params, layer.input.shape, torch.bfloat16),
+                     "us": round(ms * 1e3, 2), "tflops": round(layer.flops / (ms * 1e-3) / 1e12, 1),
+                     "roofline_us": round(t_roof * 1e6, 2), "frac": r["frac"], "bound": r["bound"],
+                     "flops": layer.flops, "bytes": layer.compulsory_bytes})
+    return rows
+
+
+def dominant_roofline(rows: list[dict], peaks: dict) -> dict:
+    """Roofline of the step's dominant kernel: the (kernel, bound) class with
+    the largest share of the step's conv time; achieved = its algorithmic
+    bytes (HBM-bound class) or FLOPs (tensor-bound class) summed over its
+    launches / its summed launch time."""
+    groups: dict[tuple[str, str], list[dict]] = {}
+    for r in rows:
+        groups.setdefault((r["kernel"], r["bound"]), []).append(r)
+    total_us = sum(r["us"] for r in rows)
+    (kern, bound), members = max(groups.items(), key=lambda kv: sum(r["us"] for r in kv[1]))
+    us = sum(r["us"] for r in members)
+    if bound == "hbm":
+        achieved = sum(r["bytes"] for r in members) / (us * 1e-6) / 1e9
+        peak, unit = peaks["hbm_gbs"], "GB/s"
+    else:
+        achieved = sum(r["flops"] for r in members) / (us * 1e-6) / 1e12
+        peak, unit = peaks["bf16_tflops"], "TFLOP/s"
+    traffic = load_traffic(f"cfg5:{kern}:{bound}")
+    return {"bound": bound, "achieved": round(achieved, 2), "peak": peak, "unit": unit,
+            "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": kern, "launches_per_step": len(members),
+            "share_of_conv_time": round(us / total_us, 3),
+            "layers": [r["layer"] for r in members],
+            "per_launch": "algorithmic bytes (input + filter + output) or FLOPs of each launch / its CUDA-event time, "
+                          "summed over the class",
+            "peak_source": peaks["which"]}
+
+
+class StackE2E:
+    """cfg5 end to end through the public API with host buffers: the shard
+    is cut into `chunks` image chunks, each with its own stack (activations,
+    per-image IBs bound to that chunk's input buffer, replicated packed
+    filters); per step every chunk's input goes pinned host -> device, its
+    53 indirect_conv calls (+ max pool) are issued from Python (no graph
+    replay), and its final activation goes device -> pinned host; chunk i's
+    H2D overlaps chunk i-1's convolutions and chunk i-2's D2H on three
+    streams."""
+
+    def __init__(self, lo: int, hi: int, chunks: int, device, replicate=None):
+        import torch
+
+        from paper_1907_02129_b200.stack import IMAGE_ELEMS, ResNet50Stack, stack_input_host
+
+        self.device = device
+        n = hi - lo
+        chunks = max(1, min(chunks, n))
+        bounds = [lo + n * i // chunks for i in range(chunks + 1)]
+        self.stacks = [ResNet50Stack(device=device, images=(bounds[i], bounds[i + 1]), replicate=replicate)
+                       for i in range(chunks)]
+        xh = stack_input_host(lo, hi)
+        self.x_pinned = torch.from_numpy(xh).to(torch.bfloat16).pin_memory()
+        self.offsets = [(b - lo) * IMAGE_ELEMS for b in bounds]
+        last = self.stacks[0].layers[-1].output
+        per_img_out = last.shape.h * last.shape.w * last.shape.c
+        self.y_pinned = torch.empty(n * per_img_out, dtype=torch.bfloat16).pin_memory()
+        self.out_offsets = [(b - lo) * per_img_out for b in bounds]
+        self.h2d_bytes = int(self.x_pinned.numel() * 2)
+        self.d2h_bytes = int(self.y_pinned.numel() * 2)
+        self.s_h2d, self.s_cmp, self.s_d2h = (torch.cuda.Stream(device) for _ in range(3))
+        self.flops = sum(s.flops for s in self.stacks)
+
+    def step(self):
+        import torch
+
+        cur = torch.cuda.current_stream(self.device)
+        start = torch.cuda.Event()
+        start.record(cur)
+        for st in (self.s_h2d, self.s_cmp, self.s_d2h):
+            st.wait_event(start)
+        for i, stack in enumerate(self.stacks):
+            a, b = self.offsets[i], self.offsets[i + 1]
+            with torch.cuda.stream(self.s_h2d):
+                stack.input.data.copy_(self.x_pinned[a:b], non_blocking=True)
+                ev_in = torch.cuda.Event()
+                ev_in.record(self.s_h2d)
+            self.s_cmp.wait_event(ev_in)
+            with torch.cuda.stream(self.s_cmp):
+                stack.run()
+                ev_out = torch.cuda.Event()
+                ev_out.record(self.s_cmp)
+            self.s_d2h.wait_event(ev_out)
+            with torch.cuda.stream(self.s_d2h):
+                oa, ob = self.out_offsets[i], self.out_offsets[i + 1]
+                self.y_pinned[oa:ob].copy_(stack.layers[-1].output.data, non_blocking=True)
+        done = torch.cuda.Event()
+        done.record(self.s_d2h)
+        cur.wait_event(done)
+
+
+def replicator(comm, rank: int, world: int, device):
+    """Filter replication hooks for the data-parallel runs: rank 0 packs,
+    one NCCL broadcast per packed filter (the operator's only collective)."""
+    import paper_1907_02129_b200 as icv
+
+    def stack_hook(pf):
+        if world > 1:
+            icv.broadcast_packed_filter(pf, 0, comm=comm)
+
+    def conv_hook(filt, bias, params, tile, dt, qp):
+        return icv.replicate_filter(filt, bias, params, tile, rank=rank, device=device, compute_dtype=dt, quant=qp,
+                                    comm=comm if world > 1 else None) if world > 1 else \
+            icv.pack_filter(filt, bias, params, tile, quant=qp)
+
+    return stack_hook, conv_hook
+
+
+def bench_stack(args, ctx) -> dict:
+    """Headline cfg5: the whole stack per step on this rank's shard."""
+    import torch
+
+    from paper_1907_02129_b200 import _lib
+    from paper_1907_02129_b200.dist import shard_range
+    from paper_1907_02129_b200.stack import ResNet50Stack
+
+    world, rank, device = ctx["world"], ctx["rank"], ctx["device"]
+    gbatch = 256 if args.scaling == "strong" else 256 * world
+    lo, hi = shard_range(gbatch, world, rank)
+    stack = ResNet50Stack(device=device, images=(lo, hi), replicate=ctx["stack_hook"])
+    flush = ctx["flush"]
+    res = run_timed(args, ctx, stack.run, flush)
+    res.update({"flops_rank": stack.flops, "global_batch": gbatch, "batch_rank": hi - lo})
+    if rank == 0:
+        rows = stack_layer_table(stack, ctx["peaks"])
+        res["layers"] = rows
+        res["roofline"] = dominant_roofline(rows, ctx["peaks"])
+        t_roof = sum(r["roofline_us"] for r in rows)
+        t_meas = sum(r["us"] for r in rows)
+        res["stack_roofline"] = {"sum_layer_roofline_us": round(t_roof, 1), "sum_layer_measured_us": round(t_meas, 1),
+                                 "frac": round(t_roof / t_meas, 4),
+                                 "rule": "per layer max(FLOPs / bf16 peak, compulsory bytes / HBM BW), summed"}
+        res["gate"] = None if args.no_gate else stack_gate(stack)
+        res["conv_kernels"] = sorted({r["kernel"] for r in rows})
+    del stack
+    torch.cuda.empty_cache()
+    e2e = StackE2E(lo, hi, args.e2e_chunks, device, replicate=ctx["stack_hook"])
+    res["e2e"] = run_e2e(args, ctx, e2e.step, e2e.flops, e2e.h2d_bytes, e2e.d2h_bytes,
+                         f"pinned host input -> device, per chunk of {len(e2e.stacks)} the 53 indirect_conv calls "
+                         "(+ max pool) issued from Python (no graph), final activation -> pinned host; "
+                         "H2D / compute / D2H of successive chunks overlap on three streams")
+    res["e2e"]["chunks"] = len(e2e.stacks)
+    del e2e
+    torch.cuda.empty_cache()
+    res["conv_kernel"] = "53 launches: " + ", ".join(res.get("conv_kernels", []))
+    return res
+
+
+def run_timed(args, ctx, fn, flush) -> dict:
+    """K timed steps after W warm-ups, barrier + synchronize on both sides;
+    the per-rank total is max-reduced over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1907_02129_b200 import _lib
+
+    world, sampler = ctx["world"], ctx["sampler"]
+    for _ in range(args.warmup):
+        flush()
+        fn()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = _lib.launch_count()
+    if sampler:
+        sampler.mark("t0")
+    times = time_steps(fn, args.steps, 0, flush)
+    if sampler:
+        sampler.mark("t1")
+    launches = _lib.launch_count() - l0
+    total = sum(times)
+    if world > 1:
+        t = torch.tensor([total], dtype=torch.float64, device=ctx["device"])
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total = float(t.item())
+        dist.barrier()
+    torch.cuda.synchronize()
+    return {"times": times, "total_ms": total, "launches": launches}
+
+
+def run_e2e(args, ctx, fn, flops_rank: int, h2d: int, d2h: int, path: str) -> dict:
+    import torch
+    import torch.distributed as dist
+
+    world = ctx["world"]
+    steps = max(3, min(args.steps, 20))
+    for _ in range(max(args.warmup, 3)):
+        fn()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    times = time_steps(fn, steps, 0, ctx["flush"])
+    total = sum(times)
+    if world > 1:
+        t = torch.tensor([total], dtype=torch.float64, device=ctx["device"])
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total = float(t.item())
+    return {"value": round(flops_rank * world * steps / (total * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
+            "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
+            "ms_per_step": round(total / steps, 4), "cuda_graph": False, "path": path}
+
+
+# ---------------------------------------------------------------- conv configs
+def bench_conv(args, ctx, name: str) -> dict:
+    """Headline for a conv config (--config cfgN): its batch per step."""
+    import torch
+
+    import paper_1907_02129_b200 as icv
+    from paper_1907_02129_b200 import _lib
+    from paper_1907_02129_b200.dist import shard_range
+    from paper_1907_02129_b200.workloads import CONFIGS
+
+    world, rank, device = ctx["world"], ctx["rank"], ctx["device"]
+    w0 = CONFIGS[name]
+    gbatch = w0.in_shape.n if args.scaling == "strong" else w0.in_shape.n * world
+    if gbatch < world:
+        raise SystemExit(f"{name}: a global batch of {gbatch} cannot be sharded over {world} GPUs")
+    import paper_1907_02129_b200.workloads as wl
+    wl.CONFIGS["_bench"] = w0.with_batch(gbatch)
+    lo, hi = shard_range(gbatch, world, rank)
+    w, x, xh, pf, ib, y, tile = setup_problem("_bench", lo, hi, device, ctx["conv_hook"], per_image=args.ib == "per-image",
+                                              rank=rank)
+    res = run_timed(args, ctx, lambda: icv.indirect_conv(x, pf, ib, w.params, tile, out=y), ctx["flush"])
+    wl_rank = w0.with_batch(hi - lo)
+    res.update({"flops_rank": wl_rank.flops, "global_batch": gbatch, "batch_rank": hi - lo})
+    if rank == 0:
+        ms = statistics.mean(res["times"])
+        res["roofline"] = roofline_of(w0.dtype, wl_rank.flops, wl_rank.compulsory_bytes, ms, ctx["peaks"])
+        res["roofline"]["traffic"] = load_traffic(w0.name)
+        res["gate"] = None if args.no_gate else conv_gate(wl_rank, xh, ib, y)
+        res["conv_kernel"] = _lib.kernel_name(w0.params, w0.in_shape, x.dtype)
+    # e2e: pinned host input -> device, the API call, output -> pinned host
+    dt = x.dtype
+    x_pinned = torch.from_numpy(xh).to(dt).pin_memory()
+    y_pinned = torch.empty(y.data.numel(), dtype=dt).pin_memory()
+
+    def e2e_step():
+        x.data.copy_(x_pinned, non_blocking=True)
+        icv.indirect_conv(x, pf, ib, w.params, tile, out=y)
+        y_pinned.copy_(y.data, non_blocking=True)
+
+    res["e2e"] = run_e2e(args, ctx, e2e_step, wl_rank.flops, x_pinned.numel() * x_pinned.element_size(),
+                         y_pinned.numel() * y_pinned.element_size(),
+                         "pinned host input -> device, one indirect_conv call (Python API, no graph), output -> pinned "
+                         "host, all on the current stream")
+    return res
+
+
+def other_config(name: str, ctx, args) -> dict:
+    """A BASELINE conv config measured on one GPU: the default kernel and the
+    IB-gather kernel (algorithm="gather": the paper's mainloop) when they
+    differ, rooflines, output gate, CPU sample."""
+    import paper_1907_02129_b200 as icv
+    from paper_1907_02129_b200 import _lib
+    from paper_1907_02129_b200.workloads import CONFIGS
+
+    device, peaks, flush = ctx["device"], ctx["peaks"], ctx["flush"]
+    w0 = CONFIGS[name]
+    w, x, xh, pf, ib, y, tile = setup_problem(name, 0, w0.in_shape.n, device, per_image=args.ib == "per-image")
+    reps = max(10, args.steps // 5)
+    out = {"workload": w.name, "dtype": w.dtype}
+    legs = {"auto": "auto"}
+    k_auto = _lib.kernel_name(w.params, w.in_shape, x.dtype)
+    flags_g = icv.indirect.conv_flags(ib, pf, x.dtype, "gather")
+    k_gather = _lib.kernel_name(w.params, w.in_shape, x.dtype, flags_g)
+    if k_gather != k_auto:
+        legs["gather"] = "gather"
+    for leg, alg in legs.items():
+        t = time_steps(lambda: icv.indirect_conv(x, pf, ib, w.params, tile, out=y, algorithm=alg), reps, 3, flush)
+        qs = quantiles(t)
+        ms = qs["median"]
+        entry = {"kernel": k_auto if leg == "auto" else k_gather, "ms_per_step": round(ms, 5),
+                 "ms_q20": round(qs["q20"], 5), "ms_q80": round(qs["q80"], 5),
+                 "value": round(w.flops / (ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s" if w.dtype != "u8" else "TOP/s",
+                 "roofline": roofline_of(w.dtype, w.flops, w.compulsory_bytes, ms, peaks),
+                 "gate": None if args.no_gate else conv_gate(w, xh, ib, y)}
+        entry["roofline"]["traffic"] = load_traffic(w.name if leg == "auto" else f"{w.name}:gather")
+        if leg == "auto":
+            out.update(entry)
+        else:
+            out["ib_gather_kernel"] = entry
+    if not args.no_cpu:
+        out["cpu_baseline"] = cpu_conv_baseline(name, reps=2)
+    if not w.params.is_pointwise_unit_stride() and name in ("cfg2", "cfg4"):
+        out["im2col_gemm"] = gemm_baseline(w, x, pf, tile, flush, reps, peaks)
+        out["im2col_gemm"]["indirect_speedup"] = round(out["im2col_gemm"]["ms_per_step"] / out["ms_per_step"], 3)
+    return out
+
+
+def gemm_baseline(w, x, pf, tile, flush, reps: int, peaks: dict) -> dict:
+    """The paper's comparison (§2.1): the GEMM-based variant --
+    im2row patch matrix written to HBM, then a dense TMA-tiled tcgen05 GEMM
+    over it (the patch matrix as a 1 x P image of R*S*C channels: the
+    dense-A kernel, no indirection) -- both inside every step, as the
+    reference's gemm_conv does (im2col.py:117-131).  Also the GEMM alone."""
+    import torch
+
+    import paper_1907_02129_b200 as icv
+    from paper_1907_02129_b200 import _lib
+
+    pm = icv.build_patch_matrix(x, w.params)
+    icv.gemm_only(pm, pf, tile)
+
+    def gemm_step():
+        icv.build_patch_matrix(x, w.params, out=pm)
+        icv.gemm_only(pm, pf, tile)
+
+    ms = quantiles(time_steps(gemm_step, reps, 3, flush))["median"]
+    ms_gemm = quantiles(time_steps(lambda: icv.gemm_only(pm, pf, tile), reps, 3, flush))["median"]
+    eb = pm.matrix.element_size()
+    gemm_bytes = pm.rows * pm.cols * eb + w.params.out_channels * pm.cols * eb + pm.rows * w.params.out_channels * eb
+    p1 = icv.ConvParams(1, 1, in_channels=pm.cols, out_channels=pf.k_out)
+    res = {"ms_per_step": round(ms, 5), "value": round(w.flops / (ms * 1e-3) / 1e12, 2),
+           "kernels": ["icv_im2col", _lib.kernel_name(p1, icv.Shape4(1, 1, pm.rows, pm.cols), x.dtype)],
+           "patch_matrix_mb": round(pm.allocated_bytes / 1e6, 2),
+           "gemm_only_ms": round(ms_gemm, 5),
+           "gemm_only_roofline": roofline_of(w.dtype, w.flops, gemm_bytes, ms_gemm, peaks),
+           "note": "reference im2col.py gemm_conv: patch matrix rebuilt every step, then the dense GEMM"}
+    del pm
+    torch.cuda.empty_cache()
+    return res
+
+
+# ---------------------------------------------------------------- driver
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def launch_ranks(args) -> int:
+    """`--gpus N` without torchrun: re-launch this script as N ranks under
+    torch.distributed.run (NCCL_DEBUG=INFO so each communicator's rank count
+    is logged); fail loudly when the box has fewer than N GPUs."""
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} requested but this box has {have} GPU(s)",
+                          "n_gpus": args.gpus}), flush=True)
+        print(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs, found {have}", file=sys.stderr)
+        return 2
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 def gpu_bench(args) -> None:
     import torch
     import torch.distributed as dist
 
-    import paper_1907_02129_b200 as icv
-    from paper_1907_02129_b200 import _lib
-
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
+    comm = None
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
         dist.init_process_group("nccl", device_id=device)
+        from paper_1907_02129_b200.dist import NcclComm
 
-    from paper_1907_02129_b200.workloads import CONFIGS
-    from paper_1907_02129_b200.dist import broadcast_packed_filter
-
-    name = args.config
-    w0 = CONFIGS[name]
-    per_rank = w0.in_shape.n                      # weak scaling: fixed images per GPU
-    big = w0.with_batch(per_rank * world)
-
-    # host input of this rank's shard (images [rank*per_rank, (rank+1)*per_rank) of the global batch)
-    def bcast(pf):
-        if world > 1:
-            broadcast_packed_filter(pf, src=0)
-
-    import paper_1907_02129_b200.workloads as wl
-    wl.CONFIGS["_bench"] = big
-    w, x, xh, pf, ib, y, tile = setup_problem("_bench", rank * per_rank, (rank + 1) * per_rank, device, bcast,
-                                              mr=args.mr, per_image=args.ib == "per-image")
-    flush = make_l2_flush(device)
-
-    def step():
-        icv.indirect_conv(x, pf, ib, w.params, tile, out=y)
-
+        comm = NcclComm.from_process_group(device)
+        print(f"bench.py rank {rank}: icv NCCL communicator of {comm.size()} ranks on {device}", file=sys.stderr,
+              flush=True)
+    stack_hook, conv_hook = replicator(comm, rank, world, device)
     peaks = load_peaks()
     sampler = ClockSampler(local).start() if rank == 0 else None
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    launches0 = _lib.launch_count()
-    times = time_steps(step, args.steps, args.warmup, flush,
-                       on_timed=(lambda: sampler.mark("t0")) if sampler else None)
-    if sampler:
-        sampler.mark("t1")
-    launches = _lib.launch_count() - launches0 - args.warmup
-    total_ms = sum(times)
-    if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-        dist.barrier()
-    torch.cuda.synchronize()
-
-    # ---- end-to-end through the public API with host buffers ----
-    # The step's input goes host -> device and its output device -> host
-    # every step.  The batch is cut into image chunks, each with its own
-    # (per-image, batch-invariant) indirection buffer bound to its slice of
-    # the persistent input buffer, so chunk i's H2D, chunk i-1's convolution
-    # and chunk i-2's D2H overlap on three streams -- how a caller streaming
-    # batches through indirect_conv would run it.
-    dt = x.dtype
-    x_pinned = torch.from_numpy(xh).to(dt).pin_memory() if dt != torch.uint8 else torch.from_numpy(xh).pin_memory()
-    y_pinned = torch.empty(y.data.numel(), dtype=dt).pin_memory()
-    n_img = x.shape.n
-    n_chunks = max(1, min(args.e2e_chunks, n_img))
-    bounds = [n_img * i // n_chunks for i in range(n_chunks + 1)]
-    in_img = x.shape.h * x.shape.w * x.shape.c
-    out_img = y.shape.h * y.shape.w * y.shape.c
-    chunks = []
-    for i in range(n_chunks):
-        a_, b_ = bounds[i], bounds[i + 1]
-        xs = icv.NhwcTensor(icv.Shape4(b_ - a_, x.shape.h, x.shape.w, x.shape.c), x.data[a_ * in_img:b_ * in_img])
-        ys = icv.NhwcTensor(icv.Shape4(b_ - a_, y.shape.h, y.shape.w, y.shape.c), y.data[a_ * out_img:b_ * out_img])
-        ibs = icv.init_indirection_buffer(xs, ib.zero_row, w.params, ys.shape, tile, per_image=True)
-        chunks.append((a_, b_, xs, ys, ibs))
-    s_h2d, s_cmp, s_d2h = torch.cuda.Stream(device), torch.cuda.Stream(device), torch.cuda.Stream(device)
-    torch.cuda.synchronize()
-
-    def e2e_enqueue():
-        cur = torch.cuda.current_stream(device)
-        start = torch.cuda.Event()
-        start.record(cur)
-        for st_ in (s_h2d, s_cmp, s_d2h):
-            st_.wait_event(start)
-        for a_, b_, xs, ys, ibs in chunks:
-            with torch.cuda.stream(s_h2d):
-                xs.data.copy_(x_pinned[a_ * in_img:b_ * in_img], non_blocking=True)
-                ev_in = torch.cuda.Event()
-                ev_in.record(s_h2d)
-            s_cmp.wait_event(ev_in)
-            with torch.cuda.stream(s_cmp):
-                icv.indirect_conv(xs, pf, ibs, w.params, tile, out=ys)
-                ev_out = torch.cuda.Event()
-                ev_out.record(s_cmp)
-            s_d2h.wait_event(ev_out)
-            with torch.cuda.stream(s_d2h):
-                y_pinned[a_ * out_img:b_ * out_img].copy_(ys.data, non_blocking=True)
-        done = torch.cuda.Event()
-        done.record(s_d2h)
-        cur.wait_event(done)
-
-    # the whole step (3 streams, 3 x chunks copies/launches) is captured once
-    # as a CUDA graph: one launch per step, no per-chunk host overhead
-    e2e_enqueue()
-    torch.cuda.synchronize()
-    graph = torch.cuda.CUDAGraph()
-    cap = torch.cuda.Stream(device)
-    with torch.cuda.stream(cap):
-        graph.capture_begin()
-        e2e_enqueue()
-        graph.capture_end()
-    torch.cuda.synchronize()
-
-    def e2e_step():
-        graph.replay()
-
-    e2e_times = time_steps(e2e_step, max(3, min(args.steps, 50)), max(args.warmup, 3), flush)
-    e2e_total = sum(e2e_times)
-    e2e_n = len(e2e_times)
-    if world > 1:
-        t = torch.tensor([e2e_total], dtype=torch.float64, device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_total = float(t.item())
+    ctx = {"world": world, "rank": rank, "device": device, "peaks": peaks, "flush": make_l2_flush(device),
+           "sampler": sampler, "stack_hook": stack_hook, "conv_hook": conv_hook, "comm": comm}
+    name = args.config
+    head = bench_stack(args, ctx) if name == "cfg5" else bench_conv(args, ctx, name)
     clocks = sampler.stop(("t0", "t1")) if sampler else None
 
-    # correctness gate on the benchmarked output (bench.py:124-142 protocol): sampled pixels vs the oracle
-    gate = None
-    if rank == 0 and not args.no_gate:
-        gate = correctness_gate(w, xh, pf, ib, y)
-
     other = {}
-    if rank == 0 and world == 1 and not args.no_other:
-        for oname in ("cfg1", "cfg3a", "cfg3b", "cfg4"):
-            if oname == name:
-                continue
-            ow_, ox, _, opf, oib_, oy, otile = setup_problem(oname, 0, CONFIGS[oname].in_shape.n, device,
-                                                             mr=args.mr, per_image=args.ib == "per-image")
-            ot = time_steps(lambda: icv.indirect_conv(ox, opf, oib_, ow_.params, otile, out=oy),
-                            max(10, args.steps // 5), 3, flush)
-            oms = statistics.median(ot)
-            other[oname] = {"workload": ow_.name, "dtype": ow_.dtype, "ms_per_step": round(oms, 5),
-                            "value": round(ow_.flops / (oms * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
-                            "kernel": _lib.kernel_name(ow_.params, ow_.in_shape, ox.dtype),
-                            "roofline": roofline_for(ow_, oms, peaks)}
-            del ox, opf, oib_, oy
-        other["cfg5"] = stack_bench(device, peaks, flush)
-        # the paper's comparison: the GEMM-based variant (im2row patch matrix in
-        # HBM + the same tcgen05 GEMM as a 1x1 conv over it) on the headline workload
-        if not w.params.is_pointwise_unit_stride():
-            pm = icv.build_patch_matrix(x, w.params)
-            icv.gemm_only(pm, pf, tile)
-
-            def gemm_step():
-                icv.build_patch_matrix(x, w.params, out=pm)
-                icv.gemm_only(pm, pf, tile)
-
-            gt = time_steps(gemm_step, max(10, args.steps // 5), 3, flush)
-            gms = statistics.median(gt)
-            other["im2col_gemm_" + name] = {
-                "workload": w.name, "dtype": w.dtype, "ms_per_step": round(gms, 5),
-                "value": round(w.flops / (gms * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
-                "kernels": ["icv_im2col", _lib.kernel_name(icv.ConvParams(1, 1, in_channels=pm.cols,
-                                                                            out_channels=pf.k_out),
-                                                          icv.Shape4(1, 1, pm.rows, pm.cols), x.dtype)],
-                "patch_matrix_mb": round(pm.allocated_bytes / 1e6, 2),
-                "indirect_speedup": None,   # filled below from the headline ms
-                "note": "reference im2col.py gemm_conv: patch matrix built every step (build_patch_matrix + gemm_only)"}
-            del pm
-
     cpu = None
+    if rank == 0 and world == 1 and not args.no_other:
+        for oname in CONV_CONFIGS:
+            if oname != name:
+                other[oname] = other_config(oname, ctx, args)
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_reference(name, steps=2, warmup=1)
+        cpu = cpu_stack_baseline() if name == "cfg5" else cpu_conv_baseline(name)
 
+    if world > 1:
+        dist.barrier()
     if rank != 0:
+        if comm is not None:
+            comm.close()
         if world > 1:
             dist.destroy_process_group()
         return
-    flops_total = w0.flops * world * args.steps
+    total_ms = head["total_ms"]
+    # FLOPs are linear in the batch: the whole job's FLOPs per step are the
+    # global batch's (rank shards differ by at most one image)
+    flops_total = head["flops_rank"] / head["batch_rank"] * head["global_batch"] * args.steps
     value = flops_total / (total_ms * 1e-3) / 1e12
-    ms_step = total_ms / args.steps
-    med = statistics.median(times)
-    roof = roofline_for(w0, statistics.mean(times), peaks)
-    for k, v in other.items():
-        if k.startswith("im2col_gemm_"):
-            v["indirect_speedup"] = round(v["ms_per_step"] / med, 3)
-    roof["traffic"] = load_traffic(w0.name)
-    roof["peak_source"] = peaks["which"] + " (MEASURED_PEAKS.json bf16_tflops burst / hbm_gbs)"
+    qs = quantiles(head["times"])
     line = {
-        "metric": "conv TFLOP/s (2*N*Ho*Wo*K*R*S*C / s)",
+        "metric": METRIC,
         "value": round(value, 3),
         "unit": "TFLOP/s",
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": round(ms_step, 6),
-        "ms_per_step_median": round(med, 6),
+        "ms_per_step": round(total_ms / args.steps, 6),
+        "ms_per_step_median": round(qs["median"], 6),
+        "ms_per_step_q20": round(qs["q20"], 6),
+        "ms_per_step_q80": round(qs["q80"], 6),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": args.scaling,
         "vs_baseline": None,
-        "dtype": "bf16" if w0.dtype == "bf16" else w0.dtype,
+        "dtype": "bf16" if name not in ("cfg1", "cfg4") else {"cfg1": "f32", "cfg4": "u8"}[name],
         "data": "synthetic (seeded numpy; BASELINE configs are synthetic)",
-        "config": {"workload": w0.name, "batch_per_gpu": per_rank, "global_batch": per_rank * world,
-                   "H": w0.in_shape.h, "W": w0.in_shape.w, "C": w0.in_shape.c, "K": w0.params.out_channels,
-                   "kernel": f"{w0.params.kernel_h}x{w0.params.kernel_w}", "parallelism": f"dp{world} (batch-sharded)",
-                   "mr": args.mr, "index_dtype": "int64", "ib_layout": args.ib,
+        "config": {"workload": workload_name(name), "global_batch": head["global_batch"],
+                   "batch_per_gpu_rank0": head["batch_rank"], "parallelism": f"dp{world} (batch-sharded, "
+                   f"{'fixed global batch' if args.scaling == 'strong' else 'fixed batch per GPU'})",
+                   "mr": 128, "index_dtype": "int64", "ib_layout": args.ib,
                    "l2": "flushed between steps (256 MiB device write + 256 MiB read, outside the timed events)",
-                   "conv_kernel": _lib.kernel_name(w0.params, w0.in_shape, x.dtype)},
-        "roofline": roof,
-        "e2e": {"value": round(w0.flops * world * e2e_n / (e2e_total * 1e-3) / 1e12, 4), "unit": "TFLOP/s",
-                "h2d_bytes_per_step": int(x.data.numel() * x.data.element_size()),
-                "d2h_bytes_per_step": int(y.data.numel() * y.data.element_size()),
-                "ms_per_step": round(e2e_total / e2e_n, 5),
-                "chunks": n_chunks, "cuda_graph": True,
-                "path": "pinned host input -> device (bound buffer slices), indirect_conv per image chunk, output -> "
-                        "pinned host; H2D / conv / D2H of successive chunks overlap on three streams"},
-        "gpu_launches": int(launches),
+                   "conv_kernel": head.get("conv_kernel")},
+        "roofline": head.get("roofline"),
+        "e2e": head["e2e"],
+        "gpu_launches": int(head["launches"]),
         "clocks": clocks,
         "cpu_baseline": cpu,
-        "gate": gate,
-        "other_configs": other or None,
+        "gate": head.get("gate"),
     }
+    if "stack_roofline" in head:
+        line["stack_roofline"] = head["stack_roofline"]
+        line["per_layer"] = [{k: r[k] for k in ("layer", "kernel", "us", "roofline_us", "frac", "bound")}
+                             for r in head["layers"]]
+    line["other_configs"] = other or None
     print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     if world > 1:
         dist.destroy_process_group()
-
-
-def stack_bench(device, peaks: dict, flush, batch: int = 256, passes: int = 5) -> dict:
-    """cfg5: the 53-layer ResNet-50 conv stack, N=256, chained through the
-    public API (paper_1907_02129_b200/stack.py); median of `passes` passes
-    after 2 warm-up passes, L2 flushed before each (the activations are far
-    larger than L2 anyway).  Per-layer parity is tests/test_gpu_stack.py."""
-    import torch
-
-    from paper_1907_02129_b200.stack import ResNet50Stack
-
-    stack = ResNet50Stack(batch=batch, device=device)
-    for _ in range(2):
-        stack.run()
-    totals, pools, per = [], [], []
-    for _ in range(passes):
-        flush()
-        t, pool, layers = stack.timed_run()
-        totals.append(t)
-        pools.append(pool)
-        per.append(layers)
-    total = statistics.median(totals)
-    conv = sum(statistics.median(p[i] for p in per) for i in range(len(stack.layers)))
-    bf16, hbm = peaks["bf16_tflops"], peaks["hbm_gbs"]
-    roof_ms = sum(max(l.flops / (bf16 * 1e9), l.compulsory_bytes / (hbm * 1e6)) for l in stack.layers)
-    res = {"workload": f"cfg5_resnet50_conv_stack_bf16_n{batch}", "dtype": "bf16", "layers": len(stack.layers),
-           "ms_per_step": round(total, 4), "conv_ms": round(conv, 4), "maxpool_ms": round(statistics.median(pools), 4),
-           "value": round(stack.flops / (total * 1e-3) / 1e12, 2), "unit": "TFLOP/s (end to end, max pool included)",
-           "value_convs_only": round(stack.flops / (conv * 1e-3) / 1e12, 2),
-           "sum_of_layer_rooflines_ms": round(roof_ms, 4), "frac_of_sum_roofline": round(roof_ms / conv, 3),
-           "per_layer": "profiles/r01e_cfg5_layers.json (tools/time_stack.py)"}
-    del stack
-    torch.cuda.empty_cache()
-    return res
-
-
-def correctness_gate(w, xh, pf, ib, y) -> dict:
-    """Sampled output pixels of the benchmarked batch vs the oracle."""
-    from oracle import conv as oconv
-
-    oh, ow = w.out_hw
-    n = y.shape.n
-    pixels = n * oh * ow
-    idx = np.unique(np.random.default_rng(1).integers(0, pixels, 512))
-    xr, wr = oconv.bf16_round(xh), oconv.bf16_round(w.filter_host())
-    ref = oconv.indirect_conv_f32(xr, np.zeros(w.in_shape.c, np.float32), ib.offsets_host(), w.params, wr, None,
-                                  n, oh, ow, pixel_index=idx)
-    got = y.numpy().reshape(pixels, -1)[idx]
-    rel = float(np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-30))
-    ok = rel <= 1e-2
-    if not ok:
-        raise SystemExit(f"correctness gate failed: normwise rel error {rel:.3e} > 1e-2")
-    return {"pixels_checked": int(len(idx)), "normwise_rel_err": rel, "tol": 1e-2, "pass": ok}
-
-
-def reference_arm(args) -> None:
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return
-    from paper_1907_02129_b200.workloads import CONFIGS
-
-    w = CONFIGS[args.config]
-    r = cpu_reference(args.config, steps=args.steps, warmup=args.warmup)
-    line = {
-        "impl": "reference",
-        "metric": "conv TFLOP/s (2*N*Ho*Wo*K*R*S*C / s)",
-        "value": r["value"], "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32 (bf16-rounded operands; reference contract)", "data": "synthetic (seeded numpy)",
-        "config": {"workload": w.name, "batch_per_gpu": w.in_shape.n, "parallelism": "host cores"},
-        "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
-        "e2e": {"value": r["value"], "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
 
 
 def main() -> None:
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["icv", "reference"], default="icv")
-    ap.add_argument("--config", default="cfg2")
-    ap.add_argument("--mr", type=int, default=128)
+    ap.add_argument("--config", default="cfg5", choices=["cfg5", *CONV_CONFIGS])
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                    help="strong: fixed global batch split over the GPUs (SURVEY.md §8(e)); weak: BASELINE batch per GPU")
     ap.add_argument("--ib", choices=["per-image", "canonical"], default="per-image",
                     help="indirection-buffer form the kernels read (DESIGN.md §3)")
     ap.add_argument("--no-other", action="store_true", help="skip the per-config extra measurements")
-    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline legs")
     ap.add_argument("--e2e-chunks", type=int, default=4, help="image chunks pipelined in the e2e leg")
     ap.add_argument("--no-gate", action="store_true")
     args = ap.parse_args()
@@ -618,6 +1030,8 @@ def main() -> None:
         args.warmup = 3
     if args.impl == "reference":
         reference_arm(args)
+    elif "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(launch_ranks(args))
     else:
         gpu_bench(args)
 

@@ -220,6 +220,43 @@ ICV_API int icv_maxpool2d(const icv_shape4* in, int32_t kh, int32_t kw, int32_t 
 ICV_API int icv_im2col(const icv_conv_desc* desc, const icv_shape4* in, int64_t batch, int32_t dtype, const void* x,
                        const void* zero_row, void* patches, void* stream);
 
+/* ---- direct convolution: the harness's correctness oracle ----------------
+ * Float32 output of the direct convolution of `x` (ICV_F32 / ICV_BF16 NHWC,
+ * first `batch` images) with the KRSC filter `w` (ICV_F32 / ICV_BF16) plus
+ * `bias` (float32, NULL = none): bias init, then ky, kx, c ascending with a
+ * rounded multiply and a rounded add per tap, padding taps skipped -- the
+ * reference's convbench.reference.direct_conv (reference.py:30-84),
+ * bit-exact with it for float32.  No indirection buffer involved. */
+ICV_API int icv_direct_conv(const icv_conv_desc* desc, const icv_shape4* in, int64_t batch, int32_t x_dtype,
+                            const void* x, int32_t w_dtype, const void* w, const float* bias, float* y,
+                            void* stream);
+
+/* ---- filter replication for the batch-sharded operator --
+ * The convolution shards by image (reference indirect.py:112-125: an
+ * image's buffer entries, sums and outputs depend only on that image and
+ * the replicated filter), so a data-parallel deployment has exactly one
+ * collective: broadcasting the packed filter (icv_pack_filter's bytes) from
+ * the source rank once per model load.  NCCL is loaded at run time
+ * (libnccl.so.2); without it these return ICV_ERR_UNSUPPORTED.  `comm` is an
+ * opaque ncclComm_t.  The reference has no multi-device path (SURVEY.md
+ * §2.3); these replace nothing in it. */
+#define ICV_NCCL_UNIQUE_ID_BYTES 128
+ICV_API int icv_nccl_version(int32_t* version);
+/* Rank 0 creates the id (ICV_NCCL_UNIQUE_ID_BYTES bytes) and ships it to the
+ * other ranks out of band (torch.distributed's store in dist.py). */
+ICV_API int icv_nccl_unique_id(void* id_out);
+/* One process per GPU: each rank, its device current, joins the communicator. */
+ICV_API int icv_nccl_init_rank(void** comm, int32_t nranks, const void* unique_id, int32_t rank);
+/* One process driving `ndev` local GPUs (devices NULL = 0..ndev-1): one
+ * communicator per device into comms[0..ndev). */
+ICV_API int icv_nccl_init_all(void** comms, int32_t ndev, const int32_t* devices);
+ICV_API int icv_nccl_comm_size(void* comm, int32_t* nranks);
+/* Broadcast `bytes` from `root`'s sendbuf (NULL = in place in recvbuf) into
+ * every rank's recvbuf, stream-ordered on `stream`. */
+ICV_API int icv_nccl_broadcast(const void* sendbuf, void* recvbuf, int64_t bytes, int32_t root, void* comm,
+                               void* stream);
+ICV_API int icv_nccl_destroy(void* comm);
+
 #ifdef __cplusplus
 }
 #endif

@@ -8,6 +8,7 @@ compute in hand-written sm_100a kernels behind the C ABI of ``libicv.so``
 for allocation, streams and torch.distributed only.
 """
 
+from .dist import NcclComm, ShardedIndirectConv, broadcast_packed_filter, replicate_filter, shard_range
 from .errors import InvalidGeometryError, NativeLibraryError, StaleBufferError, UnsupportedError
 from .gemm import PackedFilter, QuantParams, TileConfig, pack_filter
 from .ib_cache import CacheStats, IndirectionCache
@@ -36,6 +37,7 @@ from .tensors import (
 __version__ = "0.1.0"
 
 __all__ = [
+    "NcclComm", "ShardedIndirectConv", "broadcast_packed_filter", "replicate_filter", "shard_range",
     "ZERO_REF", "CacheStats", "ConvParams", "FilterTensor", "IndirectionCache", "PatchMatrix", "build_patch_matrix", "gemm_conv", "gemm_only", "IndirectionBuffer", "InvalidGeometryError",
     "NativeLibraryError", "NhwcTensor", "PackedFilter", "QuantParams", "Shape4", "StaleBufferError",
     "TileConfig", "UnsupportedError", "conv_output_shape", "filter_fill_random", "indirect_conv",

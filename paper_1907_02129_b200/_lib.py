@@ -69,6 +69,15 @@ SIGNATURES = {
     "icv_conv_kernel_name": (ctypes.c_int, [ctypes.POINTER(Desc), ctypes.POINTER(Shape), _I32, _I32,
                                             ctypes.POINTER(ctypes.c_char_p)]),
     "icv_set_tuning": (ctypes.c_int, [ctypes.c_char_p, _I32]),
+    "icv_direct_conv": (ctypes.c_int, [ctypes.POINTER(Desc), ctypes.POINTER(Shape), _I64, _I32, _P, _I32, _P, _P,
+                                        _P, _P]),
+    "icv_nccl_version": (ctypes.c_int, [ctypes.POINTER(_I32)]),
+    "icv_nccl_unique_id": (ctypes.c_int, [_P]),
+    "icv_nccl_init_rank": (ctypes.c_int, [ctypes.POINTER(_P), _I32, _P, _I32]),
+    "icv_nccl_init_all": (ctypes.c_int, [ctypes.POINTER(_P), _I32, ctypes.POINTER(_I32)]),
+    "icv_nccl_comm_size": (ctypes.c_int, [_P, ctypes.POINTER(_I32)]),
+    "icv_nccl_broadcast": (ctypes.c_int, [_P, _P, _I64, _I32, _P, _P]),
+    "icv_nccl_destroy": (ctypes.c_int, [_P]),
     "icv_get_tuning": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(_I32)]),
     "icv_launch_count": (_I64, []),
     "icv_maxpool2d": (ctypes.c_int, [ctypes.POINTER(Shape), _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P, _P, _P]),

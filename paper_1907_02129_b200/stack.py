@@ -72,15 +72,42 @@ class StackLayer:
         return 2 * (self.input.shape.numel + p.out_channels * p.kernel_elems * p.in_channels + self.output.shape.numel)
 
 
-class ResNet50Stack:
-    """All 53 layers with persistent activations, packed filters and IBs."""
+IMAGE_ELEMS = 224 * 224 * 3
 
-    def __init__(self, batch: int = 256, device="cuda", mr: int = 128, per_image: bool = True):
+
+def stack_input_host(lo: int, hi: int) -> np.ndarray:
+    """Images [lo, hi) of the network input: the N(0, 1) float32 stream of
+    seed 0, image i = elements [i*224*224*3, (i+1)*224*224*3) (so a shard
+    holds exactly its slice of the global batch)."""
+    x = np.random.default_rng(0).standard_normal(hi * IMAGE_ELEMS, dtype=np.float32)
+    return x[lo * IMAGE_ELEMS:]
+
+
+def stack_weights_host(index: int, params: ConvParams) -> np.ndarray:
+    """He-normal KRSC weights of layer ``index`` (seed index + 1), float32."""
+    kk = params.kernel_elems * params.in_channels
+    wrng = np.random.default_rng(index + 1)
+    return wrng.standard_normal(params.out_channels * kk, dtype=np.float32) * np.float32(np.sqrt(2.0 / kk))
+
+
+class ResNet50Stack:
+    """All 53 layers with persistent activations, packed filters and IBs.
+
+    ``images=(lo, hi)`` builds the stack for that slice of the global batch
+    (one data-parallel rank's shard); ``replicate``, when
+    given, is called with every packed filter right after packing (the
+    data-parallel runner broadcasts rank 0's bytes to the other ranks there).
+    """
+
+    def __init__(self, batch: int = 256, device="cuda", mr: int = 128, per_image: bool = True,
+                 images: tuple[int, int] | None = None, replicate=None):
         self.device = torch.device(device)
         self.tile = TileConfig(mr=mr)
+        lo, hi = images if images is not None else (0, batch)
+        batch = hi - lo
+        self.images = (lo, hi)
         specs = resnet50_layers(batch)
-        rng = np.random.default_rng(0)
-        x0 = rng.standard_normal(batch * 224 * 224 * 3, dtype=np.float32)
+        x0 = stack_input_host(lo, hi)
         self.input = NhwcTensor(Shape4(batch, 224, 224, 3), torch.from_numpy(x0).to(self.device).to(torch.bfloat16))
         self.layers: list[StackLayer] = []
         self.pool_out: NhwcTensor | None = None
@@ -102,12 +129,12 @@ class ResNet50Stack:
                 src = block_in
             assert src.shape == shape, (name, src.shape, shape)
             out = NhwcTensor.empty(conv_output_shape(params, shape), dtype=torch.bfloat16, device=self.device)
-            wrng = np.random.default_rng(idx + 1)
-            kk = params.kernel_elems * params.in_channels
-            w = (wrng.standard_normal(params.out_channels * kk, dtype=np.float32) * np.sqrt(2.0 / kk))
+            w = stack_weights_host(idx, params)
             w_dev = torch.from_numpy(w).to(self.device).to(torch.bfloat16)
             filt = FilterTensor(params.out_channels, params.kernel_h, params.kernel_w, params.in_channels, w_dev)
             pf = pack_filter(filt, None, params, self.tile, compute_dtype=torch.bfloat16)
+            if replicate is not None:
+                replicate(pf)
             c = params.in_channels
             if c not in zero_rows:
                 zero_rows[c] = make_zero_row(c, dtype=torch.bfloat16, device=self.device)
