@@ -113,15 +113,25 @@ def gemm_only(prebuilt: PatchMatrix, pf: PackedFilter, tile: TileConfig) -> torc
     if prebuilt.cols != pf.reduction_len:
         raise ValueError("patch matrix columns do not match packed filter")             # :144-145
     view = _gemm_view(pf, tile)
-    key = (prebuilt.matrix.data_ptr(), tile.mr, tile.nr)
-    cached = prebuilt._gemm.get("ib")
+    m = prebuilt.matrix
+    key = (m.data_ptr(), prebuilt.rows, prebuilt.cols, m.dtype, m.device, tile.mr, tile.nr)
+    # the buffer of the 1 x P view is built once per patch-matrix location;
+    # a pointwise layer's "patch matrix" is a fresh view of the input each
+    # call, so its buffer is cached on the packed filter, keyed by location
+    store = prebuilt._gemm if not prebuilt.is_view else pf.__dict__.setdefault("_gemm_ib_cache", {})
+    cached = store.get("ib") if not prebuilt.is_view else store.get(key)
     if cached is None or cached[0] != key:
-        x1 = NhwcTensor(Shape4(1, 1, prebuilt.rows, prebuilt.cols), prebuilt.matrix.view(-1))
+        x1 = NhwcTensor(Shape4(1, 1, prebuilt.rows, prebuilt.cols), m.view(-1))
         fill = pf.quant.input_zero_point if pf.quant is not None else 0
-        zero = make_zero_row(prebuilt.cols, dtype=prebuilt.matrix.dtype, device=prebuilt.matrix.device, fill=fill)
+        zero = make_zero_row(prebuilt.cols, dtype=m.dtype, device=m.device, fill=fill)
         ib = init_indirection_buffer(x1, zero, view.params, conv_output_shape(view.params, x1.shape), tile)
         cached = (key, x1, ib)
-        prebuilt._gemm["ib"] = cached
+        if prebuilt.is_view:
+            if len(store) >= 8:
+                store.clear()
+            store[key] = cached
+        else:
+            store["ib"] = cached
     _, x1, ib = cached
     y = indirect_conv(x1, view, ib, view.params, tile)
     return y.data.view(prebuilt.rows, pf.k_out)
