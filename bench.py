@@ -688,7 +688,11 @@ def bench_stack(args, ctx) -> dict:
     lo, hi = shard_range(gbatch, world, rank)
     stack = ResNet50Stack(device=device, images=(lo, hi), replicate=ctx["stack_hook"])
     flush = ctx["flush"]
-    res = run_timed(args, ctx, stack.run, flush)
+    # the device-timed step replays the pass as one CUDA graph (the e2e leg
+    # below issues every indirect_conv call from Python instead)
+    step = stack.run if args.no_graph else stack.graphed()
+    res = run_timed(args, ctx, step, flush, None if args.no_graph else stack.graph_launches)
+    res["cuda_graph"] = not args.no_graph
     res.update({"flops_rank": stack.flops, "global_batch": gbatch, "batch_rank": hi - lo})
     if rank == 0:
         rows = stack_layer_table(stack, ctx["peaks"])
@@ -715,9 +719,11 @@ def bench_stack(args, ctx) -> dict:
     return res
 
 
-def run_timed(args, ctx, fn, flush) -> dict:
+def run_timed(args, ctx, fn, flush, launches_per_replay: int | None = None) -> dict:
     """K timed steps after W warm-ups, barrier + synchronize on both sides;
-    the per-rank total is max-reduced over ranks."""
+    the per-rank total is max-reduced over ranks.  `launches_per_replay`:
+    fn replays a CUDA graph holding that many libicv kernels (the host-side
+    launch counter does not see replays)."""
     import torch
     import torch.distributed as dist
 
@@ -738,6 +744,8 @@ def run_timed(args, ctx, fn, flush) -> dict:
     if sampler:
         sampler.mark("t1")
     launches = _lib.launch_count() - l0
+    if launches_per_replay is not None:
+        launches += launches_per_replay * args.steps
     total = sum(times)
     if world > 1:
         t = torch.tensor([total], dtype=torch.float64, device=ctx["device"])
@@ -990,7 +998,8 @@ def gpu_bench(args) -> None:
                    f"{'fixed global batch' if args.scaling == 'strong' else 'fixed batch per GPU'})",
                    "mr": 128, "index_dtype": "int64", "ib_layout": args.ib,
                    "l2": "flushed between steps (256 MiB device write + 256 MiB read, outside the timed events)",
-                   "conv_kernel": head.get("conv_kernel")},
+                   "conv_kernel": head.get("conv_kernel"), "cuda_graph": head.get("cuda_graph", False),
+                   "pdl": True},
         "roofline": head.get("roofline"),
         "e2e": head["e2e"],
         "gpu_launches": int(head["launches"]),
@@ -1025,6 +1034,7 @@ def main() -> None:
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline legs")
     ap.add_argument("--e2e-chunks", type=int, default=4, help="image chunks pipelined in the e2e leg")
     ap.add_argument("--no-gate", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="cfg5: issue the timed passes from Python, no CUDA graph")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

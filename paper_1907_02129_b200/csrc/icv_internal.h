@@ -43,6 +43,8 @@ enum TuneKey {
   kTuneTmaStore,         // 1: TMA tile stores in the epilogue, 0: thread stores
   kTuneRowsRp,           // row kernel: output rows per tile (1, or 2 = opt-in)
   kTuneDenseA,           // 1: 1x1 stride-1 layers load A as dense TMA boxes, 0: IB gathers
+  kTuneDenseCs,          // dense A: 2 = CTA pairs (M = 256), 1 = single CTAs
+  kTunePdl,              // 1: persistent conv kernels use programmatic dependent launch
   kTuneCount
 };
 int tune(TuneKey k);
@@ -53,6 +55,40 @@ int tune(TuneKey k);
 // co-resident (written to *max_clusters; 0 otherwise).  Function attributes
 // are per device, so a process driving several GPUs sets them on each.
 int kernel_setup(const void* fn, int smem_bytes, int cluster, int threads, int* max_clusters);
+
+// Launch a persistent conv kernel: thread-block clusters of `cluster` CTAs
+// (1 = none) and, unless knob pdl = 0, programmatic dependent launch -- the
+// kernel may start while the previous kernel in the stream drains (its
+// setup overlaps that kernel's tail; it calls griddep_wait() before touching
+// any tensor a previous kernel may write).
+template <typename... KArgs, typename... Args>
+int launch_conv_kernel(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                       int cluster, const char* what, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[2];
+  int n = 0;
+  if (cluster > 1) {
+    at[n].id = cudaLaunchAttributeClusterDimension;
+    at[n].val.clusterDim.x = cluster;
+    at[n].val.clusterDim.y = 1;
+    at[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  if (tune(kTunePdl)) {
+    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = at;
+  cfg.numAttrs = n;
+  if (cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, args...); e != cudaSuccess) return cuda_check(e, what);
+  note_launch();
+  return cuda_check(cudaGetLastError(), what);
+}
 
 // ---- geometry --------------------------------------------------------------
 struct Geom {

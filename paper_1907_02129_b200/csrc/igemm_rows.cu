@@ -213,6 +213,8 @@ __global__ void __launch_bounds__(kThreadsR, 1) igemm_rows_kernel(const __grid_c
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  griddep_wait();   // (setup read only constants; tensors may belong to the previous kernel)
+  griddep_launch_dependents();
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) RT(1);
 
@@ -448,9 +450,7 @@ int launch_rows_ring(const ConvArgs& c, cudaStream_t st, const RowsPlan& pl, int
   a.t.use_tma_y = tune(kTuneTmaStore) != 0;
   const int sms = sm_count();
   const int grid = (int)(a.total_tiles < sms ? a.total_tiles : sms);
-  kernel<<<grid, kThreadsR, pl.bytes, st>>>(tmap_y, a, pl);
-  note_launch();
-  return cuda_check(cudaGetLastError(), "igemm_rows launch");
+  return launch_conv_kernel(kernel, (unsigned)grid, kThreadsR, pl.bytes, st, 1, "igemm_rows launch", tmap_y, a, pl);
 }
 
 // The deeper ring (converters up to kAccR - 1 tiles ahead of the MMA: cfg3a

@@ -233,6 +233,8 @@ __global__ void __launch_bounds__(kThreadsStem, 1) igemm_stem_kernel(const __gri
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  griddep_wait();   // (setup read only constants; tensors may belong to the previous kernel)
+  griddep_launch_dependents();
   const uint32_t tmem_base = *tmem_slot;
   const uint32_t sA_u32 = smem_u32(sA);
   const uint32_t sB_u32 = smem_u32(sB);
@@ -551,9 +553,8 @@ int launch_stem_t(const ConvArgs& c, cudaStream_t st) {
   CUtensorMap tmap_y;
   a.use_tma_y = make_output_tmap(c, &tmap_y) == ICV_OK;
   if (!a.use_tma_y) tmap_y = tmap;   // unused placeholder
-  kernel<<<grid, kThreadsStem, Cf::kSmemBytes, st>>>(tmap, tmap_y, a, (int32_t)x_elems, tiles);
-  note_launch();
-  return cuda_check(cudaGetLastError(), "igemm_stem launch");
+  return launch_conv_kernel(kernel, (unsigned)grid, kThreadsStem, Cf::kSmemBytes, st, 1, "igemm_stem launch", tmap,
+                            tmap_y, a, (int32_t)x_elems, tiles);
 }
 
 template <typename IbT>

@@ -153,7 +153,6 @@ __global__ void __launch_bounds__(kThreadsS<kI8, kEpiW>, 1) igemm_smem_kernel(co
   // the filter bytes of the single-CTA kernel.
   using C = CfgS<kI8, BN, kCS, kEpiW, kIsDense<IbT>>;
   static_assert(kCS == 1 || kCS == 2, "single CTA or CTA pair");
-  static_assert(!kIsDense<IbT> || kCS == 1, "dense A: single CTAs");
   constexpr uint16_t kMask = (uint16_t)((1u << kCS) - 1);
   const ClusterTiles<kCS> sched{a.total_tiles / a.n_tiles, a.n_tiles};
   const uint32_t crank = kCS > 1 ? cluster_ctarank() : 0;
@@ -192,7 +191,9 @@ __global__ void __launch_bounds__(kThreadsS<kI8, kEpiW>, 1) igemm_smem_kernel(co
     for (int s = 0; s < kStages; ++s) {
       // TMA path: 1 expect_tx arrival; cp.async path: 128 producer arrivals + 1
       // cp.async path: 128 producer arrivals + 1 expect_tx (+ 1 forwarded from the peer, pair leader)
-      mbar_init(&full[s], dense_a ? 1 : 32 * kProdWarpsS<kI8> + 1 + (kCS == 2 && crank == 0 ? 1 : 0));
+      // dense A: the issuing thread's expect_tx arrival; gather: 32 per producer
+      // warp + 1 expect_tx; a pair leader also counts the peer's forwarded arrival
+      mbar_init(&full[s], (dense_a ? 1 : 32 * kProdWarpsS<kI8> + 1) + (kCS == 2 && crank == 0 ? 1 : 0));
       mbar_init(&empty[s], 1);       // tcgen05.commit (multicast to both CTAs of a pair)
     }
     for (int s = 0; s < 2; ++s) {
@@ -220,6 +221,10 @@ __global__ void __launch_bounds__(kThreadsS<kI8, kEpiW>, 1) igemm_smem_kernel(co
   if constexpr (kCS > 1) cluster_sync_all();   // peers' barriers initialised before any remote arrival
   else __syncthreads();
   tc_fence_after();
+  // setup above read only constants (bias, zero row); the input activation
+  // and the output may belong to the previous kernel in the stream
+  griddep_wait();
+  griddep_launch_dependents();
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) TRACE(1);
   const int num_kb = a.RS * a.cblocks;
@@ -265,22 +270,29 @@ __global__ void __launch_bounds__(kThreadsS<kI8, kEpiW>, 1) igemm_smem_kernel(co
       const int32_t* rbase = sRowBase + (k & 1) * kBM;
       const int nt = (int)(tile % a.n_tiles);
       if constexpr (dense_a) {
-        // one thread issues, per stage, the kKB A boxes and the filter box
-        // under one expect_tx: no thread-side arrivals
-        if (threadIdx.x == 0) {
-          const int64_t mt = tile / a.n_tiles;
-          for (int kb = 0; kb < num_kb; ++kb) {
-            const int j = kb % C::kKB;
-            if (j == 0) {
-              mbar_wait(&empty[stage], phase ^ 1);
-              mbar_arrive_expect_tx(&full[stage], min(C::kKB, num_kb - kb) * kABytes + C::kKB * C::kBBytes);
-              tma_load_3d(sB_u32 + stage * C::kKB * C::kBBytes, &tmap_b, &full[stage], 0, nt * BN, kb);
-            }
-            tma_load_2d(sA_u32 + (stage * C::kKB + j) * kABytes, &tmap_x, &full[stage], kb * a.cblock_elems,
-                        (int32_t)(mt * kBM));
-            if (j == C::kKB - 1 || kb == num_kb - 1) {
-              if (++stage == kStages) { stage = 0; phase ^= 1; }
-            }
+        // Stage q of the CTA's K-block sequence (kKB = 1: one A box + one
+        // filter box under one expect_tx, no thread-side arrivals) is issued
+        // by lane 0 of producer warp q % kPW: a thread's TMA loads issue one
+        // after another at ~450 cycles each whatever their size
+        // (tools/micro/tma_rate.cu), so one issuer would cap the ring at
+        // ~50 B/cycle; kPW issuers keep several stages in flight.
+        // At most kStages issuers: an issuer's previous stage, q - niss,
+        // waited for the consumption of q - niss - kStages, so with
+        // niss <= kStages the empty barrier of stage q is at most one phase
+        // behind and its parity wait is unambiguous.
+        static_assert(C::kKB == 1, "dense A: one K block per stage");
+        const int niss = kStages < kPW ? kStages : kPW;
+        const int64_t mt = tile / a.n_tiles;
+        const int64_t q0 = k * num_kb;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          const int64_t q = q0 + kb;
+          if (lane == 0 && (int)(q % niss) == warp) {
+            const int st = (int)(q % kStages);
+            mbar_wait(&empty[st], (uint32_t)((q / kStages) & 1) ^ 1u);
+            mbar_arrive_expect_tx(&full[st], kABytes + C::kBBytes);
+            // (a pair member loads its half of the BN filter rows)
+            tma_load_3d(sB_u32 + st * C::kBBytes, &tmap_b, &full[st], 0, nt * BN + (int)crank * (BN / kCS), kb);
+            tma_load_2d(sA_u32 + st * kABytes, &tmap_x, &full[st], kb * a.cblock_elems, (int32_t)(mt * kBM));
           }
         }
       } else {
@@ -367,11 +379,13 @@ __global__ void __launch_bounds__(kThreadsS<kI8, kEpiW>, 1) igemm_smem_kernel(co
         else gather_tile(std::integral_constant<int, 0>{});
       }
       if (threadIdx.x == 0 && k < 8) TRACE(40 + k);   // producer: all of tile k's loads issued
-      // slice k+1 landed (its group was committed before this tile's gathers)
-      // and every producer is done reading slice k
-      cp_async_wait_committed();
-      if (threadIdx.x == 0 && k < 8) TRACE(48 + k);   // producer: next slice landed
-      named_bar_sync(1, 32 * kProdWarpsS<kI8>);
+      if constexpr (!dense_a) {
+        // slice k+1 landed (its group was committed before this tile's gathers)
+        // and every producer is done reading slice k
+        cp_async_wait_committed();
+        if (threadIdx.x == 0 && k < 8) TRACE(48 + k);   // producer: next slice landed
+        named_bar_sync(1, 32 * kProdWarpsS<kI8>);
+      }
     }
 #ifdef ICV_TRACE
     if (threadIdx.x == 0) {
@@ -508,7 +522,7 @@ int launch_smem_cs(const ConvArgs& c, cudaStream_t st) {
   // dense A: 1x1 stride-1 layers with a canonical buffer (and the GEMM
   // baseline's patch matrix) load the A tile as TMA boxes of consecutive rows
   a.use_tma_x = 0;
-  if constexpr (kIsDense<IbT>) {
+  if constexpr (kIsDense<IbT>) {   // (single CTAs and pairs alike: each CTA loads its own 128 rows)
     if (int s = make_input_tmap(c, &tmap_x)) return fail(s, "dense-A input tensor map");
     a.use_tma_x = 1;
   } else {
@@ -518,31 +532,18 @@ int launch_smem_cs(const ConvArgs& c, cudaStream_t st) {
   a.use_tma_y = make_output_tmap(c, &tmap_y) == ICV_OK;
   if (!a.use_tma_y) tmap_y = tmap;   // unused placeholder
   const int sms = sm_count();
+  int64_t grid;
   if constexpr (kCS == 1) {
-    const int grid = (int)(a.total_tiles < sms ? a.total_tiles : sms);
-    kernel<<<grid, kThreadsS<kI8, kEpiW>, pl.bytes, st>>>(tmap, tmap_x, tmap_y, a, pl);
+    grid = a.total_tiles < sms ? a.total_tiles : sms;
   } else {
     const int64_t groups = (a.total_tiles / a.n_tiles + kCS - 1) / kCS * a.n_tiles;
     int64_t clusters = sms / kCS;
     if (max_clusters > 0 && clusters > max_clusters) clusters = max_clusters;
     if (clusters > groups) clusters = groups;
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = kCS;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.gridDim = dim3((unsigned)(clusters * kCS));
-    cfg.blockDim = dim3(kThreadsS<kI8, kEpiW>);
-    cfg.dynamicSmemBytes = pl.bytes;
-    cfg.stream = st;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    if (cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, tmap, tmap_x, tmap_y, a, pl); e != cudaSuccess)
-      return cuda_check(e, "igemm_smem cluster launch");
+    grid = clusters * kCS;
   }
-  note_launch();
-  return cuda_check(cudaGetLastError(), "igemm_smem launch");
+  return launch_conv_kernel(kernel, (unsigned)grid, kThreadsS<kI8, kEpiW>, pl.bytes, st, kCS, "igemm_smem launch", tmap,
+                            tmap_x, tmap_y, a, pl);
 }
 
 // CTA pairs (cta_group::2, M = 256): tuning knob "cluster" = 2 (see the kernel).
@@ -553,7 +554,16 @@ int launch_smem(const ConvArgs& c, cudaStream_t st) {
   if (use_clusters()) return launch_smem_cs<kI8, BN, IbT, 2, kEpiWarpsS<kI8>>(c, st);
   if (tune(kTuneDenseA) && dense_a_eligible(c)) {
     PlanS pl;
-    if (!kI8 && (int64_t)c.g.K >= 4 * (int64_t)c.g.C && plan_smem<kI8, BN, DenseA, 1, 8>(1, c.L.n_pad, &pl))
+    const bool wide_out = !kI8 && (int64_t)c.g.K >= 4 * (int64_t)c.g.C;
+    if (tune(kTuneDenseCs) == 2) {
+      // CTA pairs (M = 256): each SM streams its own A rows and half of the
+      // filter block, so the L2 -> SM bytes per MMA drop by a third at BN 256
+      if (wide_out && plan_smem<kI8, BN, DenseA, 2, 8>(1, c.L.n_pad, &pl))
+        return launch_smem_cs<kI8, BN, DenseA, 2, 8>(c, st);
+      if (plan_smem<kI8, BN, DenseA, 2, kEpiWarpsS<kI8>>(1, c.L.n_pad, &pl))
+        return launch_smem_cs<kI8, BN, DenseA, 2, kEpiWarpsS<kI8>>(c, st);
+    }
+    if (wide_out && plan_smem<kI8, BN, DenseA, 1, 8>(1, c.L.n_pad, &pl))
       return launch_smem_cs<kI8, BN, DenseA, 1, 8>(c, st);
     if (plan_smem<kI8, BN, DenseA, 1, kEpiWarpsS<kI8>>(1, c.L.n_pad, &pl))
       return launch_smem_cs<kI8, BN, DenseA, 1, kEpiWarpsS<kI8>>(c, st);
@@ -749,8 +759,10 @@ int launch_conv_tc(const ConvArgs& c, cudaStream_t st) {
 const char* tc_kernel_name(const ConvArgs& c) {
   const bool i8 = c.L.family == kFamTcU8;
   if (win_kernel_eligible(c)) return i8 ? "icv_igemm_win<u8>" : "icv_igemm_win<bf16>";
-  if (dense_a_eligible(c) && tune(kTuneDenseA) && !use_clusters())
+  if (dense_a_eligible(c) && tune(kTuneDenseA) && !use_clusters()) {
+    if (tune(kTuneDenseCs) == 2) return i8 ? "icv_igemm_smem<u8,dense,pair>" : "icv_igemm_smem<bf16,dense,pair>";
     return i8 ? "icv_igemm_smem<u8,dense>" : "icv_igemm_smem<bf16,dense>";
+  }
   return i8 ? "icv_igemm_smem<u8>" : "icv_igemm_smem<bf16>";
 }
 

@@ -394,6 +394,8 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
   if constexpr (kCS > 1) cluster_sync_all();   // the peer's barriers exist before any remote signal
   else __syncthreads();
   tc_fence_after();
+  griddep_wait();   // (setup read only constants; tensors may belong to the previous kernel)
+  griddep_launch_dependents();
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) TRACE(1);
   const int cblocks = a.t.cblocks;
@@ -422,12 +424,21 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
     // (nor the reverse).  cp.async windows: all producer threads gather,
     // thread 0 loads the filter.  (An idle thread must not trail the barrier
     // phases it waits on, hence the exits.)
+    // TMA windows: the producer warps past the window issuers all load filter
+    // blocks, taking the stage's taps round-robin (each filter block is one
+    // TMA load of BN / kCS rows, so at ~450 cycles per load one thread would
+    // cap a stage at RS loads * 450 cycles).
     const bool win_thread = !tma_win || (lane == 0 && warp < a.win_split);
-    const bool filt_thread = tma_win ? (lane == 0 && warp == kProdWarpsW - 1) : threadIdx.x == 0;
+    // (at most bslots filter threads, so each ring slot's parity wait is
+    // never more than one phase ahead: see the dense-A producer, igemm_tc.cu)
+    const int nfilt = tma_win ? min(kProdWarpsW - a.win_split, pl.bslots) : 1;
+    const int fidx = tma_win ? warp - a.win_split : 0;
+    const bool filt_thread = tma_win ? (lane == 0 && warp >= a.win_split && fidx < nfilt) : threadIdx.x == 0;
     if (!win_thread && !filt_thread) goto done;
     {
-      int ws = 0, bs = 0;
-      uint32_t wph = 0, bph = 0;
+      int ws = 0;
+      uint32_t wph = 0;
+      int64_t fq = 0;   // filter blocks issued so far by all filter threads (ring sequence)
       int uk = 0;
       for (int32_t u = cid; u < a.units; u += ncl, ++uk) {
         if (threadIdx.x == 0 && uk < 8) TRACE(26 + uk);
@@ -502,18 +513,19 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
           if (filt_thread && pl.resident) {
             if (uk == 0)
               for (int i = kS2 ? sPh[pi] : 0; i < (kS2 ? sPh[pi + 1] : RS); ++i)
-                load_filter_slot(cb * RS + (kS2 ? sTapE[i] : i));
+                if (i % nfilt == fidx) load_filter_slot(cb * RS + (kS2 ? sTapE[i] : i));
           } else if (filt_thread) {
-            for (int i = kS2 ? sPh[pi] : 0; i < (kS2 ? sPh[pi + 1] : RS); ++i) {
+            for (int i = kS2 ? sPh[pi] : 0; i < (kS2 ? sPh[pi + 1] : RS); ++i, ++fq) {
+              if ((int)(fq % nfilt) != fidx) continue;
               const int e = kS2 ? sTapE[i] : i;
-              mbar_wait(&bempty[bs], bph ^ 1);
+              const int bs = (int)(fq % pl.bslots);
+              mbar_wait(&bempty[bs], (uint32_t)((fq / pl.bslots) & 1) ^ 1u);
               if (crank == 0) mbar_arrive_expect_tx(&bfull[bs], kCS * C::kBBytes);
               if constexpr (kCS == 2)
                 tma_load_3d_cg2(sB_u32 + bs * C::kBBytes, &tmap_b, mapa_rank(smem_u32(&bfull[bs]), 0), 0,
                                 nt * BN + (int)crank * (BN / kCS), e * cblocks + cb);
               else
                 tma_load_3d(sB_u32 + bs * C::kBBytes, &tmap_b, &bfull[bs], 0, nt * BN, e * cblocks + cb);
-              if (++bs == pl.bslots) { bs = 0; bph ^= 1; }
             }
           }
         }
@@ -1042,7 +1054,7 @@ int slot_bytes(const WinGeom& w, int kmt, int kcs) {
 template <bool kI8, int BN, int kMT, int kCS, bool kS2>
 bool win_plan_for(const ConvArgs& c, const WinGeom& w, PlanW* pl, bool resident = false) {
   if (kMT == 2 && w.WR2 == 0) return false;
-  if (resident && (kMT != 1 || c.L.n_pad != BN)) return false;
+  if (resident && c.L.n_pad != BN) return false;
   return plan_win<kI8, BN, kMT, kCS, kS2>(slot_bytes(w, kMT, kCS), c.g.RS(), c.g.RS() * c.L.cblocks, c.L.n_pad, resident,
                                      pl);
 }
@@ -1136,26 +1148,8 @@ int launch_win(const ConvArgs& c, const WinGeom& w, cudaStream_t st, bool reside
                     "Wp %d Hz %d WR %d WR2 %d tiles %d units %d (two %d) clusters %lld split %d\n",
             BN, kMT, kCS, (int)kS2, pl.resident, pl.wstages, pl.bslots, pl.win_stage, pl.bytes, w.Wp, w.Hz, w.WR, w.WR2,
             w.tiles, a.units, a.two_units, (long long)clusters, a.win_split);
-  if constexpr (kCS == 1) {
-    kernel<<<(unsigned)clusters, kThreadsW, pl.bytes, st>>>(tmap_b, maps, a, pl);
-  } else {
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = kCS;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.gridDim = dim3((unsigned)(clusters * kCS));
-    cfg.blockDim = dim3(kThreadsW);
-    cfg.dynamicSmemBytes = pl.bytes;
-    cfg.stream = st;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    if (cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, tmap_b, maps, a, pl); e != cudaSuccess)
-      return cuda_check(e, "igemm_win pair launch");
-  }
-  note_launch();
-  return cuda_check(cudaGetLastError(), "igemm_win launch");
+  return launch_conv_kernel(kernel, (unsigned)(clusters * kCS), kThreadsW, pl.bytes, st, kCS, "igemm_win launch", tmap_b,
+                            maps, a, pl);
 }
 
 
@@ -1177,6 +1171,11 @@ int dispatch_bn(const ConvArgs& c, const WinGeom& w, cudaStream_t st, bool launc
   // two tiles share each filter block and one window of WR2 rows), pair
   // with a resident filter, pair, then the single-CTA kernels
   if constexpr (mt_fits<kI8, BN, 2>()) {
+    // two-tile units with the filter resident (one N tile whose blocks fit
+    // beside the windows: the C = K = 64 / 128 layers) load no filter block
+    // after the first unit
+    if (pair && mt2 && res && win_plan_for<kI8, BN, 2, 2, kS2>(c, w, &pl, true))
+      return launch ? launch_win<kI8, BN, 2, 2, kS2>(c, w, st, true) : ICV_OK;
     if (pair && mt2 && win_plan_for<kI8, BN, 2, 2, kS2>(c, w, &pl))
       return launch ? launch_win<kI8, BN, 2, 2, kS2>(c, w, st, false) : ICV_OK;
   }

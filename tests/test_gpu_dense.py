@@ -47,11 +47,16 @@ def _case(g, per_image, index_dtype, seed=3):
     return p, shape, xh, wh, bias, x, pf, zero, ib, tile, o
 
 
+@pytest.mark.parametrize("cs", [1, 2])
 @pytest.mark.parametrize("per_image,index_dtype", [(True, torch.int64), (False, torch.int32)])
 @pytest.mark.parametrize("geom", DENSE_GEOMS)
-def test_dense_a_matches_oracle_and_gather(geom, per_image, index_dtype):
+def test_dense_a_matches_oracle_and_gather(geom, per_image, index_dtype, cs, tune):
+    """Single CTAs and CTA pairs (cta_group::2, M = 256, each CTA its own
+    rows and half the filter block; odd M-tile counts leave a dummy)."""
+    tune(dense_cs=cs)
     p, shape, xh, wh, bias, x, pf, zero, ib, tile, o = _case(geom, per_image, index_dtype)
-    assert L.kernel_name(p, shape, torch.bfloat16) == "icv_igemm_smem<bf16,dense>"
+    assert L.kernel_name(p, shape, torch.bfloat16) == ("icv_igemm_smem<bf16,dense,pair>" if cs == 2
+                                                       else "icv_igemm_smem<bf16,dense>")
     y = icv.indirect_conv(x, pf, ib, p, tile).numpy()
     ref = oconv.indirect_conv_f32(oconv.bf16_round(xh), np.zeros(p.in_channels, np.float32), ib.offsets_host(), p,
                                   oconv.bf16_round(wh), bias, shape.n, o.h, o.w)
@@ -79,7 +84,7 @@ def test_dense_a_u8_bit_exact(geom):
     n, h, wd = g.pop("n"), g.pop("h"), g.pop("w")
     p = make_params(**g)
     shape = icv.Shape4(n, h, wd, p.in_channels)
-    assert L.kernel_name(p, shape, torch.uint8) == "icv_igemm_smem<u8,dense>"
+    assert L.kernel_name(p, shape, torch.uint8).startswith("icv_igemm_smem<u8,dense")
     rng = np.random.default_rng(7)
     xh = rng.integers(0, 256, shape.numel, dtype=np.uint8)
     wh = rng.integers(0, 256, p.out_channels * p.in_channels, dtype=np.uint8)
@@ -112,3 +117,18 @@ def test_misaligned_tensors_fail_cleanly():
         icv.indirect_conv(xv, pf, ibv, p, tile)
     torch.cuda.synchronize()
     assert icv.indirect_conv(x, pf, ib, p, tile).numpy().shape[0] == o.numel
+
+
+@pytest.mark.parametrize("cs", [1, 2])
+@pytest.mark.parametrize("geom", [dict(c=128, k=512, n=64, h=28, w=28),    # 3 stages, 8 epilogue warps, 2 N tiles
+                                  dict(c=1024, k=256, n=64, h=14, w=14),   # 16 K blocks per tile
+                                  dict(c=64, k=64, n=64, h=56, w=56)])     # ~42 tiles per CTA
+def test_dense_a_many_tiles_per_cta_equals_gather(geom, cs, tune):
+    """Full-size ResNet-50 1x1 shapes: every CTA runs many tiles, so the
+    stage ring wraps many times under several TMA issuers; the output must
+    equal the IB-gather kernel's byte for byte."""
+    tune(dense_cs=cs)
+    p, shape, xh, wh, bias, x, pf, zero, ib, tile, o = _case(geom, True, torch.int64)
+    y = icv.indirect_conv(x, pf, ib, p, tile)
+    yg = icv.indirect_conv(x, pf, ib, p, tile, algorithm="gather")
+    assert torch.equal(y.data, yg.data)

@@ -147,3 +147,17 @@ def test_window_kernel_u8_bit_exact(geom):
     ref = oq.indirect_conv_u8(xh, zero.cpu().numpy(), ib.offsets_host(), p, wh, bias, n, o.h, o.w,
                               zx, 0.02, zw, 0.005, 128, 0.1)
     assert np.array_equal(y, ref), int((y != ref).sum())
+
+
+@pytest.mark.parametrize("geom", [dict(r=3, s=3, pt=1, pl=1, c=64, k=64, n=32, h=56, w=56, mr=128),
+                                  dict(r=3, s=3, pt=1, pl=1, c=256, k=256, n=64, h=14, w=14, mr=128)])
+def test_window_kernel_full_size_equals_gather(geom, tune):
+    """ResNet-50 stride-1 3x3 shapes at full size (many units per CTA: the
+    filter ring and the resident-filter plans wrap many times) agree with the
+    IB-gather kernel."""
+    tune(win=-1)
+    p, shape, xh, wh, bias, x, pf, zero, ib, tile, o = _bf16_case(geom)
+    assert L.kernel_name(p, shape, torch.bfloat16) == "icv_igemm_win<bf16>"
+    y = icv.indirect_conv(x, pf, ib, p, tile).numpy()
+    yg = icv.indirect_conv(x, pf, ib, p, tile, algorithm="gather").numpy()
+    assert_bf16_close(y, yg)
