@@ -45,6 +45,7 @@ enum TuneKey {
   kTuneDenseA,           // 1: 1x1 stride-1 layers load A as dense TMA boxes, 0: IB gathers
   kTuneDenseCs,          // dense A: 2 = CTA pairs (M = 256), 1 = single CTAs
   kTunePdl,              // 1: persistent conv kernels use programmatic dependent launch
+  kTuneDensePf,          // dense A: L2 bulk prefetch of the A rows this many tiles ahead (0 = off)
   kTuneCount
 };
 int tune(TuneKey k);

@@ -61,6 +61,8 @@ struct TcArgs {
   int32_t ow;                // row-tiled kernels: output row width (pixels >= ow are not stored)
   int64_t ohw, img_elems;    // Ho*Wo, H*W*C
   int32_t oh;                // row-pair tiles (kSubRows 2): output rows per image
+  int32_t dense_pf;          // dense A: L2-prefetch the A rows this many local tiles ahead (0 = off)
+  int64_t x_rows;            // dense A: pixel rows of the bound input
 };
 
 // Where the references of output pixel p = tile_m*128 + row live: entry of

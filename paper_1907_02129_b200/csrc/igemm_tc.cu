@@ -21,6 +21,7 @@
 //              an all-ones tile: the per-pixel input row sums needed by the
 //              zero-point correction); tcgen05.commit releases smem stages
 //              and publishes finished accumulators.
+#include <cstdio>
 #include <cstdlib>
 
 #include "igemm_common.cuh"
@@ -283,6 +284,23 @@ __global__ void __launch_bounds__(kThreadsS<kI8, kEpiW>, 1) igemm_smem_kernel(co
         static_assert(C::kKB == 1, "dense A: one K block per stage");
         const int niss = kStages < kPW ? kStages : kPW;
         const int64_t mt = tile / a.n_tiles;
+        // L2 prefetch of the A rows of local tile k + dense_pf (one
+        // contiguous range of 128 pixel rows), by a thread that issues no
+        // TMA loads: the stage ring then reads A from L2, not from HBM
+        if (a.dense_pf > 0 && threadIdx.x == 1 && k + a.dense_pf < my_tiles) {
+          const int64_t mtp = sched(k + a.dense_pf) / a.n_tiles;
+          const int64_t rows = min((int64_t)kBM, a.x_rows - mtp * kBM);
+          if (rows > 0) {
+            const uint8_t* src = a.x + mtp * kBM * (int64_t)a.c_bytes;
+            int64_t bytes = rows * (int64_t)a.c_bytes;
+            while (bytes > 0) {
+              const uint32_t b = (uint32_t)(bytes < 65536 ? bytes : 65536);
+              bulk_prefetch_l2(src, b);
+              src += b;
+              bytes -= b;
+            }
+          }
+        }
         const int64_t q0 = k * num_kb;
         for (int kb = 0; kb < num_kb; ++kb) {
           const int64_t q = q0 + kb;
@@ -525,6 +543,8 @@ int launch_smem_cs(const ConvArgs& c, cudaStream_t st) {
   if constexpr (kIsDense<IbT>) {   // (single CTAs and pairs alike: each CTA loads its own 128 rows)
     if (int s = make_input_tmap(c, &tmap_x)) return fail(s, "dense-A input tensor map");
     a.use_tma_x = 1;
+    a.dense_pf = tune(kTuneDensePf);
+    a.x_rows = c.g.N * c.g.H * c.g.W;
   } else {
     tmap_x = tmap;   // unused placeholder
   }
@@ -542,6 +562,10 @@ int launch_smem_cs(const ConvArgs& c, cudaStream_t st) {
     if (clusters > groups) clusters = groups;
     grid = clusters * kCS;
   }
+  if (tune(kTuneWinDebug))   // (knob "win_debug" prints every tensor-core plan)
+    fprintf(stderr, "igemm_smem: i8 %d BN %d CS %d epi %d dense %d | grid %lld max_clusters %d stages %d slots %d "
+                    "smem %d tiles %lld n_tiles %d\n", (int)kI8, BN, kCS, kEpiW, (int)kIsDense<IbT>, (long long)grid,
+            max_clusters, pl.stages, pl.slots, pl.bytes, (long long)a.total_tiles, a.n_tiles);
   return launch_conv_kernel(kernel, (unsigned)grid, kThreadsS<kI8, kEpiW>, pl.bytes, st, kCS, "igemm_smem launch", tmap,
                             tmap_x, tmap_y, a, pl);
 }
@@ -702,6 +726,8 @@ int make_input_tmap(const ConvArgs& c, CUtensorMap* tmap) {
 void fill_tc_args(const ConvArgs& c, int block_n, TcArgs* a) {
   const bool i8 = c.L.family == kFamTcU8;
   a->use_tma_y = 0;
+  a->dense_pf = 0;
+  a->x_rows = c.g.N * c.g.H * c.g.W;
   a->tiles_per_row = 1;
   a->ow = 0;
   a->x = static_cast<const uint8_t*>(c.x);

@@ -28,7 +28,7 @@ def main():
         ms = statistics.median(t)
         ok = ""
         if w.dtype == "bf16" and not os.environ.get("ICV_NO_GATE"):
-            ok = bench.correctness_gate(w, xh, pf, ib, y)["normwise_rel_err"]
+            ok = bench.conv_gate(w, xh, ib, y)["normwise_rel_err"]
         kname = icv._lib.kernel_name(w.params, w.in_shape, x.dtype)
         print(f"{name:6s} {ms * 1e3:8.2f} us  {w.flops / ms / 1e9:8.1f} TFLOP/s  gate={ok}  [{kname}]")
         del x, pf, ib, y
