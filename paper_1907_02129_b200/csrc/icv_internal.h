@@ -46,6 +46,8 @@ enum TuneKey {
   kTuneDenseCs,          // dense A: 2 = CTA pairs (M = 256), 1 = single CTAs
   kTunePdl,              // 1: persistent conv kernels use programmatic dependent launch
   kTuneDensePf,          // dense A: L2 bulk prefetch of the A rows this many tiles ahead (0 = off)
+  kTuneRowsPf,           // row kernel: L2 bulk prefetch of the input rows this many tiles ahead (0 = off)
+  kTuneDenseResB,        // dense A: keep the filter blocks resident when they fit in this many KB (0 = off)
   kTuneCount
 };
 int tune(TuneKey k);

@@ -82,6 +82,7 @@ struct RowsArgs {
   int32_t row_bytes;            // W * C * 2 (one raw input row)
   int32_t ksteps;               // MMA K steps per kernel row (1 or 2)
   int64_t total_tiles;          // N * OH * tpr
+  int32_t pf;                   // loader: L2-prefetch the rows this many tiles ahead (0 = off)
 };
 
 struct RowsPlan {
@@ -227,8 +228,20 @@ __global__ void __launch_bounds__(kThreadsR, 1) igemm_rows_kernel(const __grid_c
       RP_T0();
       TileWalk walk;
       walk.start(a, t0);
+      // L2 prefetch of the rows `a.pf` tiles ahead: each tile adds only ~2
+      // input rows (a few KB), so the few stages in flight cannot cover the
+      // HBM latency; prefetched rows arrive from L2
+      TileWalk pwalk;
+      pwalk.start(a, t0);
+      auto prefetch_next = [&]() {
+        const TileRows pr = pwalk.next(a);
+        const int32_t pc = pr.new_hi - pr.new_lo + 1;
+        if (pc > 0) bulk_prefetch_l2(a.t.x + ((int64_t)pr.n * a.H + pr.new_lo) * a.row_bytes, (uint32_t)(pc * a.row_bytes));
+      };
+      for (int64_t k = 0; k < a.pf && k < my_tiles; ++k) prefetch_next();
       for (int64_t k = 0; k < my_tiles; ++k) {
         const int s = (int)(k % kStagesR);
+        if (a.pf > 0 && k + a.pf < my_tiles) prefetch_next();
         const TileRows tr = walk.next(a);
         RP_ACC(1);
         if (k >= kStagesR) mbar_wait(&stage_free[s], (uint32_t)((k / kStagesR - 1) & 1));
@@ -448,6 +461,7 @@ int launch_rows_ring(const ConvArgs& c, cudaStream_t st, const RowsPlan& pl, int
     if (cr != CUDA_SUCCESS) return fail(ICV_ERR_CUDA, "row kernel: output tensor map");
   }
   a.t.use_tma_y = tune(kTuneTmaStore) != 0;
+  a.pf = tune(kTuneRowsPf);
   const int sms = sm_count();
   const int grid = (int)(a.total_tiles < sms ? a.total_tiles : sms);
   return launch_conv_kernel(kernel, (unsigned)grid, kThreadsR, pl.bytes, st, 1, "igemm_rows launch", tmap_y, a, pl);

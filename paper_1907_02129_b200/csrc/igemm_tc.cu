@@ -96,21 +96,26 @@ struct CfgS {
 struct PlanS {
   int slots, stages;
   int off_b, off_ones, off_epi, off_bias, off_ib, off_bar, bytes;
+  int res_b;   // dense A: filter blocks of this CTA's N tile kept resident (0 = streamed per stage)
 };
 
 template <bool kI8, int BN, typename IbT, int kPair = 1, int kEpiW = kEpiWarpsS<kI8>>
-bool plan_smem(int rs, int n_pad, PlanS* p) {
+bool plan_smem(int rs, int n_pad, PlanS* p, int res_kb = 0) {
   using C = CfgS<kI8, BN, kPair, kEpiW, kIsDense<IbT>>;
   const int bias = (n_pad * 4 + 15) / 16 * 16;
   const int ib = kIsDense<IbT> ? 0 : 2 * rs * kBM * 4 + 2 * kBM * 4;   // int32 index slices + per-row bases
-  const int fixed = 1024 + C::kOnesBytes + C::kEpiBytes + bias + ib + C::kBarBytes;
-  int slots = (232448 - fixed) / C::kSlotBytes;
+  // resident filter (dense A only): res_kb blocks of B, the ring holds A only
+  const int res = res_kb * C::kBBytes;
+  const int slot_bytes = res_kb ? kABytes : C::kSlotBytes;
+  const int fixed = 1024 + C::kOnesBytes + C::kEpiBytes + bias + ib + C::kBarBytes + res;
+  int slots = (232448 - fixed) / slot_bytes;
   slots = (slots > C::kMaxSlots ? C::kMaxSlots : slots) / C::kKB * C::kKB;
   if (slots < 2 * C::kKB) return false;
+  p->res_b = res_kb;
   p->slots = slots;
   p->stages = slots / C::kKB;
   p->off_b = slots * kABytes;
-  p->off_ones = p->off_b + slots * C::kBBytes;
+  p->off_ones = p->off_b + (res_kb ? res : slots * C::kBBytes);
   p->off_epi = p->off_ones + C::kOnesBytes;
   p->off_bias = p->off_epi + C::kEpiBytes;
   p->off_ib = p->off_bias + bias;
@@ -175,7 +180,8 @@ __global__ void __launch_bounds__(kThreadsS<kI8, kEpiW>, 1) igemm_smem_kernel(co
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* bres = tempty + 2;                                        // resident filter landed (dense A)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -202,6 +208,7 @@ __global__ void __launch_bounds__(kThreadsS<kI8, kEpiW>, 1) igemm_smem_kernel(co
       // one arrival per epilogue warp (of both CTAs at the pair leader)
       mbar_init(&tempty[s], (kCS == 2 && crank == 0) ? 2 * kEpiW : kEpiW);
     }
+    mbar_init(bres, 1);
     fence_mbar_init();
     tma_prefetch_desc(&tmap_b);
     if (dense_a) tma_prefetch_desc(&tmap_x);
@@ -255,6 +262,15 @@ __global__ void __launch_bounds__(kThreadsS<kI8, kEpiW>, 1) igemm_smem_kernel(co
       }
       cp_async_commit();
     };
+    if constexpr (dense_a) {
+      // resident filter: every K block of this CTA's (fixed) N tile, once
+      if (pl.res_b && threadIdx.x == 0 && my_tiles > 0) {
+        const int nt0 = (int)(sched(0) % a.n_tiles);
+        mbar_arrive_expect_tx(bres, pl.res_b * C::kBBytes);
+        for (int kb = 0; kb < pl.res_b; ++kb)
+          tma_load_3d(sB_u32 + kb * C::kBBytes, &tmap_b, bres, 0, nt0 * BN, kb);
+      }
+    }
     stage_index_slice(0);
     cp_async_wait_committed();
     named_bar_sync(1, 32 * kProdWarpsS<kI8>);
@@ -307,9 +323,13 @@ __global__ void __launch_bounds__(kThreadsS<kI8, kEpiW>, 1) igemm_smem_kernel(co
           if (lane == 0 && (int)(q % niss) == warp) {
             const int st = (int)(q % kStages);
             mbar_wait(&empty[st], (uint32_t)((q / kStages) & 1) ^ 1u);
-            mbar_arrive_expect_tx(&full[st], kABytes + C::kBBytes);
-            // (a pair member loads its half of the BN filter rows)
-            tma_load_3d(sB_u32 + st * C::kBBytes, &tmap_b, &full[st], 0, nt * BN + (int)crank * (BN / kCS), kb);
+            if (pl.res_b) {   // resident filter: the stage holds A only
+              mbar_arrive_expect_tx(&full[st], kABytes);
+            } else {
+              mbar_arrive_expect_tx(&full[st], kABytes + C::kBBytes);
+              // (a pair member loads its half of the BN filter rows)
+              tma_load_3d(sB_u32 + st * C::kBBytes, &tmap_b, &full[st], 0, nt * BN + (int)crank * (BN / kCS), kb);
+            }
             tma_load_2d(sA_u32 + st * kABytes, &tmap_x, &full[st], kb * a.cblock_elems, (int32_t)(mt * kBM));
           }
         }
@@ -440,6 +460,10 @@ __global__ void __launch_bounds__(kThreadsS<kI8, kEpiW>, 1) igemm_smem_kernel(co
     long long c_wait_full = 0, c_wait_tempty = 0, c_begin = clock64();
 #endif
     const int64_t n_local = sched.count();
+    if (pl.res_b && n_local > 0) {   // resident filter landed
+      mbar_wait(bres, 0);
+      tc_fence_after();
+    }
     for (int64_t ti_local = 0; ti_local < n_local; ++ti_local) {
 #ifdef ICV_TRACE
       long long c0 = clock64();
@@ -465,7 +489,7 @@ __global__ void __launch_bounds__(kThreadsS<kI8, kEpiW>, 1) igemm_smem_kernel(co
           for (int j = 0; j < nsub; ++j) {
             const int slot = stage * C::kKB + j;
             const uint64_t adesc = sw128_kmajor_desc(sA_u32 + slot * kABytes);
-            const uint64_t bdesc = sw128_kmajor_desc(sB_u32 + slot * C::kBBytes);
+            const uint64_t bdesc = sw128_kmajor_desc(sB_u32 + (pl.res_b ? si * C::kKB + j : slot) * C::kBBytes);
 #pragma unroll
             for (int k = 0; k < 4; ++k) {  // 4 x 32-byte K steps per 128-byte block
               const uint32_t acc = (si | j | k) != 0;
@@ -528,6 +552,21 @@ int launch_smem_cs(const ConvArgs& c, cudaStream_t st) {
   PlanS pl;
   if (!plan_smem<kI8, BN, IbT, kCS, kEpiW>(c.g.RS(), c.L.n_pad, &pl))
     return fail(ICV_ERR_UNSUPPORTED, "indirection slice of this kernel size does not fit in shared memory");
+  // dense A with few K blocks: keep the CTA's filter blocks resident (the
+  // grid is then a multiple of the N-tile count, so every CTA keeps one N
+  // tile) when they fit in dense_resb KB and the A ring keeps >= 4 stages
+  int grid_mult = 1;
+  if constexpr (kIsDense<IbT> && kCS == 1) {
+    using Cd = CfgS<kI8, BN, 1, kEpiW, true>;
+    const int kbs = c.L.cblocks;   // K blocks per tile (R = S = 1)
+    const int n_tiles = c.L.n_pad / BN;
+    PlanS pr;
+    if (tune(kTuneDenseResB) > 0 && kbs * Cd::kBBytes <= tune(kTuneDenseResB) * 1024 && n_tiles <= 8 &&
+        plan_smem<kI8, BN, IbT, kCS, kEpiW>(1, c.L.n_pad, &pr, kbs) && pr.stages >= 4) {
+      pl = pr;
+      grid_mult = n_tiles;
+    }
+  }
   if (c.g.N * c.g.H * c.g.W * (int64_t)c.g.C >= (int64_t(1) << 31))
     return fail(ICV_ERR_UNSUPPORTED, "tensor-core kernel: input tensors of 2^31 or more elements are not supported");
   int max_clusters = 0;
@@ -555,6 +594,7 @@ int launch_smem_cs(const ConvArgs& c, cudaStream_t st) {
   int64_t grid;
   if constexpr (kCS == 1) {
     grid = a.total_tiles < sms ? a.total_tiles : sms;
+    if (grid_mult > 1) grid = grid / grid_mult * grid_mult;   // (resident filter: one N tile per CTA)
   } else {
     const int64_t groups = (a.total_tiles / a.n_tiles + kCS - 1) / kCS * a.n_tiles;
     int64_t clusters = sms / kCS;
@@ -564,8 +604,9 @@ int launch_smem_cs(const ConvArgs& c, cudaStream_t st) {
   }
   if (tune(kTuneWinDebug))   // (knob "win_debug" prints every tensor-core plan)
     fprintf(stderr, "igemm_smem: i8 %d BN %d CS %d epi %d dense %d | grid %lld max_clusters %d stages %d slots %d "
-                    "smem %d tiles %lld n_tiles %d\n", (int)kI8, BN, kCS, kEpiW, (int)kIsDense<IbT>, (long long)grid,
-            max_clusters, pl.stages, pl.slots, pl.bytes, (long long)a.total_tiles, a.n_tiles);
+                    "smem %d tiles %lld n_tiles %d resident filter blocks %d\n", (int)kI8, BN, kCS, kEpiW,
+            (int)kIsDense<IbT>, (long long)grid, max_clusters, pl.stages, pl.slots, pl.bytes, (long long)a.total_tiles,
+            a.n_tiles, pl.res_b);
   return launch_conv_kernel(kernel, (unsigned)grid, kThreadsS<kI8, kEpiW>, pl.bytes, st, kCS, "igemm_smem launch", tmap,
                             tmap_x, tmap_y, a, pl);
 }
