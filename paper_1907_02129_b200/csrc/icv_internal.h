@@ -48,6 +48,7 @@ enum TuneKey {
   kTuneDensePf,          // dense A: L2 bulk prefetch of the A rows this many tiles ahead (0 = off)
   kTuneRowsPf,           // row kernel: L2 bulk prefetch of the input rows this many tiles ahead (0 = off)
   kTuneDenseResB,        // dense A: keep the filter blocks resident when they fit in this many KB (0 = off)
+  kTuneEpiWide,          // bf16 epilogue: 64-column chunks with 4 KB TMA stores (1) or 32-column chunks (0)
   kTuneCount
 };
 int tune(TuneKey k);

@@ -62,6 +62,7 @@ struct TcArgs {
   int64_t ohw, img_elems;    // Ho*Wo, H*W*C
   int32_t oh;                // row-pair tiles (kSubRows 2): output rows per image
   int32_t dense_pf;          // dense A: L2-prefetch the A rows this many local tiles ahead (0 = off)
+  int32_t epi_wide;          // bf16 epilogue: 64-column chunks, 128-byte-swizzled staging, 64 x 32 TMA boxes
   int64_t x_rows;            // dense A: pixel rows of the bound input
 };
 
@@ -227,6 +228,68 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
 #else
     const int nchunks = cols_left > 0 && row_valid ? (min(kColsPerWarp, cols_left) + 31) / 32 : 0;
 #endif
+    if constexpr (!kI8 && !kRowTiles && kColsPerWarp % 64 == 0) {
+      if (use_tma && a.epi_wide) {
+        // 64-column chunks: two TMEM loads under one wait, the 32 x 64 block
+        // staged 128-byte swizzled (conflict-free row-per-lane writes) and
+        // stored as one 4 KB TMA box -- half the fences, stores and waits of
+        // the 32-column path.  One staging buffer per warp: the previous
+        // box must have been read before it is rewritten (that wait overlaps
+        // this chunk's TMEM loads and conversion).
+        const int nw = nchunks > 0 ? (min(kColsPerWarp, cols_left) + 63) / 64 : 0;
+        const uint32_t sb = smem_u32(stg);
+#pragma unroll 1
+        for (int ci = 0; ci < nw; ++ci) {
+          const int c = col0 + ci * 64;
+          const int n = nt * BN + c;
+          uint32_t v0[32], v1[32];
+          tmem_ld_32x32b_x32(taddr + c, v0);
+          tmem_ld_32x32b_x32(taddr + c + 32, v1);
+          tmem_ld_wait_regs(v0);
+          tmem_ld_wait_regs(v1);
+          uint32_t w[32];
+          const float4* bias4 = reinterpret_cast<const float4*>(sBias + n);
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const float4 b = bias4[q];
+            const uint32_t* vv = q < 8 ? v0 : v1;
+            const int o = 4 * (q & 7);
+            __nv_bfloat162 lo = __floats2bfloat162_rn(__uint_as_float(vv[o + 0]) + b.x, __uint_as_float(vv[o + 1]) + b.y);
+            __nv_bfloat162 hi = __floats2bfloat162_rn(__uint_as_float(vv[o + 2]) + b.z, __uint_as_float(vv[o + 3]) + b.w);
+            w[2 * q] = *reinterpret_cast<uint32_t*>(&lo);
+            w[2 * q + 1] = *reinterpret_cast<uint32_t*>(&hi);
+          }
+          if (chunk_seq > 0) {
+            if (lane == 0) bulk_wait_group_read<0>();
+            __syncwarp();
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            sts128(sb + lane * 128 + ((q ^ (lane & 7)) << 4), w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(tmap_y, sb, n, (int32_t)row0);
+            bulk_commit_group();
+          }
+          ++chunk_seq;
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (tempty_remote) mbar_arrive_remote_relaxed(tempty_remote + as * 8);
+          else mbar_arrive(&tempty[as]);
+        }
+        if constexpr (kTileGroups > 1) {
+          as += kTileGroups;
+          if (as >= kAccStages) { as -= kAccStages; aphase ^= 1; }
+        } else if (++as == kAccStages) {
+          as = 0;
+          aphase ^= 1;
+        }
+        continue;
+      }
+    }
     uint32_t v[32];
     if (nchunks > 0) {
       tmem_ld_32x32b_x32(taddr + col0, v);
@@ -385,7 +448,7 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
 PFN_cuTensorMapEncodeTiled_v12000 get_tensor_map_encoder();
 int make_filter_tmap(const ConvArgs& c, int block_n, int depth, CUtensorMap* tmap);
 int make_input_tmap(const ConvArgs& c, CUtensorMap* tmap);
-int make_output_tmap(const ConvArgs& c, CUtensorMap* tmap);
+int make_output_tmap(const ConvArgs& c, CUtensorMap* tmap, bool wide = false);
 void fill_tc_args(const ConvArgs& c, int block_n, TcArgs* a);
 int sm_count();
 

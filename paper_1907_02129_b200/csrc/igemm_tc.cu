@@ -588,7 +588,11 @@ int launch_smem_cs(const ConvArgs& c, cudaStream_t st) {
     tmap_x = tmap;   // unused placeholder
   }
   CUtensorMap tmap_y;
-  a.use_tma_y = make_output_tmap(c, &tmap_y) == ICV_OK;
+  // wide epilogue chunks when each epilogue warp owns a multiple of 64 columns
+  constexpr bool kWideOk = !kI8 && (BN / (kEpiW / 4)) % 64 == 0;
+  a.epi_wide = kWideOk && tune(kTuneEpiWide) != 0;
+  a.use_tma_y = make_output_tmap(c, &tmap_y, a.epi_wide) == ICV_OK;
+  if (!a.use_tma_y) a.epi_wide = 0;
   if (!a.use_tma_y) tmap_y = tmap;   // unused placeholder
   const int sms = sm_count();
   int64_t grid;
@@ -710,7 +714,7 @@ int make_filter_tmap(const ConvArgs& c, int block_n, int depth, CUtensorMap* tma
 // for the epilogue's TMA tile stores: box = 32 columns x 32 rows; bf16 rows
 // of the box are 64 bytes with the 64-byte swizzle, uint8 rows 32 bytes
 // unswizzled.  Needs 16-byte aligned rows (K*elem % 16 == 0).
-int make_output_tmap(const ConvArgs& c, CUtensorMap* tmap) {
+int make_output_tmap(const ConvArgs& c, CUtensorMap* tmap, bool wide) {
   if (tune(kTuneTmaStore) == 0) return ICV_ERR_UNSUPPORTED;
   const bool i8 = c.L.family == kFamTcU8;
   if (!i8 && c.L.family != kFamTcBf16 && c.L.family != kFamStemBf16) return ICV_ERR_UNSUPPORTED;
@@ -721,12 +725,15 @@ int make_output_tmap(const ConvArgs& c, CUtensorMap* tmap) {
   if (!encode) return ICV_ERR_CUDA;
   const cuuint64_t dims[2] = {(cuuint64_t)c.g.K, (cuuint64_t)c.P};
   const cuuint64_t strides[1] = {(cuuint64_t)c.g.K * eb};
-  const cuuint32_t box[2] = {32, 32};
+  // box: 32 columns x 32 rows (bf16: 64-byte swizzle), or for the wide bf16
+  // epilogue 64 columns x 32 rows with the 128-byte swizzle
+  const bool w64 = wide && !i8;
+  const cuuint32_t box[2] = {w64 ? 64u : 32u, 32};
   const cuuint32_t estr[2] = {1, 1};
   CUresult cr = encode(tmap, i8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, c.y, dims, strides,
                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                       i8 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                       i8 ? CU_TENSOR_MAP_SWIZZLE_NONE : (w64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B),
+                       CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return cr == CUDA_SUCCESS ? ICV_OK : ICV_ERR_CUDA;
 }
 
@@ -768,6 +775,7 @@ void fill_tc_args(const ConvArgs& c, int block_n, TcArgs* a) {
   const bool i8 = c.L.family == kFamTcU8;
   a->use_tma_y = 0;
   a->dense_pf = 0;
+  a->epi_wide = 0;
   a->x_rows = c.g.N * c.g.H * c.g.W;
   a->tiles_per_row = 1;
   a->ow = 0;

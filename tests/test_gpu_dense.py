@@ -132,3 +132,23 @@ def test_dense_a_many_tiles_per_cta_equals_gather(geom, cs, tune):
     y = icv.indirect_conv(x, pf, ib, p, tile)
     yg = icv.indirect_conv(x, pf, ib, p, tile, algorithm="gather")
     assert torch.equal(y.data, yg.data)
+
+
+@pytest.mark.parametrize("wide", [0, 1])
+@pytest.mark.parametrize("geom", [dict(c=64, k=256, n=2, h=14, w=14), dict(c=128, k=512, n=8, h=28, w=28),
+                                  dict(c=72, k=200, n=1, h=9, w=7), dict(c=256, k=128, n=3, h=14, w=14)])
+def test_epilogue_chunk_width_bit_identical(geom, wide, tune):
+    """The 64-column epilogue (one 4 KB TMA box per chunk) and the 32-column
+    one store the same bytes (same fp32 sums, same rounding); ragged K tails
+    are clipped by TMA in both."""
+    p, shape, xh, wh, bias, x, pf, zero, ib, tile, o = _case(geom, True, torch.int64)
+    tune(epi_wide=0)
+    y0 = icv.indirect_conv(x, pf, ib, p, tile).numpy()
+    g0 = icv.indirect_conv(x, pf, ib, p, tile, algorithm="gather").numpy()
+    tune(epi_wide=wide)
+    y1 = icv.indirect_conv(x, pf, ib, p, tile).numpy()
+    g1 = icv.indirect_conv(x, pf, ib, p, tile, algorithm="gather").numpy()
+    assert y0.tobytes() == y1.tobytes() and g0.tobytes() == g1.tobytes()
+    ref = oconv.indirect_conv_f32(oconv.bf16_round(xh), np.zeros(p.in_channels, np.float32), ib.offsets_host(), p,
+                                  oconv.bf16_round(wh), bias, shape.n, o.h, o.w)
+    assert_bf16_close(y1.reshape(-1, p.out_channels), ref.reshape(-1, p.out_channels))
