@@ -152,3 +152,18 @@ def test_epilogue_chunk_width_bit_identical(geom, wide, tune):
     ref = oconv.indirect_conv_f32(oconv.bf16_round(xh), np.zeros(p.in_channels, np.float32), ib.offsets_host(), p,
                                   oconv.bf16_round(wh), bias, shape.n, o.h, o.w)
     assert_bf16_close(y1.reshape(-1, p.out_channels), ref.reshape(-1, p.out_channels))
+
+
+@pytest.mark.parametrize("geom", [dict(c=512, k=512, n=4, h=7, w=7), dict(c=128, k=256, n=2, h=9, w=9)])
+def test_half_width_tiles_on_a_block256_packing(geom, tune):
+    """BLOCK_N 128 tiles (chosen when BLOCK_N 256 would leave a partial last
+    wave) read the BLOCK_N-256 packed filter unchanged: same sums, same bytes
+    for the dense and the gather kernels."""
+    p, shape, xh, wh, bias, x, pf, zero, ib, tile, o = _case(geom, True, torch.int64)
+    tune(small_tile_bn=0)
+    y0 = icv.indirect_conv(x, pf, ib, p, tile).numpy()
+    g0 = icv.indirect_conv(x, pf, ib, p, tile, algorithm="gather").numpy()
+    tune(small_tile_bn=100000)
+    y1 = icv.indirect_conv(x, pf, ib, p, tile).numpy()
+    g1 = icv.indirect_conv(x, pf, ib, p, tile, algorithm="gather").numpy()
+    assert y0.tobytes() == y1.tobytes() and g0.tobytes() == g1.tobytes()
