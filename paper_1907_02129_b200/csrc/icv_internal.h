@@ -50,6 +50,7 @@ enum TuneKey {
   kTuneDenseResB,        // dense A: keep the filter blocks resident when they fit in this many KB (0 = off)
   kTuneEpiWide,          // bf16 epilogue: 64-column chunks with 4 KB TMA stores (1) or 32-column chunks (0)
   kTuneSmallTileBn,      // bf16 gather/dense: BLOCK_N 128 instead of 256 when tiles < this % of the SM count (0 = never)
+  kTuneWinFiltLanes,     // window kernel: filter-block issuing lanes per filter producer warp
   kTuneCount
 };
 int tune(TuneKey k);

@@ -230,7 +230,32 @@ __global__ void __launch_bounds__(kThreadsS<kI8, kEpiW>, 1) igemm_smem_kernel(co
   else __syncthreads();
   tc_fence_after();
   // setup above read only constants (bias, zero row); the input activation
-  // and the output may belong to the previous kernel in the stream
+  // and the output may belong to the previous kernel in the stream.  The
+  // filter does not: with dense A the first ring pass's filter blocks (or the
+  // resident filter) are requested before the wait, so under programmatic
+  // dependent launch they arrive while the previous kernel drains.
+  if constexpr (dense_a && kCS == 1) {
+    constexpr int kPWd = kProdWarpsS<kI8>;
+    if (warp < kPWd && lane == 0) {
+      const int64_t my_tiles0 = sched.count();
+      const int nkb = a.RS * a.cblocks;
+      if (pl.res_b) {
+        if (warp == 0 && my_tiles0 > 0) {
+          const int nt0 = (int)(sched(0) % a.n_tiles);
+          mbar_arrive_expect_tx(bres, pl.res_b * C::kBBytes);
+          for (int kb = 0; kb < pl.res_b; ++kb)
+            tma_load_3d(smem_u32(sB) + kb * C::kBBytes, &tmap_b, bres, 0, nt0 * BN, kb);
+        }
+      } else {
+        const int niss = pl.stages < kPWd ? pl.stages : kPWd;
+        for (int64_t q = warp; warp < niss && q < pl.stages && q < my_tiles0 * nkb; q += niss) {
+          const int nt0 = (int)(sched(q / nkb) % a.n_tiles);
+          mbar_arrive_expect_tx(&full[q], kABytes + C::kBBytes);
+          tma_load_3d(smem_u32(sB) + (int)q * C::kBBytes, &tmap_b, &full[q], 0, nt0 * BN, (int)(q % nkb));
+        }
+      }
+    }
+  }
   griddep_wait();
   griddep_launch_dependents();
   const uint32_t tmem_base = *tmem_slot;
@@ -262,15 +287,6 @@ __global__ void __launch_bounds__(kThreadsS<kI8, kEpiW>, 1) igemm_smem_kernel(co
       }
       cp_async_commit();
     };
-    if constexpr (dense_a) {
-      // resident filter: every K block of this CTA's (fixed) N tile, once
-      if (pl.res_b && threadIdx.x == 0 && my_tiles > 0) {
-        const int nt0 = (int)(sched(0) % a.n_tiles);
-        mbar_arrive_expect_tx(bres, pl.res_b * C::kBBytes);
-        for (int kb = 0; kb < pl.res_b; ++kb)
-          tma_load_3d(sB_u32 + kb * C::kBBytes, &tmap_b, bres, 0, nt0 * BN, kb);
-      }
-    }
     stage_index_slice(0);
     cp_async_wait_committed();
     named_bar_sync(1, 32 * kProdWarpsS<kI8>);
@@ -323,14 +339,22 @@ __global__ void __launch_bounds__(kThreadsS<kI8, kEpiW>, 1) igemm_smem_kernel(co
           if (lane == 0 && (int)(q % niss) == warp) {
             const int st = (int)(q % kStages);
             mbar_wait(&empty[st], (uint32_t)((q / kStages) & 1) ^ 1u);
+#ifdef ICV_TRACE
+            if (k == (my_tiles > 1 ? 1 : 0) && kb < 16) TRACE(64 + kb);   // stage free
+#endif
             if (pl.res_b) {   // resident filter: the stage holds A only
               mbar_arrive_expect_tx(&full[st], kABytes);
+            } else if (kCS == 1 && q < kStages) {
+              // (first ring pass: expect_tx and the filter block were issued before griddep_wait)
             } else {
               mbar_arrive_expect_tx(&full[st], kABytes + C::kBBytes);
               // (a pair member loads its half of the BN filter rows)
               tma_load_3d(sB_u32 + st * C::kBBytes, &tmap_b, &full[st], 0, nt * BN + (int)crank * (BN / kCS), kb);
             }
             tma_load_2d(sA_u32 + st * kABytes, &tmap_x, &full[st], kb * a.cblock_elems, (int32_t)(mt * kBM));
+#ifdef ICV_TRACE
+            if (k == (my_tiles > 1 ? 1 : 0) && kb < 16) TRACE(96 + kb);   // stage issued
+#endif
           }
         }
       } else {
@@ -482,7 +506,7 @@ __global__ void __launch_bounds__(kThreadsS<kI8, kEpiW>, 1) igemm_smem_kernel(co
         mbar_wait(&full[stage], phase);
 #ifdef ICV_TRACE
         c_wait_full += clock64() - c1;
-        if (lane == 0 && ti_local == 1 && si < 16) TRACE(80 + si);   // stage full (MMA warp wakes)
+        if (lane == 0 && ti_local == (n_local > 1 ? 1 : 0) && si < 16) TRACE(80 + si);   // stage full (MMA warp wakes)
 #endif
         tc_fence_after();
         if (elect_one()) {

@@ -81,6 +81,7 @@ struct WinArgs {
   int32_t win_lead;      // bytes from a slot's start to the window's first row (1024-aligned)
   int32_t zero_known;    // host certifies the zero row is all zeros (no in-kernel check)
   int32_t win_split;     // TMA windows: rows split over this many issuing threads (lane 0 of warps 0..)
+  int32_t filt_lanes;    // filter-block issuers per remaining producer warp (lanes 0..filt_lanes-1)
   // stride 2: the input is read as nph phase planes (row parity py, column
   // parity px); php[p] = 2 * py + px of the p-th plane holding taps
   int32_t sy;            // 1 or 2 (both directions)
@@ -394,10 +395,6 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
   if constexpr (kCS > 1) cluster_sync_all();   // the peer's barriers exist before any remote signal
   else __syncthreads();
   tc_fence_after();
-  griddep_wait();   // (setup read only constants; tensors may belong to the previous kernel)
-  griddep_launch_dependents();
-  const uint32_t tmem_base = *tmem_slot;
-  if (threadIdx.x == 0) TRACE(1);
   const int cblocks = a.t.cblocks;
   const int RS = a.t.RS;
   const uint32_t sWin_u32 = smem_u32(sWin);
@@ -414,6 +411,48 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
     else
       tma_load_3d(sB_u32 + slot * C::kBBytes, &tmap_b, &bfull[slot], 0, 0, e * cblocks + cb);
   };
+  // Filter-block issue order (the producer loop below and the pre-issue):
+  // TMA windows -- the producer warps past the window issuers load filter
+  // blocks round-robin over the ring sequence fq (at most bslots threads, so
+  // a slot's parity wait is never more than one phase ahead; lanes
+  // 0 .. filt_lanes-1 of each such warp issue independently).
+  const int nfilt = tma_win ? min((kProdWarpsW - a.win_split) * a.filt_lanes, pl.bslots) : 1;
+  const int fidx = tma_win ? (warp - a.win_split) * a.filt_lanes + lane : 0;
+  const bool filt_thread = warp < kProdWarpsW &&
+                           (tma_win ? (lane < a.filt_lanes && warp >= a.win_split && fidx < nfilt) : threadIdx.x == 0);
+  // The filter is not written by the previous kernel, so the first unit's
+  // filter blocks (the whole filter when it is resident; otherwise the first
+  // ring pass) are requested before griddep_wait: under programmatic
+  // dependent launch they land while the previous kernel drains.
+  int64_t pre_fq = 0;   // ring blocks issued before the wait (non-resident)
+  if (filt_thread && cid < a.units) {
+    const int32_t nt0 = cid % a.t.n_tiles;
+    int64_t fq = 0;
+    for (int st = 0; st < cblocks * nph && fq < (pl.resident ? (int64_t)1 << 40 : (int64_t)pl.bslots); ++st) {
+      const int cb = kS2 ? st / nph : st, pi = kS2 ? st - cb * nph : 0;
+      for (int i = kS2 ? sPh[pi] : 0; i < (kS2 ? sPh[pi + 1] : RS); ++i, ++fq) {
+        if (!pl.resident && fq >= pl.bslots) break;
+        if ((int)(fq % nfilt) != fidx) continue;
+        const int e = kS2 ? sTapE[i] : i;
+        if (pl.resident) {
+          load_filter_slot(cb * RS + e);
+        } else {
+          const int bs = (int)fq;   // first ring pass: slot fq, phase 0 (free)
+          if (crank == 0) mbar_arrive_expect_tx(&bfull[bs], kCS * C::kBBytes);
+          if constexpr (kCS == 2)
+            tma_load_3d_cg2(sB_u32 + bs * C::kBBytes, &tmap_b, mapa_rank(smem_u32(&bfull[bs]), 0), 0,
+                            nt0 * BN + (int)crank * (BN / kCS), e * cblocks + cb);
+          else
+            tma_load_3d(sB_u32 + bs * C::kBBytes, &tmap_b, &bfull[bs], 0, nt0 * BN, e * cblocks + cb);
+        }
+      }
+    }
+    pre_fq = pl.resident ? 0 : (fq < pl.bslots ? fq : pl.bslots);
+  }
+  griddep_wait();   // (setup read only constants; tensors may belong to the previous kernel)
+  griddep_launch_dependents();
+  const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) TRACE(1);
   if (warp < kProdWarpsW) {
     // ------------------------------------------------------------ producers
     // TMA windows: lane 0 of warps 0 .. win_split-1 each load a share of
@@ -429,11 +468,6 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
     // TMA load of BN / kCS rows, so at ~450 cycles per load one thread would
     // cap a stage at RS loads * 450 cycles).
     const bool win_thread = !tma_win || (lane == 0 && warp < a.win_split);
-    // (at most bslots filter threads, so each ring slot's parity wait is
-    // never more than one phase ahead: see the dense-A producer, igemm_tc.cu)
-    const int nfilt = tma_win ? min(kProdWarpsW - a.win_split, pl.bslots) : 1;
-    const int fidx = tma_win ? warp - a.win_split : 0;
-    const bool filt_thread = tma_win ? (lane == 0 && warp >= a.win_split && fidx < nfilt) : threadIdx.x == 0;
     if (!win_thread && !filt_thread) goto done;
     {
       int ws = 0;
@@ -511,12 +545,10 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
           // this CTA's rows of the filter blocks of this stage, one per tap
           // (resident filter: loaded during the first unit only)
           if (filt_thread && pl.resident) {
-            if (uk == 0)
-              for (int i = kS2 ? sPh[pi] : 0; i < (kS2 ? sPh[pi + 1] : RS); ++i)
-                if (i % nfilt == fidx) load_filter_slot(cb * RS + (kS2 ? sTapE[i] : i));
+            // (resident: every slot was requested before griddep_wait)
           } else if (filt_thread) {
             for (int i = kS2 ? sPh[pi] : 0; i < (kS2 ? sPh[pi + 1] : RS); ++i, ++fq) {
-              if ((int)(fq % nfilt) != fidx) continue;
+              if ((int)(fq % nfilt) != fidx || fq < pre_fq) continue;
               const int e = kS2 ? sTapE[i] : i;
               const int bs = (int)(fq % pl.bslots);
               mbar_wait(&bempty[bs], (uint32_t)((fq / pl.bslots) & 1) ^ 1u);
@@ -1106,6 +1138,7 @@ int launch_win(const ConvArgs& c, const WinGeom& w, cudaStream_t st, bool reside
   a.g_shift = w.g_shift;
   a.rel_shift = w.rel_shift;
   a.win_split = tune(kTuneWinSplit);
+  a.filt_lanes = tune(kTuneWinFiltLanes) < 1 ? 1 : (tune(kTuneWinFiltLanes) > 8 ? 8 : tune(kTuneWinFiltLanes));
   if (a.win_split < 1) a.win_split = 1;
   if (a.win_split > kProdWarpsW) a.win_split = kProdWarpsW;
   if (a.win_split > w.WR) a.win_split = w.WR;

@@ -17,9 +17,10 @@ from paper_1907_02129_b200.stack import ResNet50Stack  # noqa: E402
 
 def main():
     name = sys.argv[1]
+    batch = int(sys.argv[2]) if len(sys.argv) > 2 else 256
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(0)
-    stack = ResNet50Stack(device=dev)
+    stack = ResNet50Stack(batch=batch, device=dev)
     layer = {l.name: l for l in stack.layers}[name]
     fn = L.lib().icv_debug_trace
     fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
@@ -60,6 +61,14 @@ def main():
     ew = buf[:148, 28].astype(np.float64)
     ek = buf[:148, 29].astype(np.float64)
     print(f"epilogue warp 0: waiting on tmem-full {ew.mean():.0f} cycles, working {ek.mean():.0f} cycles")
+    for cta in (0, 1):
+        r = tr[cta]
+        print(f"cta {cta}: per stage of the traced tile (us after entry): free / issued / full")
+        for s_ in range(16):
+            if r[64 + s_] == 0 and r[80 + s_] == 0:
+                break
+            f = lambda v: f"{(v - r[0]) / 1e3:7.2f}" if v > 0 else "      -"   # noqa: E731
+            print(f"   s{s_:2d}: {f(r[64 + s_])} {f(r[96 + s_])} {f(r[80 + s_])}")
     d = rel[:, 3] - rel[:, 2]
     print(f"median tile-1 mainloop (mma_end1 - mma_end0) {np.median(d[d > 0]) / 1e3:.2f} us; "
           f"median epilogue {np.median((rel[:, 18] - rel[:, 10])[rel[:, 10] >= 0]) / 1e3:.2f} us")
