@@ -51,6 +51,7 @@ enum TuneKey {
   kTuneEpiWide,          // bf16 epilogue: 64-column chunks with 4 KB TMA stores (1) or 32-column chunks (0)
   kTuneSmallTileBn,      // bf16 gather/dense: BLOCK_N 128 instead of 256 when tiles < this % of the SM count (0 = never)
   kTuneWinFiltLanes,     // window kernel: filter-block issuing lanes per filter producer warp
+  kTuneRowsLoaders,      // row kernel: lanes issuing the raw-row bulk copies
   kTuneCount
 };
 int tune(TuneKey k);

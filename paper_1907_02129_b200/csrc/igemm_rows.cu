@@ -83,6 +83,7 @@ struct RowsArgs {
   int32_t ksteps;               // MMA K steps per kernel row (1 or 2)
   int64_t total_tiles;          // N * OH * tpr
   int32_t pf;                   // loader: L2-prefetch the rows this many tiles ahead (0 = off)
+  int32_t loaders;              // loader lanes issuing the raw-row copies round-robin
 };
 
 struct RowsPlan {
@@ -221,16 +222,22 @@ __global__ void __launch_bounds__(kThreadsR, 1) igemm_rows_kernel(const __grid_c
 
   if (warp == kLoadWarpR) {
     // ------------------------------------------------------------ loader
-    if (lane == 0) {
-      const uint32_t b_bytes = (uint32_t)(a.R * BN * 64);
-      mbar_arrive_expect_tx(bfull, b_bytes);
-      bulk_load(smem_u32(sB), a.wrows, b_bytes, bfull);
+    // Lanes 0 .. nload-1 issue the raw-row copies of tiles k = lane, lane +
+    // nload, ...: each copy is small (the ~2 rows a tile adds) and one
+    // thread's bulk copies are served one after another, so a single loader
+    // caps the kernel at one tile per copy latency.  nload <= kStagesR keeps
+    // every stage barrier's parity wait within one phase.
+    const int nload = a.loaders < 1 ? 1 : (a.loaders > kStagesR ? kStagesR : a.loaders);
+    if (lane < nload) {
+      if (lane == 0) {
+        const uint32_t b_bytes = (uint32_t)(a.R * BN * 64);
+        mbar_arrive_expect_tx(bfull, b_bytes);
+        bulk_load(smem_u32(sB), a.wrows, b_bytes, bfull);
+      }
       RP_T0();
       TileWalk walk;
       walk.start(a, t0);
-      // L2 prefetch of the rows `a.pf` tiles ahead: each tile adds only ~2
-      // input rows (a few KB), so the few stages in flight cannot cover the
-      // HBM latency; prefetched rows arrive from L2
+      // L2 prefetch of the rows `a.pf` tiles ahead (lane 0; knob rows_pf)
       TileWalk pwalk;
       pwalk.start(a, t0);
       auto prefetch_next = [&]() {
@@ -238,11 +245,13 @@ __global__ void __launch_bounds__(kThreadsR, 1) igemm_rows_kernel(const __grid_c
         const int32_t pc = pr.new_hi - pr.new_lo + 1;
         if (pc > 0) bulk_prefetch_l2(a.t.x + ((int64_t)pr.n * a.H + pr.new_lo) * a.row_bytes, (uint32_t)(pc * a.row_bytes));
       };
-      for (int64_t k = 0; k < a.pf && k < my_tiles; ++k) prefetch_next();
+      if (lane == 0)
+        for (int64_t k = 0; k < a.pf && k < my_tiles; ++k) prefetch_next();
       for (int64_t k = 0; k < my_tiles; ++k) {
         const int s = (int)(k % kStagesR);
-        if (a.pf > 0 && k + a.pf < my_tiles) prefetch_next();
+        if (lane == 0 && a.pf > 0 && k + a.pf < my_tiles) prefetch_next();
         const TileRows tr = walk.next(a);
+        if ((int)(k % nload) != lane) continue;
         RP_ACC(1);
         if (k >= kStagesR) mbar_wait(&stage_free[s], (uint32_t)((k / kStagesR - 1) & 1));
         RP_ACC(0);
@@ -462,6 +471,7 @@ int launch_rows_ring(const ConvArgs& c, cudaStream_t st, const RowsPlan& pl, int
   }
   a.t.use_tma_y = tune(kTuneTmaStore) != 0;
   a.pf = tune(kTuneRowsPf);
+  a.loaders = tune(kTuneRowsLoaders);
   const int sms = sm_count();
   const int grid = (int)(a.total_tiles < sms ? a.total_tiles : sms);
   return launch_conv_kernel(kernel, (unsigned)grid, kThreadsR, pl.bytes, st, 1, "igemm_rows launch", tmap_y, a, pl);
