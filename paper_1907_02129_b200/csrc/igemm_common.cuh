@@ -228,7 +228,8 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
 #else
     const int nchunks = cols_left > 0 && row_valid ? (min(kColsPerWarp, cols_left) + 31) / 32 : 0;
 #endif
-    if constexpr (!kI8 && !kRowTiles && kColsPerWarp % 64 == 0) {
+    bool done_wide = false;
+    if constexpr (!kI8 && kColsPerWarp % 64 == 0) {
       if (use_tma && a.epi_wide) {
         // 64-column chunks: two TMEM loads under one wait, the 32 x 64 block
         // staged 128-byte swizzled (conflict-free row-per-lane writes) and
@@ -269,27 +270,18 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(tmap_y, sb, n, (int32_t)row0);
+            if constexpr (kRowTiles)   // (channel, pixel in the output row, output row); pixels >= Wo clipped
+              tma_store_3d(tmap_y, sb, n, rt_ox0, rt_row);
+            else
+              tma_store_2d(tmap_y, sb, n, (int32_t)row0);
             bulk_commit_group();
           }
           ++chunk_seq;
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if (tempty_remote) mbar_arrive_remote_relaxed(tempty_remote + as * 8);
-          else mbar_arrive(&tempty[as]);
-        }
-        if constexpr (kTileGroups > 1) {
-          as += kTileGroups;
-          if (as >= kAccStages) { as -= kAccStages; aphase ^= 1; }
-        } else if (++as == kAccStages) {
-          as = 0;
-          aphase ^= 1;
-        }
-        continue;
+        done_wide = true;
       }
     }
+    if (!done_wide) {
     uint32_t v[32];
     if (nchunks > 0) {
       tmem_ld_32x32b_x32(taddr + col0, v);
@@ -401,6 +393,7 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
         for (int i = 0; i < 32; ++i) v[i] = vn[i];
       }
     }
+    }   // !done_wide
     tc_fence_before();
     __syncwarp();
     if (lane == 0) {   // one arrival per epilogue warp (at the pair leader for a pair peer)

@@ -462,11 +462,15 @@ int launch_rows_ring(const ConvArgs& c, cudaStream_t st, const RowsPlan& pl, int
     if (!encode) return fail(ICV_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     const cuuint64_t dims[3] = {(cuuint64_t)c.g.K, (cuuint64_t)c.g.OW, (cuuint64_t)(c.P / c.g.OW)};
     const cuuint64_t strides[2] = {(cuuint64_t)c.g.K * 2, (cuuint64_t)(c.g.OW * c.g.K * 2)};
-    const cuuint32_t box[3] = {32, 32, 1};
+    // box: 32 channels x 32 pixels (64-byte swizzle), or for the wide
+    // epilogue 64 channels x 32 pixels (128-byte swizzle)
+    a.t.epi_wide = tune(kTuneEpiWide) != 0 && BN % 64 == 0;
+    const cuuint32_t box[3] = {a.t.epi_wide ? 64u : 32u, 32, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     CUresult cr = encode(&tmap_y, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, c.y, dims, strides, box, estr,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                         CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         a.t.epi_wide ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                         CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) return fail(ICV_ERR_CUDA, "row kernel: output tensor map");
   }
   a.t.use_tma_y = tune(kTuneTmaStore) != 0;
