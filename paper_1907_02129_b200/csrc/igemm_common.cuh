@@ -150,7 +150,7 @@ template <bool kI8, int BN, int kEpiWarps, int kAccStride, typename Sched = Stri
 __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane, uint32_t tmem_base, uint8_t* sEpi,
                                               const uint32_t* sBias, uint64_t* tfull, uint64_t* tempty,
                                               Sched sched = Sched{0}, const CUtensorMap* tmap_y = nullptr,
-                                              uint32_t tempty_remote = 0) {
+                                              uint32_t tempty_remote = 0, const int32_t* smem_sums = nullptr) {
   constexpr int kOutRowBytes = kI8 ? 32 : 64;
   constexpr int kStageRowBytes = kI8 ? 48 : 80;  // padded: row-per-lane staging writes are conflict free
   const int slot = ew & 3;
@@ -216,10 +216,14 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
     const uint32_t taddr = tmem_base + ((uint32_t)(slot * 32) << 16) + as * kAccStride + (kSubRows > 1 ? group * BN : 0);
     int32_t rowsum = 0;
     if constexpr (kI8) {
-      uint32_t rs;
-      tmem_ld_32x32b_x1(taddr + BN, rs);
-      tmem_ld_wait();
-      rowsum = (int32_t)rs;
+      if (smem_sums) {   // (row sums computed by the kernel's row-sum warps: [accumulator stage][row])
+        rowsum = smem_sums[as * kBM + slot * 32 + lane];
+      } else {
+        uint32_t rs;
+        tmem_ld_32x32b_x1(taddr + BN, rs);
+        tmem_ld_wait();
+        rowsum = (int32_t)rs;
+      }
     }
     const int cols_left = a.K - nt * BN - col0;
 #ifdef ICV_EXP_NOEPI   // experiment: release the accumulators without storing

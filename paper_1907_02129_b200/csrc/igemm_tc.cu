@@ -63,8 +63,17 @@ constexpr bool kIsDense = std::is_same<IbT, DenseA>::value;
 
 template <bool kI8, int BN, int kPair = 1, int kEpiW = kEpiWarpsS<kI8>, bool kDense = false>
 struct CfgS {
-  // B bytes per K block held by this CTA (a CTA pair splits the BN rows)
-  static constexpr int kBBytes = BN * 128 / kPair;
+  // uint8 row sums (the zero-point correction needs sum_k x[p][k] per output
+  // pixel): 16 all-ones rows sit behind the BN filter rows of every B block
+  // in smem and the MMA runs N = BN + 16 -- tcgen05 time is linear in N (72
+  // vs 64 cycles at N 144 / 128, tools/micro/mma_rate.cu), while a separate
+  // N = 16 MMA per K step costs its 45-cycle floor (107 cycles per pair).
+  // CTA pairs and BN 256 (N <= 256) keep the separate ones tile.
+  static constexpr bool kFuseOnes = kI8 && kPair == 1 && BN + 16 <= 256;
+  // bytes one K block of the filter tile occupies in smem / brings in by TMA
+  // (a CTA pair splits the BN rows)
+  static constexpr int kBLoadBytes = BN * 128 / kPair;
+  static constexpr int kBBytes = kBLoadBytes + (kFuseOnes ? 16 * 128 : 0);
   // One smem slot = one 128-byte K block of A (128 rows) and of B (BN rows).
   // A stage groups kKB slots behind one full/empty barrier pair so the MMA
   // warp pays one barrier round trip per kKB*4 MMAs.
@@ -73,16 +82,23 @@ struct CfgS {
 #endif
   // (dense A: one K block per stage -- 1x1 layers have few K blocks per
   // tile, and the stages then run straight across tile boundaries)
-  static constexpr int kKB = (kDense || BN >= 256) ? 1 : ICV_KKB;
+  // (fused ones rows: one TMA box per K block, and the larger slots would
+  // leave only two 2-block stages)
+  static constexpr int kKB = (kDense || BN >= 256 || kFuseOnes) ? 1 : ICV_KKB;
   static constexpr int kSlotBytes = kABytes + kBBytes;
 #ifndef ICV_MAX_SLOTS
 #define ICV_MAX_SLOTS 8
 #endif
   static constexpr int kMaxSlots = kDense ? 12 : ICV_MAX_SLOTS;
-  static constexpr int kOnesBytes = kI8 ? 16 * 128 : 0;
+  // BN 256 (single CTA): two 256-column accumulators fill TMEM, so the row
+  // sums are computed by four extra warps that read each full A stage from
+  // shared memory (one row per thread, dp4a) and hand the per-tile sums to
+  // the epilogue through smem ([2][128] int32 in the ones-tile region).
+  static constexpr int kSumWarps = (kI8 && !kFuseOnes && kPair == 1) ? 4 : 0;
+  static constexpr int kOnesBytes = kSumWarps ? 2 * kBM * 4 : (kI8 && !kFuseOnes) ? 16 * 128 : 0;
   // TMEM columns per accumulator stage (uint8: row sums at +BN; BN = 256
   // keeps 32 columns for them and runs one accumulator stage)
-  static constexpr int kAccStride = kI8 ? (BN == 256 ? BN + 32 : 2 * BN) : BN;
+  static constexpr int kAccStride = kI8 ? (kSumWarps ? BN : BN == 256 ? BN + 32 : 2 * BN) : BN;
   static constexpr int kAccStages = 2 * kAccStride <= 512 ? 2 : 1;
   static constexpr int kTmemNeed = kAccStages * kAccStride;
   static constexpr uint32_t kTmemCols = kTmemNeed <= 64 ? 64 : kTmemNeed <= 128 ? 128 : kTmemNeed <= 256 ? 256 : 512;
@@ -148,8 +164,12 @@ struct ClusterTiles {
   }
 };
 
+// (+ the row-sum warps of the uint8 BN 256 plan)
+template <bool kI8, int BN, int kCS, int kEpiW>
+constexpr int kThreadsK = kThreadsS<kI8, kEpiW> + 32 * CfgS<kI8, BN, kCS, kEpiW, false>::kSumWarps;
+
 template <bool kI8, int BN, typename IbT, int kCS, int kEpiW>
-__global__ void __launch_bounds__(kThreadsS<kI8, kEpiW>, 1) igemm_smem_kernel(const __grid_constant__ CUtensorMap tmap_b,
+__global__ void __launch_bounds__(kThreadsK<kI8, BN, kCS, kEpiW>, 1) igemm_smem_kernel(const __grid_constant__ CUtensorMap tmap_b,
                                                                   const __grid_constant__ CUtensorMap tmap_x,
                                                                   const __grid_constant__ CUtensorMap tmap_y,
                                                                   const TcArgs a, const PlanS pl) {
@@ -201,10 +221,10 @@ __global__ void __launch_bounds__(kThreadsS<kI8, kEpiW>, 1) igemm_smem_kernel(co
       // dense A: the issuing thread's expect_tx arrival; gather: 32 per producer
       // warp + 1 expect_tx; a pair leader also counts the peer's forwarded arrival
       mbar_init(&full[s], (dense_a ? 1 : 32 * kProdWarpsS<kI8> + 1) + (kCS == 2 && crank == 0 ? 1 : 0));
-      mbar_init(&empty[s], 1);       // tcgen05.commit (multicast to both CTAs of a pair)
+      mbar_init(&empty[s], 1 + C::kSumWarps);   // tcgen05.commit (multicast to both CTAs of a pair) + row-sum warps
     }
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&tfull[s], 1);                   // tcgen05.commit after the last K block
+      mbar_init(&tfull[s], 1 + C::kSumWarps);    // tcgen05.commit after the last K block (+ the tile's row sums)
       // one arrival per epilogue warp (of both CTAs at the pair leader)
       mbar_init(&tempty[s], (kCS == 2 && crank == 0) ? 2 * kEpiW : kEpiW);
     }
@@ -213,7 +233,15 @@ __global__ void __launch_bounds__(kThreadsS<kI8, kEpiW>, 1) igemm_smem_kernel(co
     tma_prefetch_desc(&tmap_b);
     if (dense_a) tma_prefetch_desc(&tmap_x);
   }
-  if constexpr (kI8) {
+  if constexpr (C::kFuseOnes) {
+    // 16 all-ones rows behind the filter rows of every B block (TMA writes
+    // only the first BN rows, so they stay); all-ones is swizzle-invariant
+    const int nblk = pl.res_b ? pl.res_b : pl.slots;
+    for (int i = threadIdx.x; i < nblk * 128; i += blockDim.x)
+      reinterpret_cast<uint4*>(sB + (i >> 7) * C::kBBytes + C::kBLoadBytes)[i & 127] =
+          make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
+    fence_proxy_async_smem();
+  } else if constexpr (kI8 && C::kSumWarps == 0) {
     if (threadIdx.x >= 128 && threadIdx.x < 256) {  // all-ones B tile (16 rows x 128 bytes)
       reinterpret_cast<uint4*>(sOnes)[threadIdx.x - 128] = make_uint4(0x01010101u, 0x01010101u, 0x01010101u,
                                                                       0x01010101u);
@@ -242,7 +270,7 @@ __global__ void __launch_bounds__(kThreadsS<kI8, kEpiW>, 1) igemm_smem_kernel(co
       if (pl.res_b) {
         if (warp == 0 && my_tiles0 > 0) {
           const int nt0 = (int)(sched(0) % a.n_tiles);
-          mbar_arrive_expect_tx(bres, pl.res_b * C::kBBytes);
+          mbar_arrive_expect_tx(bres, pl.res_b * C::kBLoadBytes);
           for (int kb = 0; kb < pl.res_b; ++kb)
             tma_load_3d(smem_u32(sB) + kb * C::kBBytes, &tmap_b, bres, 0, nt0 * BN, kb);
         }
@@ -250,7 +278,7 @@ __global__ void __launch_bounds__(kThreadsS<kI8, kEpiW>, 1) igemm_smem_kernel(co
         const int niss = pl.stages < kPWd ? pl.stages : kPWd;
         for (int64_t q = warp; warp < niss && q < pl.stages && q < my_tiles0 * nkb; q += niss) {
           const int nt0 = (int)(sched(q / nkb) % a.n_tiles);
-          mbar_arrive_expect_tx(&full[q], kABytes + C::kBBytes);
+          mbar_arrive_expect_tx(&full[q], kABytes + C::kBLoadBytes);
           tma_load_3d(smem_u32(sB) + (int)q * C::kBBytes, &tmap_b, &full[q], 0, nt0 * BN, (int)(q % nkb));
         }
       }
@@ -347,7 +375,7 @@ __global__ void __launch_bounds__(kThreadsS<kI8, kEpiW>, 1) igemm_smem_kernel(co
             } else if (kCS == 1 && q < kStages) {
               // (first ring pass: expect_tx and the filter block were issued before griddep_wait)
             } else {
-              mbar_arrive_expect_tx(&full[st], kABytes + C::kBBytes);
+              mbar_arrive_expect_tx(&full[st], kABytes + C::kBLoadBytes);
               // (a pair member loads its half of the BN filter rows)
               tma_load_3d(sB_u32 + st * C::kBBytes, &tmap_b, &full[st], 0, nt * BN + (int)crank * (BN / kCS), kb);
             }
@@ -403,10 +431,14 @@ __global__ void __launch_bounds__(kThreadsS<kI8, kEpiW>, 1) igemm_smem_kernel(co
                 // block past the filter is zero-filled and never multiplied),
                 // issued by the producer warps in turn
                 if (lane == 0 && warp == (stage_seq % kPW)) {
-                  mbar_arrive_expect_tx(&full[stage], C::kKB * C::kBBytes);
+#ifdef ICV_EXP_NOB   // experiment: no filter loads
+                  mbar_arrive(&full[stage]);
+#else
+                  mbar_arrive_expect_tx(&full[stage], C::kKB * C::kBLoadBytes);
                   // (a pair member loads its half of the BN filter rows)
                   tma_load_3d(sB_u32 + stage * C::kKB * C::kBBytes, &tmap_b, &full[stage], 0,
                               nt * BN + (int)crank * (BN / kCS), kb);
+#endif
                 }
                 ++stage_seq;
               }
@@ -472,7 +504,7 @@ __global__ void __launch_bounds__(kThreadsS<kI8, kEpiW>, 1) igemm_smem_kernel(co
       }
   } else if (warp == kMmaWarpS<kI8, kEpiW>) {
     // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc = make_idesc<kI8>(kBM * kCS, BN);
+    constexpr uint32_t idesc = make_idesc<kI8>(kBM * kCS, BN + (C::kFuseOnes ? 16 : 0));
     constexpr uint32_t idesc_ones = make_idesc<kI8>(kBM * kCS, 16);
     const uint64_t ones_desc = sw128_kmajor_desc(smem_u32(sOnes));
     const int stages_per_tile = (num_kb + C::kKB - 1) / C::kKB;
@@ -521,7 +553,8 @@ __global__ void __launch_bounds__(kThreadsS<kI8, kEpiW>, 1) igemm_smem_kernel(co
 #ifndef ICV_EXP_NOMMA   // experiment: fills only
                 tc_mma<kI8>(d, adesc + 2 * k, bdesc + 2 * k, idesc, acc);
 #endif
-                if constexpr (kI8) tc_mma<true>(d + BN, adesc + 2 * k, ones_desc + 2 * k, idesc_ones, acc);
+                if constexpr (kI8 && !C::kFuseOnes && !C::kSumWarps)
+                  tc_mma<true>(d + BN, adesc + 2 * k, ones_desc + 2 * k, idesc_ones, acc);
               } else {
                 tc_mma2<kI8>(d, adesc + 2 * k, bdesc + 2 * k, idesc, acc);
                 if constexpr (kI8) tc_mma2<true>(d + BN, adesc + 2 * k, ones_desc + 2 * k, idesc_ones, acc);
@@ -552,12 +585,49 @@ __global__ void __launch_bounds__(kThreadsS<kI8, kEpiW>, 1) igemm_smem_kernel(co
       g_icv_trace[blockIdx.x][36] = (unsigned long long)c_wait_tempty;
     }
 #endif
+  } else if (C::kSumWarps > 0 && warp > kMmaWarpS<kI8, kEpiW>) {
+    // ------------------------------------------------------------ row sums (uint8, BN 256)
+    // Thread r of the four warps sums row r of every A stage of the tile:
+    // the 128 bytes of the row in its swizzled order (chunk j ^ (r & 7):
+    // conflict-free across a quarter warp).  Padding taps hold the bound
+    // zero row, zero-filled channel tails add nothing -- the same bytes the
+    // MMA multiplies.  The stage is released by the MMA commit AND these
+    // warps; the sums reach the epilogue through smem under the tfull barrier.
+    static_assert(C::kSumWarps == 0 || C::kKB == 1, "row-sum warps: one K block per stage");
+    const int row = (warp - kMmaWarpS<kI8, kEpiW> - 1) * 32 + lane;
+    int32_t* sSum = reinterpret_cast<int32_t*>(sOnes);
+    const int64_t n_local = sched.count();
+    int stage = 0, as = 0;
+    uint32_t phase = 0, aphase = 0;
+    for (int64_t t = 0; t < n_local; ++t) {
+      uint32_t acc = 0;
+      for (int si = 0; si < num_kb; ++si) {
+        mbar_wait(&full[stage], phase);
+        const uint8_t* rowp = sA + stage * kABytes + row * 128;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint4 v = *reinterpret_cast<const uint4*>(rowp + ((j ^ (row & 7)) << 4));
+          acc = __dp4a(v.x, 0x01010101u, acc);
+          acc = __dp4a(v.y, 0x01010101u, acc);
+          acc = __dp4a(v.z, 0x01010101u, acc);
+          acc = __dp4a(v.w, 0x01010101u, acc);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
+      }
+      mbar_wait(&tempty[as], aphase ^ 1);   // the epilogue has read the sums of the tile two back
+      sSum[as * kBM + row] = (int32_t)acc;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tfull[as]);
+      if (++as == C::kAccStages) { as = 0; aphase ^= 1; }
+    }
   } else {
     // a pair peer releases accumulators at the leader (which issues the next MMAs)
     const uint32_t tempty_remote = (kCS == 2 && crank != 0) ? mapa_rank(smem_u32(tempty), 0) : 0u;
     epilogue_loop<kI8, BN, kEpiW, C::kAccStride, std::remove_const_t<decltype(sched)>, C::kAccStages>(
         a, warp - kProdWarpsS<kI8>, lane, tmem_base, sEpi, sBias, tfull, tempty, sched, a.use_tma_y ? &tmap_y : nullptr,
-        tempty_remote);
+        tempty_remote, C::kSumWarps ? reinterpret_cast<const int32_t*>(sOnes) : nullptr);
   }
 
   tc_fence_before();
@@ -594,10 +664,11 @@ int launch_smem_cs(const ConvArgs& c, cudaStream_t st) {
   if (c.g.N * c.g.H * c.g.W * (int64_t)c.g.C >= (int64_t(1) << 31))
     return fail(ICV_ERR_UNSUPPORTED, "tensor-core kernel: input tensors of 2^31 or more elements are not supported");
   int max_clusters = 0;
-  if (int s = kernel_setup(reinterpret_cast<const void*>(kernel), 232448, kCS, kThreadsS<kI8, kEpiW>, &max_clusters))
+  constexpr int kThreads = kThreadsK<kI8, BN, kCS, kEpiW>;
+  if (int s = kernel_setup(reinterpret_cast<const void*>(kernel), 232448, kCS, kThreads, &max_clusters))
     return s;
   CUtensorMap tmap, tmap_x;
-  if (int s = make_filter_tmap(c, BN / kCS, CfgS<kI8, BN, 1, kEpiW, kIsDense<IbT>>::kKB, &tmap)) return s;
+  if (int s = make_filter_tmap(c, BN / kCS, CfgS<kI8, BN, kCS, kEpiW, kIsDense<IbT>>::kKB, &tmap)) return s;
   TcArgs a;
   fill_tc_args(c, BN, &a);
   // dense A: 1x1 stride-1 layers with a canonical buffer (and the GEMM
@@ -635,7 +706,7 @@ int launch_smem_cs(const ConvArgs& c, cudaStream_t st) {
                     "smem %d tiles %lld n_tiles %d resident filter blocks %d\n", (int)kI8, BN, kCS, kEpiW,
             (int)kIsDense<IbT>, (long long)grid, max_clusters, pl.stages, pl.slots, pl.bytes, (long long)a.total_tiles,
             a.n_tiles, pl.res_b);
-  return launch_conv_kernel(kernel, (unsigned)grid, kThreadsS<kI8, kEpiW>, pl.bytes, st, kCS, "igemm_smem launch", tmap,
+  return launch_conv_kernel(kernel, (unsigned)grid, kThreads, pl.bytes, st, kCS, "igemm_smem launch", tmap,
                             tmap_x, tmap_y, a, pl);
 }
 

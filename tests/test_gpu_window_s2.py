@@ -175,8 +175,9 @@ def test_stride1_window_u8_zero_point_row_pairs(geom, cls, tune):
     (dict(r=3, s=3, pt=1, pl=0, pb=0, pr=1, c=64, k=512, n=2, h=9, w=11), 7, 200),
 ])
 def test_u8_gather_kernel_block_n_256(geom, zx, zw, tune):
-    """Opt-in BLOCK_N 256 of the uint8 gather kernel (one accumulator stage,
-    32 TMEM columns for the row sums): bit-exact."""
+    """Opt-in BLOCK_N 256 of the uint8 gather kernel (two 256-column
+    accumulator stages; the row sums come from the kernel's row-sum warps
+    through shared memory instead of TMEM): bit-exact."""
     tune(win=0)
     tune(u8_bn=256)
     p, shape = _params(geom)

@@ -54,6 +54,24 @@ __global__ void __launch_bounds__(128, 1) mma_rate(int iters, unsigned long long
     mbar_wait(&bar, 0);
     long long t1 = clock64();
     if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = (unsigned long long)(t1 - t0);
+  } else if (kVar == 9 && threadIdx.x == 0) {
+    // the uint8 gather kernel's pattern: one N-wide MMA + one N=16 MMA (row sums) per K step
+    constexpr uint32_t idesc = make_idesc<kI8>(128, N);
+    constexpr uint32_t idesc16 = make_idesc<kI8>(128, 16);
+    const uint64_t ad = sw128_kmajor_desc(smem_u32(sA));
+    const uint64_t bd = sw128_kmajor_desc(smem_u32(sB));
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        tc_mma<kI8>(tmem, ad + 2 * k, bd + 2 * k, idesc, (it | k) != 0);
+        tc_mma<kI8>(tmem + N, ad + 2 * k, bd + 2 * k, idesc16, (it | k) != 0);
+      }
+    }
+    tc_commit(&bar);
+    mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    if (blockIdx.x == 0) out[0] = (unsigned long long)(t1 - t0);
   } else if ((kVar < 7 || kVar == 8) && threadIdx.x == 0) {
     constexpr uint32_t idesc = make_idesc<kI8>(128, N);
     const uint64_t ad = sw128_kmajor_desc(smem_u32(sA));
@@ -123,5 +141,8 @@ int main() {
   run<false, 128, 2>(d); run<false, 128, 3>(d); run<false, 128, 7>(d); run<false, 64, 7>(d);
   run<false, 64, 0>(d); run<false, 64, 8>(d); run<false, 128, 0>(d); run<false, 128, 8>(d); run<false, 32, 0>(d);
   run<false, 32, 8>(d); run<true, 64, 0>(d); run<true, 128, 0>(d); run<true, 256, 0>(d);
+  // uint8 row-sum options: a separate N=16 MMA per K step vs ones rows fused into the filter tile (N + 16)
+  run<true, 16, 0>(d); run<true, 32, 0>(d); run<true, 144, 0>(d); run<true, 160, 0>(d); run<true, 192, 0>(d);
+  run<true, 128, 9>(d); run<true, 240, 0>(d); run<false, 144, 0>(d); run<false, 256, 0>(d);
   return 0;
 }

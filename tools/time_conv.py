@@ -11,6 +11,10 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 import paper_1907_02129_b200 as icv  # noqa: E402
 
+# plan knobs for the run: ICV_KNOBS="cluster=2,u8_bn=256"
+for _kv in filter(None, os.environ.get("ICV_KNOBS", "").split(",")):
+    icv._lib.set_tuning(_kv.split("=")[0], int(_kv.split("=")[1]))
+
 
 def main():
     from paper_1907_02129_b200.workloads import CONFIGS
