@@ -43,7 +43,7 @@ enum TuneKey {
   kTuneTmaStore,         // 1: TMA tile stores in the epilogue, 0: thread stores
   kTuneRowsRp,           // row kernel: output rows per tile (1, or 2 = opt-in)
   kTuneDenseA,           // 1: 1x1 stride-1 layers load A as dense TMA boxes, 0: IB gathers
-  kTuneDenseCs,          // dense A: 2 = CTA pairs (M = 256), 1 = single CTAs
+  kTuneDenseCs,          // dense A on CTA pairs (M = 256): 0 = auto (long K loops), 1 = never, 2 = always
   kTunePdl,              // 1: persistent conv kernels use programmatic dependent launch
   kTuneDensePf,          // dense A: L2 bulk prefetch of the A rows this many tiles ahead (0 = off)
   kTuneRowsPf,           // row kernel: L2 bulk prefetch of the input rows this many tiles ahead (0 = off)

@@ -220,7 +220,8 @@ __global__ void __launch_bounds__(kThreadsK<kI8, BN, kCS, kEpiW>, 1) igemm_smem_
       // cp.async path: 128 producer arrivals + 1 expect_tx (+ 1 forwarded from the peer, pair leader)
       // dense A: the issuing thread's expect_tx arrival; gather: 32 per producer
       // warp + 1 expect_tx; a pair leader also counts the peer's forwarded arrival
-      mbar_init(&full[s], (dense_a ? 1 : 32 * kProdWarpsS<kI8> + 1) + (kCS == 2 && crank == 0 ? 1 : 0));
+      // (dense pairs: both CTAs' TMA loads complete on the leader's barrier, armed by the leader's issuer)
+      mbar_init(&full[s], (dense_a ? 1 : 32 * kProdWarpsS<kI8> + 1) + (kCS == 2 && crank == 0 && !dense_a ? 1 : 0));
       mbar_init(&empty[s], 1 + C::kSumWarps);   // tcgen05.commit (multicast to both CTAs of a pair) + row-sum warps
     }
     for (int s = 0; s < 2; ++s) {
@@ -374,12 +375,25 @@ __global__ void __launch_bounds__(kThreadsK<kI8, BN, kCS, kEpiW>, 1) igemm_smem_
               mbar_arrive_expect_tx(&full[st], kABytes);
             } else if (kCS == 1 && q < kStages) {
               // (first ring pass: expect_tx and the filter block were issued before griddep_wait)
+            } else if constexpr (kCS == 2) {
+              // CTA pair: each member loads its own 128 A rows and its half of
+              // the BN filter rows into its own smem; every load completes on
+              // the LEADER's full barrier (TMA .cta_group::2), which the
+              // leader's issuer arms with the bytes of both members -- no
+              // forwarding hop.  (A member's complete_tx may precede the arming:
+              // the phase cannot complete before the leader's arrival.)
+              if (crank == 0) mbar_arrive_expect_tx(&full[st], 2 * (kABytes + C::kBLoadBytes));
+              tma_load_3d_cg2(sB_u32 + st * C::kBBytes, &tmap_b, mapa_rank(smem_u32(&full[st]), 0), 0,
+                              nt * BN + (int)crank * (BN / kCS), kb);
             } else {
               mbar_arrive_expect_tx(&full[st], kABytes + C::kBLoadBytes);
-              // (a pair member loads its half of the BN filter rows)
-              tma_load_3d(sB_u32 + st * C::kBBytes, &tmap_b, &full[st], 0, nt * BN + (int)crank * (BN / kCS), kb);
+              tma_load_3d(sB_u32 + st * C::kBBytes, &tmap_b, &full[st], 0, nt * BN, kb);
             }
-            tma_load_2d(sA_u32 + st * kABytes, &tmap_x, &full[st], kb * a.cblock_elems, (int32_t)(mt * kBM));
+            if constexpr (kCS == 2)
+              tma_load_2d_cg2(sA_u32 + st * kABytes, &tmap_x, mapa_rank(smem_u32(&full[st]), 0), kb * a.cblock_elems,
+                              (int32_t)(mt * kBM));
+            else
+              tma_load_2d(sA_u32 + st * kABytes, &tmap_x, &full[st], kb * a.cblock_elems, (int32_t)(mt * kBM));
 #ifdef ICV_TRACE
             if (k == (my_tiles > 1 ? 1 : 0) && kb < 16) TRACE(96 + kb);   // stage issued
 #endif
@@ -492,7 +506,7 @@ __global__ void __launch_bounds__(kThreadsK<kI8, BN, kCS, kEpiW>, 1) igemm_smem_
     // The leader's MMAs read this CTA's stages too: once a stage is full here
     // (own gathers + own filter half), tell the leader's full barrier.
     const int stages_per_tile = (num_kb + C::kKB - 1) / C::kKB;
-    const int64_t n_local = sched.count();
+    const int64_t n_local = dense_a ? 0 : sched.count();   // (dense A: the member's loads signal the leader directly)
     int stage = 0;
     uint32_t phase = 0;
     for (int64_t t = 0; t < n_local; ++t)
@@ -713,13 +727,28 @@ int launch_smem_cs(const ConvArgs& c, cudaStream_t st) {
 // CTA pairs (cta_group::2, M = 256): tuning knob "cluster" = 2 (see the kernel).
 bool use_clusters() { return tune(kTuneCluster) == 2; }
 
+// Dense-A layers on CTA pairs (knob "dense_cs": 0 auto, 1 never, 2 always).
+// A pair member streams its own A rows and HALF of every filter block, so the
+// L2 -> SM bytes per tile drop by a third at BN 256.  That pays once the K loop
+// is long enough for the filter re-stream to dominate the fill (ResNet-50,
+// N = 256, single CTA -> pair: 512->256 at 28x28 59.5 -> 53.1 us, 1024->512 at
+// 14x14 53.2 -> 45.9, 2048->512 at 7x7 37.0 -> 32.9, 256->1024 39.2 -> 36.9 us)
+// and loses on short K loops (64->64 37.7 -> 45.1, 128->512 53.3 -> 56.4 us):
+// auto takes pairs from four 128-byte channel blocks up.
+bool dense_pair_wanted(const ConvArgs& c) {
+  const int mode = tune(kTuneDenseCs);
+  if (mode == 2) return true;
+  if (mode == 1) return false;
+  return c.L.family == kFamTcBf16 && c.L.cblocks >= 4;
+}
+
 template <bool kI8, int BN, typename IbT>
 int launch_smem(const ConvArgs& c, cudaStream_t st) {
   if (use_clusters()) return launch_smem_cs<kI8, BN, IbT, 2, kEpiWarpsS<kI8>>(c, st);
   if (tune(kTuneDenseA) && dense_a_eligible(c)) {
     PlanS pl;
     const bool wide_out = !kI8 && (int64_t)c.g.K >= 4 * (int64_t)c.g.C;
-    if (tune(kTuneDenseCs) == 2) {
+    if (dense_pair_wanted(c)) {
       // CTA pairs (M = 256): each SM streams its own A rows and half of the
       // filter block, so the L2 -> SM bytes per MMA drop by a third at BN 256
       if (wide_out && plan_smem<kI8, BN, DenseA, 2, 8>(1, c.L.n_pad, &pl))
@@ -939,7 +968,7 @@ const char* tc_kernel_name(const ConvArgs& c) {
   const bool i8 = c.L.family == kFamTcU8;
   if (win_kernel_eligible(c)) return i8 ? "icv_igemm_win<u8>" : "icv_igemm_win<bf16>";
   if (dense_a_eligible(c) && tune(kTuneDenseA) && !use_clusters()) {
-    if (tune(kTuneDenseCs) == 2) return i8 ? "icv_igemm_smem<u8,dense,pair>" : "icv_igemm_smem<bf16,dense,pair>";
+    if (dense_pair_wanted(c)) return i8 ? "icv_igemm_smem<u8,dense,pair>" : "icv_igemm_smem<bf16,dense,pair>";
     return i8 ? "icv_igemm_smem<u8,dense>" : "icv_igemm_smem<bf16,dense>";
   }
   return i8 ? "icv_igemm_smem<u8>" : "icv_igemm_smem<bf16>";

@@ -619,6 +619,7 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
               mbar_wait(&bfull[bslot], pl.resident ? 0u : bphl);
 #ifdef ICV_TRACE
               c_wait_full += clock64() - c1;
+              if (uk == 1 && st == 0 && ti - i_beg < 12) TRACE(96 + ti - i_beg);    // tap's filter block seen
 #endif
               tc_fence_after();
             }
@@ -657,6 +658,9 @@ __global__ void __launch_bounds__(kThreadsW, 1) igemm_win_kernel(const __grid_co
               }
             }
             if (++bsl == pl.bslots) { bsl = 0; bphl ^= 1; }
+#ifdef ICV_TRACE
+            if (uk == 1 && st == 0 && ti - i_beg < 12) TRACE(108 + ti - i_beg);   // tap's MMAs and commits issued
+#endif
           }
         }
         __syncwarp();

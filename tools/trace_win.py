@@ -16,6 +16,10 @@ import paper_1907_02129_b200 as icv  # noqa: E402
 from paper_1907_02129_b200 import _lib as L  # noqa: E402
 from paper_1907_02129_b200 import workloads as wl  # noqa: E402
 
+# plan knobs for the run: ICV_KNOBS="win_mt=1,win_debug=1"
+for _kv in filter(None, os.environ.get("ICV_KNOBS", "").split(",")):
+    L.set_tuning(_kv.split("=")[0], int(_kv.split("=")[1]))
+
 # ResNet-50 layers by name (not BASELINE configs): trace_win.py r50:s1b1_3x3
 for _name, _shape, _params in wl.resnet50_layers(256):
     wl.CONFIGS["r50:" + _name] = wl.ConvWorkload("r50_" + _name, "bf16", _shape, _params)
@@ -86,7 +90,9 @@ def windows(name="cfg2"):
     tr = buf[:148].astype(np.int64)
     ok = tr[:, 61] > 0
     ghz = np.median((tr[ok, 60] - tr[ok, 62]) / (tr[ok, 61] - tr[ok, 0]))
-    print(f"clock {ghz:.3f} GHz, span {(tr[ok, 61].max() - tr[ok, 0].min()) * ghz:.0f} cycles")
+    print(f"clock64 rate {ghz:.3f} GHz (undercounts: the counter stalls while every warp of the SM sleeps), "
+          f"span {(tr[ok, 61].max() - tr[ok, 0].min()) / 1e3:.2f} us; times below in ns after CTA entry")
+    ghz = 1.0
     for cta in (0, 2, 72):
         r = tr[cta]
         t0 = r[0]
@@ -97,6 +103,9 @@ def windows(name="cfg2"):
             iss, full, done = ((r[64 + k] - t0) * ghz, (r[72 + k] - t0) * ghz, (r[80 + k] - t0) * ghz)
             cells.append(f"u{k // 2}c{k % 2}: issue {iss:.0f} full {full:.0f} (+{full - iss:.0f}) mma_issued {done:.0f}")
         print(f"cta {cta}: " + " | ".join(cells))
+        taps = [f"t{k}: +{r[96 + k] - t0} -> +{r[108 + k] - t0}" for k in range(12) if r[96 + k] or r[108 + k]]
+        if taps:
+            print(f"   unit 1, stage 0, per tap (filter block seen -> MMAs + commits issued, ns): " + ", ".join(taps))
 
 
 if __name__ == "__main__" and len(sys.argv) > 2 and sys.argv[2] == "windows":
