@@ -575,9 +575,11 @@ def dominant_roofline(rows: list[dict], peaks: dict) -> dict:
     the largest share of the step's conv time; achieved = its algorithmic
     bytes (HBM-bound class) or FLOPs (tensor-bound class) summed over its
     launches / its summed launch time."""
+    # (one class per kernel family: the dense-A kernel's single-CTA and CTA-pair
+    # plans are the same __global__ template, like its BLOCK_N variants)
     groups: dict[tuple[str, str], list[dict]] = {}
     for r in rows:
-        groups.setdefault((r["kernel"], r["bound"]), []).append(r)
+        groups.setdefault((r["kernel"].replace(",pair>", ">"), r["bound"]), []).append(r)
     total_us = sum(r["us"] for r in rows)
     (kern, bound), members = max(groups.items(), key=lambda kv: sum(r["us"] for r in kv[1]))
     us = sum(r["us"] for r in members)
@@ -591,6 +593,7 @@ def dominant_roofline(rows: list[dict], peaks: dict) -> dict:
     return {"bound": bound, "achieved": round(achieved, 2), "peak": peak, "unit": unit,
             "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": kern, "launches_per_step": len(members),
             "share_of_conv_time": round(us / total_us, 3),
+            "plans": {k: sum(1 for r in members if r["kernel"] == k) for k in sorted({r["kernel"] for r in members})},
             "layers": [r["layer"] for r in members],
             "per_launch": "algorithmic bytes (input + filter + output) or FLOPs of each launch / its CUDA-event time, "
                           "summed over the class",

@@ -65,6 +65,20 @@ def test_dense_a_matches_oracle_and_gather(geom, per_image, index_dtype, cs, tun
     assert y.tobytes() == y_gather.tobytes()
 
 
+def test_dense_a_pairs_chosen_by_k_loop_length():
+    """Default plan (dense_cs = 0): CTA pairs from four 128-byte channel
+    blocks up (the filter re-stream dominates the fill), single CTAs below;
+    both equal the gather kernel bit for bit."""
+    for c, want in ((64, "icv_igemm_smem<bf16,dense>"), (128, "icv_igemm_smem<bf16,dense>"),
+                    (256, "icv_igemm_smem<bf16,dense,pair>"), (512, "icv_igemm_smem<bf16,dense,pair>")):
+        g = dict(c=c, k=128, n=3, h=14, w=14)
+        p, shape, xh, wh, bias, x, pf, zero, ib, tile, o = _case(g, True, torch.int64)
+        assert L.kernel_name(p, shape, torch.bfloat16) == want
+        y = icv.indirect_conv(x, pf, ib, p, tile).numpy()
+        y_gather = icv.indirect_conv(x, pf, ib, p, tile, algorithm="gather").numpy()
+        assert y.tobytes() == y_gather.tobytes()
+
+
 def test_dense_a_offset_input_view():
     """An input that starts 16 bytes into its allocation still takes the TMA
     path (16-byte aligned base); the result equals the gather kernel's."""
