@@ -65,8 +65,8 @@ int kernel_setup(const void* fn, int smem_bytes, int cluster, int threads, int* 
 static const char* const kTuneNames[kTuneCount] = {
     "win", "win_min_useful_pm", "win_s2", "win_u8", "win_ws", "win_tma", "win_u8_cls", "win_split",
     "win_debug", "win_cs", "win_mt", "win_res", "win_u8_bn", "cluster", "u8_bn", "tma_store", "rows_rp",
-    "dense_a", "dense_cs", "pdl", "dense_pf", "rows_pf", "dense_resb", "epi_wide", "small_tile_bn", "win_filt_lanes", "rows_loaders"};
-static const int kTuneDefaults[kTuneCount] = {-1, 700, 0, 0, 0, 1, 1, 1, 0, 2, 2, 1, 256, 1, 0, 1, 1, 1, 0, 1, 0, 0, 128, 1, 0, 1, 1};
+    "dense_a", "dense_cs", "pdl", "dense_pf", "rows_pf", "dense_resb", "epi_wide", "small_tile_bn", "win_filt_lanes", "rows_loaders", "im2col_a"};
+static const int kTuneDefaults[kTuneCount] = {-1, 700, 0, 0, 0, 1, 1, 1, 0, 2, 2, 1, 256, 1, 0, 1, 1, 1, 0, 1, 0, 0, 128, 1, 0, 1, 1, 1};
 static std::atomic<int> g_tune[kTuneCount];
 static std::once_flag g_tune_once;
 static void tune_init() {

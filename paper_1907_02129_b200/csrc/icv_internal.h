@@ -52,6 +52,7 @@ enum TuneKey {
   kTuneSmallTileBn,      // bf16 gather/dense: BLOCK_N 128 instead of 256 when tiles < this % of the SM count (0 = never)
   kTuneWinFiltLanes,     // window kernel: filter-block issuing lanes per filter producer warp
   kTuneRowsLoaders,      // row kernel: lanes issuing the raw-row bulk copies
+  kTuneIm2colA,          // im2col TMA A tiles: 0 off, 1 auto (long K loops; over the window kernel on small images), 2 wherever eligible
   kTuneCount
 };
 int tune(TuneKey k);
@@ -159,6 +160,8 @@ int launch_conv_core(const ConvArgs& a, cudaStream_t st);       // bf16 / u8, an
 int launch_conv_tc(const ConvArgs& a, cudaStream_t st);         // bf16 / u8 tcgen05
 bool win_kernel_eligible(const ConvArgs& a);                   // stride-1 window kernel applies
 bool dense_a_eligible(const ConvArgs& a);                      // 1x1 stride-1: A is the dense input matrix
+bool im2col_a_eligible(const ConvArgs& a);                     // canonical buffer, zero zero row: A tiles by im2col TMA
+int tma_a_mode(const ConvArgs& a);                             // 0 IB gather, 1 dense TMA boxes, 2 im2col TMA
 int launch_conv_win(const ConvArgs& a, cudaStream_t st);        // bf16 / u8 tcgen05, sliding window A
 const char* tc_kernel_name(const ConvArgs& a);
 int launch_conv_stem(const ConvArgs& a, cudaStream_t st);   // channel-poor bf16 (tcgen05)

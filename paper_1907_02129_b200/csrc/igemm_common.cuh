@@ -64,6 +64,8 @@ struct TcArgs {
   int32_t dense_pf;          // dense A: L2-prefetch the A rows this many local tiles ahead (0 = off)
   int32_t epi_wide;          // bf16 epilogue: 64-column chunks, 128-byte-swizzled staging, 64 x 32 TMA boxes
   int64_t x_rows;            // dense A: pixel rows of the bound input
+  // im2col A (use_tma_x == 2): output width, kernel width, strides, dilations, leading pads
+  int32_t im_ow, im_s, im_sx, im_sy, im_dx, im_dy, im_pl, im_pt;
 };
 
 // Where the references of output pixel p = tile_m*128 + row live: entry of
@@ -445,6 +447,7 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
 PFN_cuTensorMapEncodeTiled_v12000 get_tensor_map_encoder();
 int make_filter_tmap(const ConvArgs& c, int block_n, int depth, CUtensorMap* tmap);
 int make_input_tmap(const ConvArgs& c, CUtensorMap* tmap);
+int make_input_tmap_im2col(const ConvArgs& c, CUtensorMap* tmap);
 int make_output_tmap(const ConvArgs& c, CUtensorMap* tmap, bool wide = false);
 void fill_tc_args(const ConvArgs& c, int block_n, TcArgs* a);
 int sm_count();

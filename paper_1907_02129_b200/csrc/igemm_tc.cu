@@ -362,6 +362,18 @@ __global__ void __launch_bounds__(kThreadsK<kI8, BN, kCS, kEpiW>, 1) igemm_smem_
             }
           }
         }
+        // im2col A (a.use_tma_x == 2): base input position (tap 0) of the tile's
+        // first output pixel; the TMA unit walks the 128 output pixels itself
+        int32_t im_w0 = 0, im_h0 = 0, im_n0 = 0;
+        if (a.use_tma_x == 2 && lane == 0) {
+          const int64_t p0 = mt * kBM;
+          const int64_t n0 = p0 / a.ohw;
+          const int32_t r0 = (int32_t)(p0 - n0 * a.ohw);
+          const int32_t oy0 = r0 / a.im_ow;
+          im_n0 = (int32_t)n0;
+          im_h0 = oy0 * a.im_sy - a.im_pt;
+          im_w0 = (r0 - oy0 * a.im_ow) * a.im_sx - a.im_pl;
+        }
         const int64_t q0 = k * num_kb;
         for (int kb = 0; kb < num_kb; ++kb) {
           const int64_t q = q0 + kb;
@@ -389,11 +401,23 @@ __global__ void __launch_bounds__(kThreadsK<kI8, BN, kCS, kEpiW>, 1) igemm_smem_
               mbar_arrive_expect_tx(&full[st], kABytes + C::kBLoadBytes);
               tma_load_3d(sB_u32 + st * C::kBBytes, &tmap_b, &full[st], 0, nt * BN, kb);
             }
-            if constexpr (kCS == 2)
+            if (a.use_tma_x == 2) {
+              // K block kb = (tap e, channel block cb), cb fastest (the packed filter's order)
+              const int e = kb / a.cblocks, cb = kb - e * a.cblocks;
+              const int ky = e / a.im_s, kx = e - ky * a.im_s;
+              const uint16_t ow_ = (uint16_t)(kx * a.im_dx), oh_ = (uint16_t)(ky * a.im_dy);
+              if constexpr (kCS == 2)
+                tma_load_im2col_4d_cg2(sA_u32 + st * kABytes, &tmap_x, mapa_rank(smem_u32(&full[st]), 0),
+                                       cb * a.cblock_elems, im_w0, im_h0, im_n0, ow_, oh_);
+              else
+                tma_load_im2col_4d(sA_u32 + st * kABytes, &tmap_x, &full[st], cb * a.cblock_elems, im_w0, im_h0, im_n0,
+                                   ow_, oh_);
+            } else if constexpr (kCS == 2) {
               tma_load_2d_cg2(sA_u32 + st * kABytes, &tmap_x, mapa_rank(smem_u32(&full[st]), 0), kb * a.cblock_elems,
                               (int32_t)(mt * kBM));
-            else
+            } else {
               tma_load_2d(sA_u32 + st * kABytes, &tmap_x, &full[st], kb * a.cblock_elems, (int32_t)(mt * kBM));
+            }
 #ifdef ICV_TRACE
             if (k == (my_tiles > 1 ? 1 : 0) && kb < 16) TRACE(96 + kb);   // stage issued
 #endif
@@ -666,7 +690,7 @@ int launch_smem_cs(const ConvArgs& c, cudaStream_t st) {
   int grid_mult = 1;
   if constexpr (kIsDense<IbT> && kCS == 1) {
     using Cd = CfgS<kI8, BN, 1, kEpiW, true>;
-    const int kbs = c.L.cblocks;   // K blocks per tile (R = S = 1)
+    const int kbs = c.g.RS() * c.L.cblocks;   // K blocks per tile
     const int n_tiles = c.L.n_pad / BN;
     PlanS pr;
     if (tune(kTuneDenseResB) > 0 && kbs * Cd::kBBytes <= tune(kTuneDenseResB) * 1024 && n_tiles <= 8 &&
@@ -689,8 +713,15 @@ int launch_smem_cs(const ConvArgs& c, cudaStream_t st) {
   // baseline's patch matrix) load the A tile as TMA boxes of consecutive rows
   a.use_tma_x = 0;
   if constexpr (kIsDense<IbT>) {   // (single CTAs and pairs alike: each CTA loads its own 128 rows)
-    if (int s = make_input_tmap(c, &tmap_x)) return fail(s, "dense-A input tensor map");
-    a.use_tma_x = 1;
+    const int mode = tma_a_mode(c);
+    if (mode == 2) {
+      if (int s = make_input_tmap_im2col(c, &tmap_x)) return fail(s, "im2col input tensor map");
+      a.im_ow = (int32_t)c.g.OW; a.im_s = c.g.S; a.im_sx = c.g.SX; a.im_sy = c.g.SY;
+      a.im_dx = c.g.DX; a.im_dy = c.g.DY; a.im_pl = c.g.PL; a.im_pt = c.g.PT;
+    } else if (int s = make_input_tmap(c, &tmap_x)) {
+      return fail(s, "dense-A input tensor map");
+    }
+    a.use_tma_x = mode == 2 ? 2 : 1;
     a.dense_pf = tune(kTuneDensePf);
     a.x_rows = c.g.N * c.g.H * c.g.W;
   } else {
@@ -739,13 +770,14 @@ bool dense_pair_wanted(const ConvArgs& c) {
   const int mode = tune(kTuneDenseCs);
   if (mode == 2) return true;
   if (mode == 1) return false;
-  return c.L.family == kFamTcBf16 && c.L.cblocks >= 4;
+  return c.L.family == kFamTcBf16 && c.g.RS() * c.L.cblocks >= 4;
 }
+
 
 template <bool kI8, int BN, typename IbT>
 int launch_smem(const ConvArgs& c, cudaStream_t st) {
   if (use_clusters()) return launch_smem_cs<kI8, BN, IbT, 2, kEpiWarpsS<kI8>>(c, st);
-  if (tune(kTuneDenseA) && dense_a_eligible(c)) {
+  if (tma_a_mode(c)) {
     PlanS pl;
     const bool wide_out = !kI8 && (int64_t)c.g.K >= 4 * (int64_t)c.g.C;
     if (dense_pair_wanted(c)) {
@@ -873,6 +905,22 @@ int make_output_tmap(const ConvArgs& c, CUtensorMap* tmap, bool wide) {
 // A 1x1, stride-1, unpadded layer over a canonical buffer reads pixel row p
 // for output pixel p (indirect.py:112-125 with R = S = 1), so its A operand
 // is the dense [pixels][C] input matrix.
+// im2col TMA A tiles (tma_a_mode 2).  The buffer must be canonical and the
+// zero row all zeros (padding = out-of-bounds zero fill); bf16 with whole
+// 128-byte channel blocks; corners / offsets inside the TMA encoding's 8-bit
+// fields (two spatial dimensions).
+bool im2col_a_eligible(const ConvArgs& c) {
+  const Geom& g = c.g;
+  if (c.prefer_gather || !c.ib_canonical || !c.zero_known) return false;
+  if (c.L.family != kFamTcBf16) return false;
+  if ((reinterpret_cast<uintptr_t>(c.x) & 15) != 0 || (g.C * 2) % 128 != 0) return false;
+  const int uw = g.PR - (g.S - 1) * g.DX, uh = g.PB - (g.R - 1) * g.DY;
+  if (g.PL > 128 || g.PT > 128 || uw < -128 || uw > 127 || uh < -128 || uh > 127) return false;
+  if ((g.S - 1) * g.DX >= 255 || (g.R - 1) * g.DY >= 255) return false;
+  if (g.SX > 8 || g.SY > 8) return false;   // (traversal strides: 3-bit fields)
+  return g.N * g.H * g.W < (int64_t(1) << 31) && c.P < (int64_t(1) << 31);
+}
+
 bool dense_a_eligible(const ConvArgs& c) {
   const Geom& g = c.g;
   if (c.prefer_gather || !c.ib_canonical) return false;
@@ -880,6 +928,24 @@ bool dense_a_eligible(const ConvArgs& c) {
   const int eb = c.L.family == kFamTcU8 ? 1 : 2;
   if ((reinterpret_cast<uintptr_t>(c.x) & 15) != 0 || (g.C * eb) % 16 != 0) return false;
   return g.N * g.H * g.W < (int64_t(1) << 31);
+}
+
+// How the A tile can be brought in by TMA instead of the IB gather: 1 = dense
+// (1x1 stride-1 unpadded: 128 consecutive pixel rows), 2 = im2col TMA (any
+// kernel size / stride / dilation / padding over a canonical buffer with an
+// all-zero zero row: the tile's references are a function of the geometry and
+// the TMA unit generates them itself), 0 = neither.
+int tma_a_mode(const ConvArgs& c) {
+  if (tune(kTuneDenseA) && dense_a_eligible(c)) return 1;
+  // im2col re-reads every input pixel once per tap that uses it, like the
+  // gather, but at TMA rates and on CTA pairs; measured against the IB-gather
+  // kernel (ResNet-50, N = 256, us): 512 ch 3x3/2 75.7 -> 57.3, 256 ch 3x3/2
+  // 55.3 -> 51.1, the 1x1/2 projections 71.7 -> 65.5, 55.3 -> 52.1, 51.3 ->
+  // 49.2, but 128 ch 3x3/2 77.9 -> 80.0: auto takes it from four channel
+  // blocks up (knob im2col_a: 0 off, 1 auto, 2 wherever eligible).
+  const int mode = tune(kTuneIm2colA);
+  if (mode && im2col_a_eligible(c) && (mode == 2 || c.L.cblocks >= 4)) return 2;
+  return 0;
 }
 
 // 2-D view of the bound input for dense-A TMA loads: rows = N*H*W pixels,
@@ -902,6 +968,45 @@ int make_input_tmap(const ConvArgs& c, CUtensorMap* tmap) {
                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return cr == CUDA_SUCCESS ? ICV_OK : ICV_ERR_CUDA;
+}
+
+// 4-D NHWC im2col map of the bound input (cuTensorMapEncodeIm2col): bounding
+// box corners from the padding and the kernel extent, traversal strides = the
+// convolution strides, 128 output pixels x one 128-byte channel block per
+// load, 128-byte swizzle (the A tile's canonical K-major layout).
+int make_input_tmap_im2col(const ConvArgs& c, CUtensorMap* tmap) {
+  typedef CUresult (*EncodeIm2col)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t, const cuuint32_t*,
+                                   CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                   CUtensorMapFloatOOBfill);
+  static EncodeIm2col fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeIm2col>(p);
+  });
+  if (!fn) return ICV_ERR_CUDA;
+  const Geom& g = c.g;
+  const cuuint64_t eb = 2;
+  const cuuint64_t dims[4] = {(cuuint64_t)g.C, (cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)g.N};
+  const cuuint64_t strides[3] = {(cuuint64_t)g.C * eb, (cuuint64_t)g.W * g.C * eb, (cuuint64_t)g.H * g.W * g.C * eb};
+  const int lower[2] = {-g.PL, -g.PT};
+  const int upper[2] = {g.PR - (g.S - 1) * g.DX, g.PB - (g.R - 1) * g.DY};
+  const cuuint32_t estr[4] = {1, (cuuint32_t)g.SX, (cuuint32_t)g.SY, 1};
+  CUresult cr = fn(tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(c.x), dims, strides, lower, upper,
+                   (cuuint32_t)(128 / eb), (cuuint32_t)kBM, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return ICV_ERR_CUDA;
+  // drivers up to 13.1 encode im2col maps of tensors under 128 KB with a bit
+  // the hardware rejects (the workaround CUTLASS applies, copy_traits_sm90_im2col.hpp)
+  int drv = 0;
+  if (cudaDriverGetVersion(&drv) == cudaSuccess && drv <= 13010 &&
+      (uint64_t)g.N * g.H * g.W * g.C * eb < 131072)
+    reinterpret_cast<uint64_t*>(tmap)[1] &= ~(1ull << 21);
+  return ICV_OK;
 }
 
 void fill_tc_args(const ConvArgs& c, int block_n, TcArgs* a) {
@@ -957,17 +1062,31 @@ bool tc_kernel_available(const ConvArgs& c) {
   return bn == 64 ? smem_plan_ok<false, 64>(c) : bn == 128 ? smem_plan_ok<false, 128>(c) : smem_plan_ok<false, 256>(c);
 }
 
+// The im2col TMA kernel instead of the window kernel: on small images with
+// many channels the window kernel's virtual grid computes many junk pixels and
+// re-streams a large filter per unit (ResNet-50 256 ch 14x14 3x3: window 58.4,
+// im2col pairs 49.2 us; 512 ch 7x7: 58.4 vs 57.4), while with few channels or
+// large images reading each input pixel once wins (128 ch 28x28: 54.3 vs
+// 75.8 us; cfg3b 62.4 vs 63.5).  Auto: four channel blocks up and output rows
+// of at most 16 pixels; knob im2col_a = 2: wherever eligible (A/B).
+static bool im2col_over_window(const ConvArgs& c) {
+  if (tma_a_mode(c) != 2) return false;
+  if (tune(kTuneIm2colA) == 2) return true;
+  return tune(kTuneWin) != 1 && c.g.OW <= 16;   // (win = 1 forces the window kernel)
+}
+
 int launch_conv_tc(const ConvArgs& c, cudaStream_t st) {
   if (c.L.n_pad > kMaxBias) return fail(ICV_ERR_UNSUPPORTED, "more than 2048 output channels");
-  if (win_kernel_eligible(c)) return launch_conv_win(c, st);
+  if (win_kernel_eligible(c) && !im2col_over_window(c)) return launch_conv_win(c, st);
   if (c.ib_is_i32) return dispatch_smem<int32_t>(c, st);
   return dispatch_smem<int64_t>(c, st);
 }
 
 const char* tc_kernel_name(const ConvArgs& c) {
   const bool i8 = c.L.family == kFamTcU8;
-  if (win_kernel_eligible(c)) return i8 ? "icv_igemm_win<u8>" : "icv_igemm_win<bf16>";
-  if (dense_a_eligible(c) && tune(kTuneDenseA) && !use_clusters()) {
+  if (win_kernel_eligible(c) && !im2col_over_window(c)) return i8 ? "icv_igemm_win<u8>" : "icv_igemm_win<bf16>";
+  if (const int mode = use_clusters() ? 0 : tma_a_mode(c)) {
+    if (mode == 2) return dense_pair_wanted(c) ? "icv_igemm_smem<bf16,im2col,pair>" : "icv_igemm_smem<bf16,im2col>";
     if (dense_pair_wanted(c)) return i8 ? "icv_igemm_smem<u8,dense,pair>" : "icv_igemm_smem<bf16,dense,pair>";
     return i8 ? "icv_igemm_smem<u8,dense>" : "icv_igemm_smem<bf16,dense>";
   }

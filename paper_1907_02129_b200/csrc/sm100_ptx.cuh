@@ -159,6 +159,34 @@ __device__ __forceinline__ void tma_load_4d_cg2(uint32_t dst, const CUtensorMap*
       : "memory");
 }
 
+// im2col tile load (4-D NHWC map made by cuTensorMapEncodeIm2col): starting
+// at base input position (w, h) of image n -- the tap-0 position of the first
+// output pixel -- the TMA unit walks `pixelsPerColumn` OUTPUT pixels (x fastest,
+// wrapping over rows and images by the map's traversal strides and bounding
+// box) and fetches, for each, `channelsPerPixel` channels from c on of the
+// input pixel at that base + (off_w, off_h); positions outside the image are
+// zero-filled.  One 128-pixel x 128-byte swizzled A tile per instruction.
+__device__ __forceinline__ void tma_load_im2col_4d(uint32_t dst, const CUtensorMap* m, uint64_t* bar, int32_t c,
+                                                   int32_t w, int32_t h, int32_t n, uint16_t off_w, uint16_t off_h) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n), "h"(off_w),
+        "h"(off_h)
+      : "memory");
+}
+// (CTA pair: completion on `bar_cluster`, e.g. the leader's barrier)
+__device__ __forceinline__ void tma_load_im2col_4d_cg2(uint32_t dst, const CUtensorMap* m, uint32_t bar_cluster,
+                                                       int32_t c, int32_t w, int32_t h, int32_t n, uint16_t off_w,
+                                                       uint16_t off_h) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.im2col.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(c), "r"(w), "r"(h), "r"(n), "h"(off_w),
+        "h"(off_h)
+      : "memory");
+}
+
 // 3-D tile load delivered to the same smem offset (and mbarrier) of every
 // CTA in `mask`.
 __device__ __forceinline__ void tma_load_3d_mc(uint32_t dst, const CUtensorMap* m, uint64_t* bar, int32_t c0,
