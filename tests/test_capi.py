@@ -70,7 +70,9 @@ def test_kernel_selection_flags():
     one = [(n, s, p) for n, s, p in resnet50_layers(8) if n == "s3b2_1x1a"][0]
     assert L.kernel_name(one[2], one[1], torch.bfloat16).startswith("icv_igemm_smem<bf16,dense")
     assert L.kernel_name(one[2], one[1], torch.bfloat16, g) == "icv_igemm_smem<bf16>"
-    with L.tuning(dense_a=0):
+    with L.tuning(dense_a=0):   # (without the dense boxes the im2col TMA tiles serve a long-K 1x1 as well)
+        assert L.kernel_name(one[2], one[1], torch.bfloat16) == "icv_igemm_smem<bf16,im2col,pair>"
+    with L.tuning(dense_a=0, im2col_a=0):
         assert L.kernel_name(one[2], one[1], torch.bfloat16) == "icv_igemm_smem<bf16>"
 
 
