@@ -66,7 +66,24 @@ struct TcArgs {
   int64_t x_rows;            // dense A: pixel rows of the bound input
   // im2col A (use_tma_x == 2): output width, kernel width, strides, dilations, leading pads
   int32_t im_ow, im_s, im_sx, im_sy, im_dx, im_dy, im_pl, im_pt;
+  // uint8 im2col A: padded taps are zero-filled by TMA instead of holding the
+  // zero point; the epilogue adds the per-channel correction of the pixel's
+  // border class (row class x column class: which taps leave the image)
+  const int32_t* tapcorr;    // [RS][n_pad] zx * sum_c (w - zw) per (tap, channel); nullptr = no corrections
+  int32_t im_r, im_h, im_w, im_oh;
+  int32_t ncls, cls_tb, cls_ohb, cls_nr, cls_lb, cls_owb, cls_ncc;
 };
+
+// Border classes of an output row / column index v of n classes: the top
+// (left) prefix v < tb one class each, the bottom (right) suffix v >= ohb one
+// class each, everything between the single interior class n - 1; border_rep
+// gives a representative index of class k.
+__device__ __forceinline__ int border_class(int v, int tb, int ohb, int n) {
+  return v < tb ? v : (v >= ohb ? tb + v - ohb : n - 1);
+}
+__device__ __forceinline__ int border_rep(int k, int tb, int ohb, int n) {
+  return k < tb ? k : (k < n - 1 ? ohb + k - tb : tb);
+}
 
 // Where the references of output pixel p = tile_m*128 + row live: entry of
 // tap 0 (tap e adds e*mr; layout tile-major, kernel element, lane,
@@ -152,7 +169,8 @@ template <bool kI8, int BN, int kEpiWarps, int kAccStride, typename Sched = Stri
 __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane, uint32_t tmem_base, uint8_t* sEpi,
                                               const uint32_t* sBias, uint64_t* tfull, uint64_t* tempty,
                                               Sched sched = Sched{0}, const CUtensorMap* tmap_y = nullptr,
-                                              uint32_t tempty_remote = 0, const int32_t* smem_sums = nullptr) {
+                                              uint32_t tempty_remote = 0, const int32_t* smem_sums = nullptr,
+                                              const int32_t* cls_corr = nullptr) {
   constexpr int kOutRowBytes = kI8 ? 32 : 64;
   constexpr int kStageRowBytes = kI8 ? 48 : 80;  // padded: row-per-lane staging writes are conflict free
   const int slot = ew & 3;
@@ -225,6 +243,20 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
         tmem_ld_32x32b_x1(taddr + BN, rs);
         tmem_ld_wait();
         rowsum = (int32_t)rs;
+      }
+    }
+    // uint8 over zero-filled (im2col TMA) A tiles: this lane's pixel's border
+    // class selects the staged correction vector ([class][n_pad], smem)
+    const int32_t* my_corr = nullptr;
+    if constexpr (kI8) {
+      if (cls_corr != nullptr) {
+        int64_t p = row0 + lane;
+        p = p < a.P ? p : a.P - 1;
+        const int64_t n = p / a.ohw;
+        const int32_t r = (int32_t)(p - n * a.ohw);
+        const int32_t oy = r / a.im_ow, ox = r - oy * a.im_ow;
+        my_corr = cls_corr + (border_class(oy, a.cls_tb, a.cls_ohb, a.cls_nr) * a.cls_ncc +
+                              border_class(ox, a.cls_lb, a.cls_owb, a.cls_ncc)) * a.n_pad;
       }
     }
     const int cols_left = a.K - nt * BN - col0;
@@ -319,7 +351,11 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
         const uint32_t corr = 0u - (uint32_t)a.zw * (uint32_t)rowsum;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          const int4 b = cst4[q];
+          int4 b = cst4[q];
+          if (my_corr != nullptr) {
+            const int4 t = reinterpret_cast<const int4*>(my_corr + n)[q];
+            b.x += t.x; b.y += t.y; b.z += t.z; b.w += t.w;
+          }
           const int bb[4] = {b.x, b.y, b.z, b.w};
           uint32_t word = 0;
 #pragma unroll

@@ -111,19 +111,28 @@ struct CfgS {
 // slices, epilogue staging and constants leave of the 227 KB.
 struct PlanS {
   int slots, stages;
-  int off_b, off_ones, off_epi, off_bias, off_ib, off_bar, bytes;
+  int off_b, off_ones, off_epi, off_bias, off_ib, off_corr, off_bar, bytes;
   int res_b;   // dense A: filter blocks of this CTA's N tile kept resident (0 = streamed per stage)
 };
 
+// Border classes of a layer's output pixels (igemm_common.cuh border_class):
+// rows / columns whose receptive field leaves the image at the top (left) or
+// bottom (right) are one class each, the interior one class.
+struct BorderClasses {
+  int ncls, tb, ohb, nr, lb, owb, ncc;
+};
+bool im2col_u8_classes(const ConvArgs& c, BorderClasses* b);
+
 template <bool kI8, int BN, typename IbT, int kPair = 1, int kEpiW = kEpiWarpsS<kI8>>
-bool plan_smem(int rs, int n_pad, PlanS* p, int res_kb = 0) {
+bool plan_smem(int rs, int n_pad, PlanS* p, int res_kb = 0, int corr_bytes = 0) {
   using C = CfgS<kI8, BN, kPair, kEpiW, kIsDense<IbT>>;
   const int bias = (n_pad * 4 + 15) / 16 * 16;
   const int ib = kIsDense<IbT> ? 0 : 2 * rs * kBM * 4 + 2 * kBM * 4;   // int32 index slices + per-row bases
   // resident filter (dense A only): res_kb blocks of B, the ring holds A only
   const int res = res_kb * C::kBBytes;
   const int slot_bytes = res_kb ? kABytes : C::kSlotBytes;
-  const int fixed = 1024 + C::kOnesBytes + C::kEpiBytes + bias + ib + C::kBarBytes + res;
+  // (corr_bytes: uint8 im2col A -- border-class correction vectors, [classes][n_pad] int32)
+  const int fixed = 1024 + C::kOnesBytes + C::kEpiBytes + bias + ib + corr_bytes + C::kBarBytes + res;
   int slots = (232448 - fixed) / slot_bytes;
   slots = (slots > C::kMaxSlots ? C::kMaxSlots : slots) / C::kKB * C::kKB;
   if (slots < 2 * C::kKB) return false;
@@ -135,7 +144,8 @@ bool plan_smem(int rs, int n_pad, PlanS* p, int res_kb = 0) {
   p->off_epi = p->off_ones + C::kOnesBytes;
   p->off_bias = p->off_epi + C::kEpiBytes;
   p->off_ib = p->off_bias + bias;
-  p->off_bar = p->off_ib + ib;
+  p->off_corr = p->off_ib + ib;
+  p->off_bar = p->off_corr + corr_bytes;
   p->bytes = 1024 + p->off_bar + C::kBarBytes;
   return true;
 }
@@ -250,6 +260,7 @@ __global__ void __launch_bounds__(kThreadsK<kI8, BN, kCS, kEpiW>, 1) igemm_smem_
     }
   }
   for (int i = threadIdx.x; i < a.n_pad; i += blockDim.x) sBias[i] = __ldg(static_cast<const uint32_t*>(a.bias) + i);
+  int32_t* sCorr = reinterpret_cast<int32_t*>(smem + pl.off_corr);
   if (warp == kMmaWarpS<kI8, kEpiW>) {
     if constexpr (kCS == 2) tmem_alloc2<C::kTmemCols>(tmem_slot);
     else tmem_alloc<C::kTmemCols>(tmem_slot);
@@ -661,11 +672,38 @@ __global__ void __launch_bounds__(kThreadsK<kI8, BN, kCS, kEpiW>, 1) igemm_smem_
       if (++as == C::kAccStages) { as = 0; aphase ^= 1; }
     }
   } else {
+    // uint8 over zero-filled im2col tiles: per border class (row class x
+    // column class) the sum of the per-tap corrections zx * sum_c (w - zw) of
+    // the taps that leave the image there -- what those taps would have
+    // contributed had they read the zero point (the zero row) instead of TMA's
+    // zero fill.  Staged by the epilogue warps while the first tile's
+    // mainloop runs (off the producers' and the MMA's critical path).
+    if constexpr (kI8) {
+      if (a.ncls > 0) {
+        for (int i = threadIdx.x - 32 * kProdWarpsS<kI8>; i < a.ncls * a.n_pad; i += 32 * kEpiW) {
+          const int cl = i / a.n_pad, n = i - cl * a.n_pad;
+          const int oy = border_rep(cl / a.cls_ncc, a.cls_tb, a.cls_ohb, a.cls_nr);
+          const int ox = border_rep(cl % a.cls_ncc, a.cls_lb, a.cls_owb, a.cls_ncc);
+          int32_t sum = 0;
+          for (int ky = 0; ky < a.im_r; ++ky) {
+            const int iy = oy * a.im_sy - a.im_pt + ky * a.im_dy;
+            const bool row_out = iy < 0 || iy >= a.im_h;
+            for (int kx = 0; kx < a.im_s; ++kx) {
+              const int ix = ox * a.im_sx - a.im_pl + kx * a.im_dx;
+              if (row_out || ix < 0 || ix >= a.im_w) sum += __ldg(a.tapcorr + (int64_t)(ky * a.im_s + kx) * a.n_pad + n);
+            }
+          }
+          sCorr[i] = sum;
+        }
+        named_bar_sync(3, 32 * kEpiW);
+      }
+    }
     // a pair peer releases accumulators at the leader (which issues the next MMAs)
     const uint32_t tempty_remote = (kCS == 2 && crank != 0) ? mapa_rank(smem_u32(tempty), 0) : 0u;
     epilogue_loop<kI8, BN, kEpiW, C::kAccStride, std::remove_const_t<decltype(sched)>, C::kAccStages>(
         a, warp - kProdWarpsS<kI8>, lane, tmem_base, sEpi, sBias, tfull, tempty, sched, a.use_tma_y ? &tmap_y : nullptr,
-        tempty_remote, C::kSumWarps ? reinterpret_cast<const int32_t*>(sOnes) : nullptr);
+        tempty_remote, C::kSumWarps ? reinterpret_cast<const int32_t*>(sOnes) : nullptr,
+        (kI8 && a.ncls > 0) ? sCorr : nullptr);
   }
 
   tc_fence_before();
@@ -682,7 +720,12 @@ template <bool kI8, int BN, typename IbT, int kCS, int kEpiW>
 int launch_smem_cs(const ConvArgs& c, cudaStream_t st) {
   auto kernel = igemm_smem_kernel<kI8, BN, IbT, kCS, kEpiW>;
   PlanS pl;
-  if (!plan_smem<kI8, BN, IbT, kCS, kEpiW>(c.g.RS(), c.L.n_pad, &pl))
+  // uint8 im2col A: border-class correction vectors staged in smem
+  BorderClasses bc;
+  int corr_bytes = 0;
+  if constexpr (kI8 && kIsDense<IbT>)
+    if (tma_a_mode(c) == 2 && im2col_u8_classes(c, &bc)) corr_bytes = bc.ncls * c.L.n_pad * 4;
+  if (!plan_smem<kI8, BN, IbT, kCS, kEpiW>(c.g.RS(), c.L.n_pad, &pl, 0, corr_bytes))
     return fail(ICV_ERR_UNSUPPORTED, "indirection slice of this kernel size does not fit in shared memory");
   // dense A with few K blocks: keep the CTA's filter blocks resident (the
   // grid is then a multiple of the N-tile count, so every CTA keeps one N
@@ -694,7 +737,7 @@ int launch_smem_cs(const ConvArgs& c, cudaStream_t st) {
     const int n_tiles = c.L.n_pad / BN;
     PlanS pr;
     if (tune(kTuneDenseResB) > 0 && kbs * Cd::kBBytes <= tune(kTuneDenseResB) * 1024 && n_tiles <= 8 &&
-        plan_smem<kI8, BN, IbT, kCS, kEpiW>(1, c.L.n_pad, &pr, kbs) && pr.stages >= 4) {
+        plan_smem<kI8, BN, IbT, kCS, kEpiW>(1, c.L.n_pad, &pr, kbs, corr_bytes) && pr.stages >= 4) {
       pl = pr;
       grid_mult = n_tiles;
     }
@@ -718,6 +761,13 @@ int launch_smem_cs(const ConvArgs& c, cudaStream_t st) {
       if (int s = make_input_tmap_im2col(c, &tmap_x)) return fail(s, "im2col input tensor map");
       a.im_ow = (int32_t)c.g.OW; a.im_s = c.g.S; a.im_sx = c.g.SX; a.im_sy = c.g.SY;
       a.im_dx = c.g.DX; a.im_dy = c.g.DY; a.im_pl = c.g.PL; a.im_pt = c.g.PT;
+      a.im_r = c.g.R; a.im_h = (int32_t)c.g.H; a.im_w = (int32_t)c.g.W; a.im_oh = (int32_t)c.g.OH;
+      if (corr_bytes) {   // (uint8, zero row = zero point: TMA's zero fill needs the padded taps' corrections)
+        a.tapcorr = reinterpret_cast<const int32_t*>(c.packed + c.L.tapcorr_off);
+        a.ncls = bc.ncls;
+        a.cls_tb = bc.tb; a.cls_ohb = bc.ohb; a.cls_nr = bc.nr;
+        a.cls_lb = bc.lb; a.cls_owb = bc.owb; a.cls_ncc = bc.ncc;
+      }
     } else if (int s = make_input_tmap(c, &tmap_x)) {
       return fail(s, "dense-A input tensor map");
     }
@@ -905,15 +955,43 @@ int make_output_tmap(const ConvArgs& c, CUtensorMap* tmap, bool wide) {
 // A 1x1, stride-1, unpadded layer over a canonical buffer reads pixel row p
 // for output pixel p (indirect.py:112-125 with R = S = 1), so its A operand
 // is the dense [pixels][C] input matrix.
+namespace {
+bool im2col_u8_classes(const ConvArgs& c, BorderClasses* b) {
+  if (c.L.family != kFamTcU8 || c.L.tapcorr_off == 0) return false;
+  const Geom& g = c.g;
+  // top rows: tap row 0 above the image; bottom rows: the last tap row below it
+  const auto border = [](int64_t O, int64_t I, int P, int span, int st, int* tb, int* ohb, int* n) {
+    const int64_t t = std::min<int64_t>(O, (P + st - 1) / st);
+    const int64_t first_bot = std::max<int64_t>(0, (I + P - span + st) / st);   // ceil((I + P - span + 1) / st)
+    const int64_t b0 = std::max<int64_t>(t, std::min<int64_t>(O, first_bot));
+    *tb = (int)t; *ohb = (int)b0; *n = (int)(t + (O - b0) + 1);
+  };
+  border(g.OH, g.H, g.PT, (g.R - 1) * g.DY + 1, g.SY, &b->tb, &b->ohb, &b->nr);
+  border(g.OW, g.W, g.PL, (g.S - 1) * g.DX + 1, g.SX, &b->lb, &b->owb, &b->ncc);
+  b->ncls = b->nr * b->ncc;
+  return b->ncls >= 1 && (int64_t)b->ncls * c.L.n_pad * 4 <= 24576;
+}
+}  // namespace
+
 // im2col TMA A tiles (tma_a_mode 2).  The buffer must be canonical and the
 // zero row all zeros (padding = out-of-bounds zero fill); bf16 with whole
 // 128-byte channel blocks; corners / offsets inside the TMA encoding's 8-bit
 // fields (two spatial dimensions).
 bool im2col_a_eligible(const ConvArgs& c) {
   const Geom& g = c.g;
-  if (c.prefer_gather || !c.ib_canonical || !c.zero_known) return false;
-  if (c.L.family != kFamTcBf16) return false;
-  if ((reinterpret_cast<uintptr_t>(c.x) & 15) != 0 || (g.C * 2) % 128 != 0) return false;
+  if (c.prefer_gather || !c.ib_canonical) return false;
+  if (c.L.family == kFamTcU8) {
+    // zero row = input zero point: TMA's zero fill is corrected per border
+    // class in the epilogue (needs the packed per-tap corrections)
+    if (!c.zero_known) {
+      BorderClasses b;
+      if (!c.zero_is_zp || !im2col_u8_classes(c, &b)) return false;
+    }
+  } else if (c.L.family != kFamTcBf16 || !c.zero_known) {
+    return false;
+  }
+  const int eb = c.L.family == kFamTcU8 ? 1 : 2;
+  if ((reinterpret_cast<uintptr_t>(c.x) & 15) != 0 || (g.C * eb) % 128 != 0) return false;
   const int uw = g.PR - (g.S - 1) * g.DX, uh = g.PB - (g.R - 1) * g.DY;
   if (g.PL > 128 || g.PT > 128 || uw < -128 || uw > 127 || uh < -128 || uh > 127) return false;
   if ((g.S - 1) * g.DX >= 255 || (g.R - 1) * g.DY >= 255) return false;
@@ -944,7 +1022,7 @@ int tma_a_mode(const ConvArgs& c) {
   // 49.2, but 128 ch 3x3/2 77.9 -> 80.0: auto takes it from four channel
   // blocks up (knob im2col_a: 0 off, 1 auto, 2 wherever eligible).
   const int mode = tune(kTuneIm2colA);
-  if (mode && im2col_a_eligible(c) && (mode == 2 || c.L.cblocks >= 4)) return 2;
+  if (mode && im2col_a_eligible(c) && (mode == 2 || c.L.cblocks >= 4 || c.L.family == kFamTcU8)) return 2;
   return 0;
 }
 
@@ -990,13 +1068,15 @@ int make_input_tmap_im2col(const ConvArgs& c, CUtensorMap* tmap) {
   });
   if (!fn) return ICV_ERR_CUDA;
   const Geom& g = c.g;
-  const cuuint64_t eb = 2;
+  const bool i8 = c.L.family == kFamTcU8;
+  const cuuint64_t eb = i8 ? 1 : 2;
   const cuuint64_t dims[4] = {(cuuint64_t)g.C, (cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)g.N};
   const cuuint64_t strides[3] = {(cuuint64_t)g.C * eb, (cuuint64_t)g.W * g.C * eb, (cuuint64_t)g.H * g.W * g.C * eb};
   const int lower[2] = {-g.PL, -g.PT};
   const int upper[2] = {g.PR - (g.S - 1) * g.DX, g.PB - (g.R - 1) * g.DY};
   const cuuint32_t estr[4] = {1, (cuuint32_t)g.SX, (cuuint32_t)g.SY, 1};
-  CUresult cr = fn(tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(c.x), dims, strides, lower, upper,
+  CUresult cr = fn(tmap, i8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
+                   const_cast<void*>(c.x), dims, strides, lower, upper,
                    (cuuint32_t)(128 / eb), (cuuint32_t)kBM, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return ICV_ERR_CUDA;
@@ -1013,6 +1093,9 @@ void fill_tc_args(const ConvArgs& c, int block_n, TcArgs* a) {
   const bool i8 = c.L.family == kFamTcU8;
   a->use_tma_y = 0;
   a->dense_pf = 0;
+  a->tapcorr = nullptr;
+  a->ncls = 0;
+  a->im_ow = 1;
   a->epi_wide = 0;
   a->x_rows = c.g.N * c.g.H * c.g.W;
   a->tiles_per_row = 1;
@@ -1086,6 +1169,7 @@ const char* tc_kernel_name(const ConvArgs& c) {
   const bool i8 = c.L.family == kFamTcU8;
   if (win_kernel_eligible(c) && !im2col_over_window(c)) return i8 ? "icv_igemm_win<u8>" : "icv_igemm_win<bf16>";
   if (const int mode = use_clusters() ? 0 : tma_a_mode(c)) {
+    if (mode == 2 && i8) return dense_pair_wanted(c) ? "icv_igemm_smem<u8,im2col,pair>" : "icv_igemm_smem<u8,im2col>";
     if (mode == 2) return dense_pair_wanted(c) ? "icv_igemm_smem<bf16,im2col,pair>" : "icv_igemm_smem<bf16,im2col>";
     if (dense_pair_wanted(c)) return i8 ? "icv_igemm_smem<u8,dense,pair>" : "icv_igemm_smem<bf16,dense,pair>";
     return i8 ? "icv_igemm_smem<u8,dense>" : "icv_igemm_smem<bf16,dense>";

@@ -96,13 +96,7 @@ struct WinArgs {
   int32_t ncls, cls_tb, cls_ohb, cls_nr, cls_lb, cls_owb, cls_ncc;
 };
 
-// border class of output row / column v (top / bottom prefix and suffix, else interior = n - 1)
-__device__ __forceinline__ int border_class(int v, int tb, int ohb, int n) {
-  return v < tb ? v : (v >= ohb ? tb + v - ohb : n - 1);
-}
-__device__ __forceinline__ int border_rep(int k, int tb, int ohb, int n) {
-  return k < tb ? k : (k < n - 1 ? ohb + k - tb : tb);
-}
+// (border_class / border_rep: igemm_common.cuh)
 
 struct PlanW {
   int wstages, bslots;

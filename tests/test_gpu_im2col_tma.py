@@ -136,3 +136,62 @@ def test_im2col_tma_fallbacks(tune):
     ref1 = oconv.indirect_conv_f32(oconv.bf16_round(xh), np.full(p.in_channels, 0.5, np.float32), ib1.offsets_host(), p,
                                    oconv.bf16_round(wh), bias, shape.n, o.h, o.w)
     assert_bf16_close(y1.reshape(-1, p.out_channels), ref1.reshape(-1, p.out_channels))
+
+
+# ---------------------------------------------------------------- uint8
+# Zero row = input zero point (the QNNPACK convention): TMA zero-fills the
+# padded taps instead, and the epilogue adds, per border class of the pixel,
+# what those taps would have contributed.  Bit-exact against the quantized
+# oracle, which follows the buffer and the zero row.
+U8_GEOMS = [
+    (dict(r=3, s=3, sy=2, sx=2, pt=1, pl=1, c=256, k=256, n=3, h=28, w=28), 128, 127),      # cfg4 geometry: 2 x 2 classes
+    (dict(r=3, s=3, pt=1, pl=1, c=128, k=128, n=2, h=9, w=11), 3, 200),                     # stride 1: 3 x 3 classes
+    (dict(r=1, s=1, sy=2, sx=2, c=128, k=64, n=2, h=10, w=10), 7, 9),                       # strided 1x1: no padding
+    (dict(r=3, s=5, sy=2, sx=1, dy=2, dx=1, pt=2, pl=1, pb=3, pr=3, c=128, k=40, n=2, h=13, w=9), 128, 1),   # asymmetric
+    (dict(r=3, s=3, sy=2, sx=2, pt=1, pl=1, c=256, k=512, n=5, h=6, w=6), 255, 0),           # 3x3 outputs: every pixel a border pixel
+]
+
+
+def _u8_case(g, zx, zw, zero_fill):
+    from oracle import quant as oq
+
+    g = dict(g)
+    n, h, wd = g.pop("n"), g.pop("h"), g.pop("w")
+    p, shape = make_params(**g), icv.Shape4(n, h, wd, g["c"])
+    rng = np.random.default_rng(31)
+    xh = rng.integers(0, 256, shape.numel, dtype=np.uint8)
+    wh = rng.integers(0, 256, p.out_channels * p.kernel_elems * p.in_channels, dtype=np.uint8)
+    bias = rng.integers(-5000, 5000, p.out_channels, dtype=np.int32)
+    qp = icv.QuantParams(zx, 0.02, zw, 0.005, 128, 0.1)
+    tile = icv.TileConfig(mr=128)
+    x = icv.NhwcTensor(shape, torch.from_numpy(xh).to(DEV))
+    filt = icv.FilterTensor(p.out_channels, p.kernel_h, p.kernel_w, p.in_channels, torch.from_numpy(wh).to(DEV))
+    pf = icv.pack_filter(filt, torch.from_numpy(bias), p, tile, quant=qp)
+    zero = icv.make_zero_row(p.in_channels, dtype=torch.uint8, device=DEV, fill=zero_fill)
+    o = icv.conv_output_shape(p, shape)
+    ib = icv.init_indirection_buffer(x, zero, p, o, tile)
+    ref = oq.indirect_conv_u8(xh, zero.cpu().numpy(), ib.offsets_host(), p, wh, bias, shape.n, o.h, o.w,
+                              zx, 0.02, zw, 0.005, 128, 0.1)
+    return p, shape, x, pf, ib, tile, ref
+
+
+@pytest.mark.parametrize("cs", [1, 2])
+@pytest.mark.parametrize("geom,zx,zw", U8_GEOMS)
+def test_im2col_tma_u8_bit_exact(geom, zx, zw, cs, tune):
+    tune(dense_cs=cs)
+    p, shape, x, pf, ib, tile, ref = _u8_case(geom, zx, zw, zx)
+    name = L.kernel_name(p, shape, torch.uint8)
+    assert name == ("icv_igemm_smem<u8,im2col,pair>" if cs == 2 else "icv_igemm_smem<u8,im2col>"), name
+    y = icv.indirect_conv(x, pf, ib, p, tile).numpy().reshape(-1, p.out_channels)
+    assert np.array_equal(y, ref), int((y != ref).sum())
+    y_gather = icv.indirect_conv(x, pf, ib, p, tile, algorithm="gather").numpy().reshape(-1, p.out_channels)
+    assert np.array_equal(y_gather, ref)
+
+
+def test_im2col_tma_u8_other_zero_rows_keep_the_gather(tune):
+    """A uint8 zero row that is neither all zeros nor the zero point is followed through the buffer."""
+    g, zx, zw = U8_GEOMS[0]
+    p, shape, x, pf, ib, tile, ref = _u8_case(g, zx, zw, 77)
+    assert L.kernel_name(p, shape, torch.uint8, L.ICV_IB_CANONICAL | L.ICV_IB_PER_IMAGE) == "icv_igemm_smem<u8>"
+    y = icv.indirect_conv(x, pf, ib, p, tile).numpy().reshape(-1, p.out_channels)
+    assert np.array_equal(y, ref), int((y != ref).sum())

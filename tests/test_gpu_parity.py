@@ -359,7 +359,7 @@ def test_kernel_selection_is_native_tensor_core_for_baseline_configs():
     assert L.kernel_name(CFG2.params, CFG2.in_shape, torch.bfloat16).endswith("<bf16>")
     assert L.kernel_name(CFG3B.params, CFG3B.in_shape, torch.bfloat16).startswith("icv_igemm_")
     assert L.kernel_name(CFG4.params, CFG4.in_shape, torch.uint8).startswith("icv_igemm_")
-    assert L.kernel_name(CFG4.params, CFG4.in_shape, torch.uint8).endswith("<u8>")
+    assert L.kernel_name(CFG4.params, CFG4.in_shape, torch.uint8).startswith("icv_igemm_smem<u8")
     assert L.kernel_name(CFG1.params, CFG1.in_shape, torch.float32) == "icv_conv_f32_exact"
     before = L.launch_count()
     bf16_problem(CFG2, n_img=1)

@@ -121,6 +121,8 @@ def test_cfg4_window_selectable(tune):
     gather kernel is faster on cfg4 today)."""
     assert L.kernel_name(CFG4.params, CFG4.in_shape, torch.uint8) == "icv_igemm_win<u8>"
     tune(win=-1)
+    assert L.kernel_name(CFG4.params, CFG4.in_shape, torch.uint8) == "icv_igemm_smem<u8,im2col>"
+    tune(im2col_a=0)
     assert L.kernel_name(CFG4.params, CFG4.in_shape, torch.uint8) == "icv_igemm_smem<u8>"
 
 
