@@ -286,6 +286,7 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
           tmem_ld_32x32b_x32(taddr + c + 32, v1);
           tmem_ld_wait_regs(v0);
           tmem_ld_wait_regs(v1);
+          EP_ACC(1);
           uint32_t w[32];
           const float4* bias4 = reinterpret_cast<const float4*>(sBias + n);
 #pragma unroll
@@ -298,15 +299,18 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
             w[2 * q] = *reinterpret_cast<uint32_t*>(&lo);
             w[2 * q + 1] = *reinterpret_cast<uint32_t*>(&hi);
           }
+          EP_ACC(2);
           if (chunk_seq > 0) {
             if (lane == 0) bulk_wait_group_read<0>();
             __syncwarp();
           }
+          EP_ACC(5);
 #pragma unroll
           for (int q = 0; q < 8; ++q)
             sts128(sb + lane * 128 + ((q ^ (lane & 7)) << 4), w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
           fence_proxy_async_smem();
           __syncwarp();
+          EP_ACC(3);
           if (lane == 0) {
             if constexpr (kRowTiles)   // (channel, pixel in the output row, output row); pixels >= Wo clipped
               tma_store_3d(tmap_y, sb, n, rt_ox0, rt_row);
@@ -314,6 +318,7 @@ __device__ __forceinline__ void epilogue_loop(const TcArgs& a, int ew, int lane,
               tma_store_2d(tmap_y, sb, n, (int32_t)row0);
             bulk_commit_group();
           }
+          EP_ACC(4);
           ++chunk_seq;
         }
         done_wide = true;

@@ -195,3 +195,20 @@ def test_im2col_tma_u8_other_zero_rows_keep_the_gather(tune):
     assert L.kernel_name(p, shape, torch.uint8, L.ICV_IB_CANONICAL | L.ICV_IB_PER_IMAGE) == "icv_igemm_smem<u8>"
     y = icv.indirect_conv(x, pf, ib, p, tile).numpy().reshape(-1, p.out_channels)
     assert np.array_equal(y, ref), int((y != ref).sum())
+
+
+@pytest.mark.parametrize("geom", [
+    dict(r=3, s=3, pt=1, pl=1, c=256, k=256, n=64, h=14, w=14),                    # ResNet-50 s3 3x3 (instead of the window kernel)
+    dict(r=3, s=3, sy=2, sx=2, pt=1, pl=1, c=512, k=512, n=64, h=14, w=14),        # s4b1 3x3 / 2
+    dict(r=1, s=1, sy=2, sx=2, c=512, k=1024, n=32, h=28, w=28),                   # s3b1 projection
+])
+def test_im2col_tma_full_size_equals_gather(geom):
+    """ResNet-50 shapes at a batch where every CTA pair runs several tiles (the
+    stage ring wraps many times, odd tile counts leave a dummy tile): the
+    automatic plan takes the im2col pair kernel and agrees with the IB-gather
+    kernel byte for byte."""
+    p, shape, xh, wh, bias, x, pf, zero, ib, tile, o = _case(geom)
+    assert L.kernel_name(p, shape, torch.bfloat16) == "icv_igemm_smem<bf16,im2col,pair>"
+    y = icv.indirect_conv(x, pf, ib, p, tile).numpy()
+    y_gather = icv.indirect_conv(x, pf, ib, p, tile, algorithm="gather").numpy()
+    assert y.tobytes() == y_gather.tobytes()
