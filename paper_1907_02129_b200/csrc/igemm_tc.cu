@@ -17,10 +17,23 @@
 //              matching packed-filter block (B).
 //   warps 4-7  epilogue (igemm_common.cuh).
 //   warp 8     MMA: one elected lane issues 4 x tcgen05.mma per 128-byte K
-//              block into a TMEM accumulator (uint8 adds an N=16 MMA against
-//              an all-ones tile: the per-pixel input row sums needed by the
-//              zero-point correction); tcgen05.commit releases smem stages
-//              and publishes finished accumulators.
+//              block into a TMEM accumulator (uint8: 16 all-ones rows behind
+//              the filter rows of every B block make the same MMA, N = BN + 16,
+//              produce the per-pixel input row sums of the zero-point
+//              correction); tcgen05.commit releases smem stages and publishes
+//              finished accumulators.
+//
+// The same kernel runs two TMA-fed plans over a canonical buffer (IbT =
+// DenseA: no index slices, the producer warps' lane 0 issue tile loads):
+//   dense   1x1 stride-1 unpadded layers: the A tile is 128 consecutive pixel
+//           rows, one 2-D box per channel block;
+//   im2col  any geometry with an all-zero (uint8: zero-point) zero row: one
+//           im2col tile load per (tap, channel block), the TMA unit walks the
+//           128 output pixels and zero-fills padded taps (uint8: corrected per
+//           border class in the epilogue);
+// both also on CTA pairs (cta_group::2, M = 256: each member loads its own A
+// rows and half of every filter block, every load completes on the leader's
+// barrier).  Opt-in: uint8 BLOCK_N 256 with row-sum warps (knob u8_bn).
 #include <cstdio>
 #include <cstdlib>
 
