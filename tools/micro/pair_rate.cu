@@ -9,7 +9,11 @@
 #include "../../paper_1907_02129_b200/csrc/sm100_ptx.cuh"
 using namespace icv;
 
-template <int kMode, int kN>
+// kTraffic: warps 4.. of BOTH CTAs stream 16-byte st.shared (1) or ld.shared
+// (2) over a 64 KB scratch region while the MMAs run -- how much does other
+// shared-memory traffic (TMA fills, epilogue staging) slow the tensor core's
+// operand reads?  out[1] = bytes moved by CTA 0's traffic warps.
+template <int kMode, int kN, int kTraffic = 0>
 __global__ void __cluster_dims__(2, 1, 1) rate(int iters, unsigned long long* cyc) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -25,6 +29,47 @@ __global__ void __cluster_dims__(2, 1, 1) rate(int iters, unsigned long long* cy
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem = tslot;
+  if (kTraffic == 3 && threadIdx.x >= 128) {
+    // epilogue-like TMEM reads of the columns next to the accumulator while the MMAs run
+    const int w = threadIdx.x >> 5;
+    const uint32_t taddr = tmem + ((uint32_t)((w & 3) * 32) << 16) + kN;
+    unsigned long long n = 0;
+    uint32_t acc = 0;
+    while (!mbar_try_wait(&bar, 0)) {
+      for (int rep = 0; rep < 8; ++rep) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(taddr, v);
+        tmem_ld_wait_regs(v);
+        acc += v[0] + v[31];
+      }
+      n += 8;
+    }
+    if (acc == 0x12345678u) cyc[3] = acc;
+    if (rank == 0 && (threadIdx.x & 31) == 0) atomicAdd(cyc + 1, n);
+  } else
+  if (kTraffic && threadIdx.x >= 128) {
+    const uint32_t base = smem_u32(smem) + 131072 + (threadIdx.x - 128) * 16;
+    unsigned long long n = 0;
+    uint32_t acc = 0;
+    while (!mbar_try_wait(&bar, 0)) {
+      for (int rep = 0; rep < 16; ++rep) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const uint32_t addr = base + i * 4096;   // (<= 384 traffic threads: 6 KB per row of the sweep)
+          if (kTraffic == 1) {
+            asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(addr), "r"(acc) : "memory");
+          } else {
+            uint32_t x, y, z, w;
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(x), "=r"(y), "=r"(z), "=r"(w) : "r"(addr) : "memory");
+            acc += x + y + z + w;
+          }
+        }
+      }
+      n += 16 * 16 * 16;
+    }
+    if (acc == 0x12345678u) cyc[3] = acc;
+    if (rank == 0) atomicAdd(cyc + 1, n);
+  } else
   if (rank == 0 && threadIdx.x < 32) {
     const uint32_t a_addr = smem_u32(smem), b_addr = smem_u32(smem + 65536);
     const uint64_t ad0 = sw128_kmajor_desc(a_addr), bd0 = sw128_kmajor_desc(b_addr);
@@ -78,6 +123,23 @@ __global__ void __cluster_dims__(2, 1, 1) rate(int iters, unsigned long long* cy
   if (threadIdx.x < 32) { tc_fence_after(); tmem_dealloc2<256>(tmem); }
 }
 
+template <int kMode, int kN, int kTraffic>
+void run_traffic(unsigned long long* d, int warps) {
+  cudaFuncSetAttribute(rate<kMode, kN, kTraffic>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+  cudaMemset(d, 0, 32);
+  rate<kMode, kN, kTraffic><<<2, 128 + 32 * warps, 205 * 1024>>>(36000, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) { printf("traffic: %s\n", cudaGetErrorString(e)); return; }
+  unsigned long long c[2];
+  cudaMemcpy(c, d, 16, cudaMemcpyDeviceToHost);
+  if (kTraffic == 3)
+    printf("pair M256 N%d K steps + %d warps of tcgen05.ld.x32 per CTA: %6.1f cycles per MMA (ideal %d), %6.1f cycles per load per warp\n",
+           kN, warps, c[0] / 36000.0, kN / 2, (double)c[0] * warps / (double)c[1]);
+  else
+  printf("pair M256 N%d K steps + %d warps of %s.shared.v4 per CTA: %6.1f cycles per MMA (ideal %d), traffic %5.1f B/cycle/SM\n",
+         kN, warps, kTraffic == 1 ? "st" : "ld", c[0] / 36000.0, kN / 2, (double)c[1] / (double)c[0]);
+}
+
 template <int kMode, int kN>
 void run(unsigned long long* d) {
   cudaFuncSetAttribute(rate<kMode, kN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
@@ -92,9 +154,15 @@ void run(unsigned long long* d) {
 
 int main() {
   unsigned long long* d;
-  cudaMalloc(&d, 8);
+  cudaMalloc(&d, 64);
   run<0, 128>(d); run<1, 128>(d); run<2, 128>(d); run<3, 128>(d);
   run<0, 256>(d); run<1, 256>(d);
   run<0, 64>(d); run<1, 64>(d); run<2, 64>(d);
+  for (int w : {1, 2, 4, 8, 12}) run_traffic<1, 128, 1>(d, w);
+  for (int w : {1, 2, 4, 8, 12}) run_traffic<1, 128, 2>(d, w);
+  for (int w : {4, 12}) run_traffic<1, 256, 1>(d, w);
+  for (int w : {4, 12}) run_traffic<1, 64, 1>(d, w);
+  for (int w : {4, 8}) run_traffic<1, 128, 3>(d, w);
+  for (int w : {4, 8}) run_traffic<1, 64, 3>(d, w);
   return 0;
 }
