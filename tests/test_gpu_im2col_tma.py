@@ -212,3 +212,17 @@ def test_im2col_tma_full_size_equals_gather(geom):
     y = icv.indirect_conv(x, pf, ib, p, tile).numpy()
     y_gather = icv.indirect_conv(x, pf, ib, p, tile, algorithm="gather").numpy()
     assert y.tobytes() == y_gather.tobytes()
+
+
+def test_im2col_tma_random_geometries():
+    """Randomized sweep (tools/fuzz_im2col.py): 150 random geometries, bf16 and
+    uint8, single CTAs and pairs, all equal to the IB-gather kernel."""
+    import os
+    import sys
+
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import fuzz_im2col
+
+    ran, bad = fuzz_im2col.run(150, 7)
+    assert bad == 0
+    assert ran["bf16"] >= 150 and ran["u8"] >= 80
